@@ -1,0 +1,30 @@
+#!/usr/bin/env bash
+# Builds the CPU oracle from the reference's OWN sources, unmodified, straight
+# from the read-only tree (never copied into this repo):
+#   /root/reference/proj/src/{matrix,quant,stats,layerwise}.cpp
+# against our from-scratch Eigen-API shim (paper_2603_28845_b200/compat) and
+# doctest shim (oracle/shim).  Outputs go to oracle/_ref/ only (git-ignored,
+# travels to the GPU box with the snapshot):
+#   oracle/_ref/libocw_ref.so        reference hot path + oracle/ref_capi.cpp C entry points
+#   oracle/_ref/ref_test_core        proj/tests/test_core.cpp      (unmodified)
+#   oracle/_ref/ref_test_layerwise   proj/tests/test_layerwise.cpp (unmodified)
+# container.cpp / pipeline.cpp need nlohmann/json (absent) and are not built;
+# the packer is restated in oracle/ocw_oracle.py (container.cpp:15-35,129-139).
+set -euo pipefail
+REF=${OCW_REFERENCE:-/root/reference/proj}
+HERE="$(cd "$(dirname "${BASH_SOURCE[0]}")" && pwd)"
+ROOT="$(dirname "$HERE")"
+OUT="$HERE/_ref"
+if [ ! -d "$REF/src" ]; then
+  echo "build_ref: $REF not present; skipping (prebuilt oracle/_ref is used if shipped)" >&2
+  exit 0
+fi
+mkdir -p "$OUT"
+CXX=${CXX:-g++}
+FLAGS="-std=c++20 -O2 -fPIC -Wall -Wextra -Wno-unused-parameter -I$REF/include -I$ROOT/paper_2603_28845_b200/compat -I$HERE/shim"
+SRCS="$REF/src/matrix.cpp $REF/src/quant.cpp $REF/src/stats.cpp $REF/src/layerwise.cpp"
+$CXX $FLAGS -shared -o "$OUT/libocw_ref.so" $SRCS "$HERE/ref_capi.cpp" -ldl
+for t in test_core test_layerwise; do
+  $CXX $FLAGS -o "$OUT/ref_$t" "$REF/tests/test_main.cpp" "$REF/tests/$t.cpp" $SRCS -ldl
+done
+echo "build_ref: built $OUT/{libocw_ref.so,ref_test_core,ref_test_layerwise}"
