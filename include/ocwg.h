@@ -1,0 +1,187 @@
+/*
+ * ocwg.h -- C ABI of the B200 (sm_100a) GPTQ layer-quantize library
+ * (libocwg.so).  Drop-in boundary for the OneComp "ocw" reference's hot path.
+ *
+ * Every entry point replaces one reference C++ function of the layer-wise PTQ
+ * path (citations are /root/reference/proj/...); the C++ drop-in
+ * (paper_2603_28845_b200/cpp/ocw_dropin.cpp) re-exposes them under the
+ * reference's own `ocw::` signatures, and the Python host mirror
+ * (paper_2603_28845_b200/__init__.py) binds them with ctypes.
+ *
+ * Conventions
+ *   - Orientation is the reference's: W is N x M with N = INPUT rows and
+ *     M = OUTPUT columns (model.hpp:14); H is N x N; X is T x N (tokens x in).
+ *     All matrices are dense row-major.
+ *   - Status codes mirror the reference's exception classes and CLI exit codes
+ *     (errors.hpp:9-21, ocw_cli.cpp:9-12): OCWG_INVALID_INPUT == invalid_input,
+ *     OCWG_NUMERIC_ERROR == numeric_error; CUDA failures are >= 16.  No C++
+ *     exception crosses the ABI; ocwg_last_error() holds the message
+ *     (thread-local).
+ *   - Host-pointer entry points are synchronous (value semantics, like the
+ *     reference).  *_dev entry points take DEVICE pointers, run on the
+ *     context's stream and return after the stream has drained.
+ *   - Grids are passed structure-of-arrays: scales (fp32 value of the
+ *     reference-fp16-rounded scale) and int32 zero points, in group-index order
+ *     (QuantizedMatrix::grids, quant.hpp:54-63).  qmin/qmax follow from the config.
+ *   - No CPU fallback: every compute entry point runs CUDA kernels; a missing
+ *     or unusable GPU is reported as OCWG_CUDA_ERROR.
+ */
+#ifndef OCWG_H
+#define OCWG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OCWG_OK 0
+#define OCWG_INVALID_INPUT 1 /* ocw::invalid_input */
+#define OCWG_IO_ERROR 2      /* ocw::io_error      */
+#define OCWG_NUMERIC_ERROR 3 /* ocw::numeric_error */
+#define OCWG_CUDA_ERROR 16
+#define OCWG_UNSUPPORTED 17
+
+/* quant.hpp:12-14 */
+#define OCWG_SYMMETRIC 0
+#define OCWG_ASYMMETRIC 1
+#define OCWG_PER_TENSOR 0
+#define OCWG_PER_CHANNEL 1
+#define OCWG_PER_GROUP 2
+#define OCWG_MINMAX 0
+#define OCWG_MSE_GRID 1
+
+/* QuantConfig (quant.hpp:21-28) */
+typedef struct ocwg_quant_config {
+  int32_t bits;        /* [1, 8] */
+  int32_t scheme;      /* OCWG_SYMMETRIC / OCWG_ASYMMETRIC */
+  int32_t granularity; /* OCWG_PER_TENSOR / _CHANNEL / _GROUP */
+  int32_t reserved;
+  uint64_t group_size; /* per_group only; short final group allowed */
+} ocwg_quant_config;
+
+/* GptqOptions (layerwise.hpp:11-15) */
+typedef struct ocwg_gptq_options {
+  int32_t actorder;    /* stable sort by descending diag(H) */
+  int32_t reserved;
+  double percdamp;     /* (0, 1] */
+  uint64_t block_cols; /* lazy-update block (reference default 32) */
+} ocwg_gptq_options;
+
+typedef struct ocwg_ctx ocwg_ctx;
+
+/* ---- library / context ------------------------------------------------ */
+const char* ocwg_last_error(void);
+int ocwg_version(void);
+/* Context on one CUDA device: stream, workspace pool, device status word. */
+int ocwg_create(int device, ocwg_ctx** out);
+int ocwg_destroy(ocwg_ctx* ctx);
+/* Run subsequent work on an external cudaStream_t (NULL = the context's own). */
+int ocwg_set_stream(ocwg_ctx* ctx, void* cuda_stream);
+int ocwg_synchronize(ocwg_ctx* ctx);
+
+/* ---- quant.hpp --------------------------------------------------------- */
+/* QuantConfig::validate (quant.cpp:19-25) */
+int ocwg_validate_config(const ocwg_quant_config* cfg);
+/* quant_group_count (quant.cpp:151-154) */
+uint64_t ocwg_group_count(const ocwg_quant_config* cfg, uint64_t rows, uint64_t cols);
+/* uniform_storage_bytes (quant.cpp:220-224) */
+uint64_t ocwg_storage_bytes(const ocwg_quant_config* cfg, uint64_t rows, uint64_t cols);
+/* calibrate_grids (quant.cpp:168-196) */
+int ocwg_calibrate_grids(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t cols,
+                         const ocwg_quant_config* cfg, int scale_mode, float* scales,
+                         int32_t* zeros);
+/* quantize_matrix (quant.cpp:198-210): codes int16 row-major */
+int ocwg_quantize_matrix(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t cols,
+                         const ocwg_quant_config* cfg, int scale_mode, int16_t* codes,
+                         float* scales, int32_t* zeros);
+/* dequantize (quant.cpp:212-218) */
+int ocwg_dequantize(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
+                    const int32_t* zeros, uint64_t rows, uint64_t cols,
+                    const ocwg_quant_config* cfg, float* out);
+/* activation_objective (quant.cpp:230-236): tr((W_hat - W)^T H (W_hat - W)) */
+int ocwg_activation_objective(ocwg_ctx* ctx, const float* w, const float* w_hat, const float* h,
+                              uint64_t n, uint64_t m, double* out);
+
+/* ---- OCW1 uniform payload (container.cpp:15-35, 66-70, 129-139, 168-199) */
+/* out_len must be >= ocwg_storage_bytes(); exactly that many bytes are written */
+int ocwg_pack_uniform(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
+                      const int32_t* zeros, uint64_t rows, uint64_t cols,
+                      const ocwg_quant_config* cfg, uint8_t* out, uint64_t out_len);
+int ocwg_unpack_uniform(ocwg_ctx* ctx, const uint8_t* payload, uint64_t len, uint64_t rows,
+                        uint64_t cols, const ocwg_quant_config* cfg, int16_t* codes,
+                        float* scales, int32_t* zeros);
+
+/* ---- stats.hpp --------------------------------------------------------- */
+/* accumulate_stats (stats.cpp:10-19): gram += Xp^T Xp; cross += Xp^T (X - Xp),
+ * fp64 n x n row-major, updated in place; cross may be NULL when
+ * x_fp == x_pert (then cross is identically 0, test_core.cpp:273-279). */
+int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert, uint64_t rows,
+                          uint64_t dim, double* gram, double* cross, uint64_t* token_count);
+/* Hessian of bf16 calibration tokens on the tensor cores: H (+)= X^T X.
+ * x: T x N bf16 bits (uint16), h: N x N fp32.  (stats.cpp:16 for bf16 X) */
+int ocwg_hessian_bf16(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, uint64_t dim, float* h,
+                      int accumulate);
+
+/* ---- layerwise.hpp ----------------------------------------------------- */
+/* gptq_order (layerwise.cpp:11-18) */
+int ocwg_gptq_order(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, int64_t* order);
+/* gptq_quantize (layerwise.cpp:20-93).  w_hat (N x M dequantized) may be NULL. */
+int ocwg_gptq_quantize(ocwg_ctx* ctx, const float* w, const float* h, uint64_t n, uint64_t m,
+                       const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
+                       int scale_mode, int16_t* codes, float* scales, int32_t* zeros,
+                       float* w_hat);
+/* Parity artefacts of layerwise.cpp:29-51: processing order, damp, the
+ * dampened permuted inverse hinv = H_p^-1 and its upper factor U (each
+ * output may be NULL; hinv/u are N x N fp64 row-major, processing order). */
+int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, double percdamp,
+                     int64_t* order, double* hinv, double* u, double* damp);
+/* quantize_layer (layerwise.cpp:120-126) over fp64 stats (gram N x N);
+ * method: 0 rtn, 1 gptq.  QEP (qep != 0) is reserved: OCWG_UNSUPPORTED. */
+int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, uint64_t n, uint64_t m,
+                        int method, const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
+                        int scale_mode, int qep, int16_t* codes, float* scales, int32_t* zeros,
+                        float* w_hat);
+
+/* ---- end-to-end layer quantize from calibration tokens (north_star call) --
+ * W (N x M fp32) + X (T x N bf16) -> codes, grids, dequantized W and the
+ * packed OCW1 payload.  Any output may be NULL.  h_out (N x N fp32) returns
+ * the Hessian X^T X (unnormalised, as stats.cpp:16). */
+int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint64_t tokens,
+                          uint64_t n, uint64_t m, const ocwg_quant_config* cfg,
+                          const ocwg_gptq_options* opts, int scale_mode, int16_t* codes,
+                          float* scales, int32_t* zeros, float* w_hat, uint8_t* payload,
+                          uint64_t payload_len, float* h_out);
+/* Same with every pointer in device memory (inputs resident in HBM). */
+int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint64_t tokens,
+                              uint64_t n, uint64_t m, const ocwg_quant_config* cfg,
+                              const ocwg_gptq_options* opts, int scale_mode, int16_t* codes,
+                              float* scales, int32_t* zeros, float* w_hat, uint8_t* payload,
+                              float* h_out);
+/* Device-pointer pieces, for sharded use (Hessian token shards + all-reduce,
+ * then GPTQ on a column slab of W).  w is N x M with row stride ldw (>= M),
+ * so a column slab of a larger W is passed as (w + j0, m = slab, ldw = M);
+ * codes / w_hat use the same row stride ldw; scales / zeros are the slab's own
+ * grids (N x ceil(m/G) for per-group). */
+int ocwg_hessian_bf16_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, uint64_t dim,
+                          float* h, int accumulate);
+int ocwg_gptq_quantize_dev(ocwg_ctx* ctx, const float* w, uint64_t ldw, const float* h,
+                           uint64_t n, uint64_t m, const ocwg_quant_config* cfg,
+                           const ocwg_gptq_options* opts, int scale_mode, int16_t* codes,
+                           float* scales, int32_t* zeros, float* w_hat);
+int ocwg_pack_uniform_dev(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
+                          const int32_t* zeros, uint64_t rows, uint64_t cols,
+                          const ocwg_quant_config* cfg, uint8_t* out);
+
+/* ---- test / profiling hooks -------------------------------------------- */
+/* impl: 0 = tcgen05 kernel (product), 1 = SIMT fp64-accumulate cross-check */
+int ocwg_debug_hessian_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, uint64_t dim,
+                           float* h, int accumulate, int impl);
+/* Number of kernels this library launched on the context so far. */
+uint64_t ocwg_launch_count(ocwg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCWG_H */

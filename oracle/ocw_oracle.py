@@ -227,6 +227,15 @@ def group_index_matrix(cfg: QuantConfig, rows: int, cols: int) -> np.ndarray:
 # --------------------------------------------------------------------------
 
 
+def _ref_int(x) -> np.ndarray:
+    """int(std::nearbyint(x)) as built for x86-64: ties-to-even, and the
+    float->int conversion (cvttss2si) yields INT_MIN for NaN / |x| >= 2^31."""
+    with np.errstate(invalid="ignore"):
+        r = np.rint(np.asarray(x, dtype=np.float32))
+        ok = (r >= np.float32(-2.0**31)) & (r < np.float32(2.0**31))
+    return np.where(ok, np.where(ok, r, 0), -(2**31)).astype(np.int64)
+
+
 def quantize_scalar(w, scale, zero, qmin, qmax):
     """code = clamp(int(nearbyint(w / s)) + z, qmin, qmax); w_hat = s * float(code - z).
 
@@ -235,9 +244,7 @@ def quantize_scalar(w, scale, zero, qmin, qmax):
     w = np.asarray(w, dtype=np.float32)
     scale = np.asarray(scale, dtype=np.float32)
     with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
-        r = np.rint(w / scale)
-    # int(...) of an out-of-range float is UB in C++; saturate instead.
-    r = np.clip(r, -2.0**31, 2.0**31 - 1).astype(np.int64)
+        r = _ref_int((w / scale).astype(np.float32))
     code = np.clip(r + np.asarray(zero, dtype=np.int64), qmin, qmax)
     w_hat = (scale * (code - np.asarray(zero, dtype=np.int64)).astype(np.float32)).astype(np.float32)
     return code, w_hat
@@ -265,8 +272,8 @@ def _from_extremes(lo: np.ndarray, hi: np.ndarray, bits: int, scheme: Scheme):
         with np.errstate(all="ignore"):
             s = positive_fp16((hi - lo) / np.float32(qmax - qmin))
             s = np.where(degen, np.float32(1.0), s).astype(np.float32)
-            zf = np.where(degen, np.float32(qmin) - lo, np.float32(qmin) - lo / s)
-        z = np.clip(np.clip(np.rint(zf), -2.0**31, 2.0**31 - 1).astype(np.int64), qmin, qmax)
+            zf = np.where(degen, np.float32(qmin) - lo, np.float32(qmin) - lo / s).astype(np.float32)
+        z = np.clip(_ref_int(zf), qmin, qmax)
         return s, z.astype(np.int32)
     amax = np.maximum(np.abs(lo), np.abs(hi)).astype(np.float32)
     s = np.where(amax == 0, np.float32(1.0), positive_fp16(amax / np.float32(qmax))).astype(np.float32)
@@ -300,8 +307,8 @@ def _mse_refine(vals: np.ndarray, valid: np.ndarray, lo, hi, s0, z0, bits, schem
         s = positive_fp16((mult * raw).astype(np.float32))
         if scheme == Scheme.asymmetric:
             with np.errstate(all="ignore"):
-                zf = np.float32(qmin) - lo / s
-            z = np.clip(np.clip(np.rint(zf), -2.0**31, 2.0**31 - 1).astype(np.int64), qmin, qmax).astype(np.int32)
+                zf = (np.float32(qmin) - lo / s).astype(np.float32)
+            z = np.clip(_ref_int(zf), qmin, qmax).astype(np.int32)
         else:
             z = np.zeros_like(z0)
         e = _ordered_sum_sq(vals, valid, s, z, qmin, qmax)
@@ -683,3 +690,17 @@ def random_gaussian(rows: int, cols: int, seed: int, stddev: float = 1.0) -> np.
 
 def identity(n: int) -> np.ndarray:
     return np.eye(n, dtype=np.float32)
+
+
+def bf16_round(x) -> np.ndarray:
+    """fp32 -> nearest bf16 (ties-to-even) -> fp32; the BASELINE configs draw X
+    this way ("each value rounded to bf16")."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32).reshape(np.shape(x))
+
+
+def bf16_bits(x) -> np.ndarray:
+    """fp32 -> bf16 bit patterns (uint16), ties-to-even."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16).reshape(np.shape(x))

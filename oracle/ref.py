@@ -1,0 +1,197 @@
+"""ctypes wrapper over oracle/_ref/libocw_ref.so -- the reference's own hot-path
+sources (proj/src/{quant,stats,layerwise,matrix}.cpp) compiled unmodified by
+oracle/build_ref.sh, plus oracle/ref_capi.cpp.
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's CPU-baseline / --impl reference arm.  The product package never
+imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "_ref" / "libocw_ref.so"
+_P, _U64, _I = C.c_void_p, C.c_uint64, C.c_int
+
+_SIGS = {
+    "ocwref_last_error": (C.c_char_p, []),
+    "ocwref_blas_name": (C.c_char_p, []),
+    "ocwref_set_threads": (None, [_I]),
+    "ocwref_group_count": (_U64, [_I, _I, _I, _U64, _U64, _U64]),
+    "ocwref_storage_bytes": (_U64, [_I, _I, _I, _U64, _U64, _U64]),
+    "ocwref_random_gaussian": (_I, [_U64, _U64, _U64, C.c_float, _P]),
+    "ocwref_calibrate_grids": (_I, [_P, _U64, _U64, _I, _I, _I, _U64, _I, _P, _P]),
+    "ocwref_quantize_matrix": (_I, [_P, _U64, _U64, _I, _I, _I, _U64, _I, _P, _P, _P]),
+    "ocwref_dequantize": (_I, [_P, _P, _P, _U64, _U64, _I, _I, _I, _U64, _P]),
+    "ocwref_activation_objective": (_I, [_P, _P, _P, _U64, _U64, _P]),
+    "ocwref_gptq_order": (_I, [_P, _U64, _I, _P]),
+    "ocwref_gptq_quantize": (_I, [_P, _P, _U64, _U64, _I, _I, _I, _U64, _I, C.c_double, _U64, _I,
+                                  _P, _P, _P, _P]),
+    "ocwref_gptq_factor": (_I, [_P, _U64, _I, C.c_double, _P, _P, _P]),
+    "ocwref_accumulate_stats": (_I, [_P, _P, _U64, _U64, _P, _P, _P, _P]),
+    "ocwref_qep_target": (_I, [_P, _P, _P, _U64, _U64, C.c_double, C.c_double, _P]),
+    "ocwref_quantize_layer": (_I, [_P, _P, _P, _U64, _U64, _I, _I, _I, _I, _U64, _I, _I, C.c_double,
+                                   _U64, _I, C.c_double, C.c_double, _P, _P, _P]),
+}
+
+_lib = None
+
+
+class RefError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{status}] {msg}")
+        self.status = status
+
+
+def available() -> bool:
+    return LIB.exists()
+
+
+def build() -> None:
+    subprocess.run(["bash", str(HERE / "build_ref.sh")], check=True)
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB.exists():
+            build()
+        l = C.CDLL(str(LIB))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(l, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def _ck(st: int) -> None:
+    if st != 0:
+        raise RefError(st, lib().ocwref_last_error().decode())
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, np.float32)
+
+
+def random_gaussian(rows: int, cols: int, seed: int, stddev: float = 1.0) -> np.ndarray:
+    """matrix.cpp:57-62 (the reference's seeded fixture generator)."""
+    out = np.zeros((rows, cols), np.float32)
+    _ck(lib().ocwref_random_gaussian(rows, cols, seed, stddev, _p(out)))
+    return out
+
+
+def group_count(bits, scheme, gran, group, rows, cols) -> int:
+    return int(lib().ocwref_group_count(bits, scheme, gran, group, rows, cols))
+
+
+def storage_bytes(bits, scheme, gran, group, rows, cols) -> int:
+    return int(lib().ocwref_storage_bytes(bits, scheme, gran, group, rows, cols))
+
+
+def calibrate_grids(w, bits, scheme, gran, group, mse=False):
+    w = _f32(w)
+    ng = group_count(bits, scheme, gran, group, *w.shape)
+    s, z = np.zeros(ng, np.float32), np.zeros(ng, np.int32)
+    _ck(lib().ocwref_calibrate_grids(_p(w), w.shape[0], w.shape[1], bits, scheme, gran, group,
+                                     int(mse), _p(s), _p(z)))
+    return s, z
+
+
+def quantize_matrix(w, bits, scheme, gran, group, mse=False):
+    w = _f32(w)
+    ng = group_count(bits, scheme, gran, group, *w.shape)
+    codes = np.zeros(w.shape, np.int16)
+    s, z = np.zeros(ng, np.float32), np.zeros(ng, np.int32)
+    _ck(lib().ocwref_quantize_matrix(_p(w), w.shape[0], w.shape[1], bits, scheme, gran, group,
+                                     int(mse), _p(codes), _p(s), _p(z)))
+    return codes, s, z
+
+
+def dequantize(codes, s, z, bits, scheme, gran, group):
+    codes = np.ascontiguousarray(codes, np.int16)
+    out = np.zeros(codes.shape, np.float32)
+    _ck(lib().ocwref_dequantize(_p(codes), _p(_f32(s)), _p(np.ascontiguousarray(z, np.int32)),
+                                codes.shape[0], codes.shape[1], bits, scheme, gran, group, _p(out)))
+    return out
+
+
+def activation_objective(w, w_hat, h) -> float:
+    w, w_hat, h = _f32(w), _f32(w_hat), _f32(h)
+    out = C.c_double()
+    _ck(lib().ocwref_activation_objective(_p(w), _p(w_hat), _p(h), w.shape[0], w.shape[1],
+                                          C.byref(out)))
+    return out.value
+
+
+def gptq_order(h, actorder: bool) -> np.ndarray:
+    h = _f32(h)
+    out = np.zeros(h.shape[0], np.int64)
+    _ck(lib().ocwref_gptq_order(_p(h), h.shape[0], int(actorder), _p(out)))
+    return out
+
+
+def gptq_quantize(w, h, bits, scheme, gran, group, actorder=False, percdamp=0.01, block=32,
+                  mse=False, timing=False):
+    w, h = _f32(w), _f32(h)
+    n, m = w.shape
+    ng = group_count(bits, scheme, gran, group, n, m)
+    codes = np.zeros((n, m), np.int16)
+    s, z = np.zeros(ng, np.float32), np.zeros(ng, np.int32)
+    sec = C.c_double()
+    _ck(lib().ocwref_gptq_quantize(_p(w), _p(h), n, m, bits, scheme, gran, group, int(actorder),
+                                   percdamp, block, int(mse), _p(codes), _p(s), _p(z),
+                                   C.byref(sec)))
+    return (codes, s, z, sec.value) if timing else (codes, s, z)
+
+
+def gptq_factor(h, actorder=False, percdamp=0.01):
+    h = _f32(h)
+    n = h.shape[0]
+    hinv, u = np.zeros((n, n)), np.zeros((n, n))
+    damp = C.c_double()
+    _ck(lib().ocwref_gptq_factor(_p(h), n, int(actorder), percdamp, _p(hinv), _p(u), C.byref(damp)))
+    return hinv, u, damp.value
+
+
+def accumulate_stats(gram, cross, x_fp, x_pert, token_count=0, timing=False):
+    """In-place on fp64 gram/cross (row-major)."""
+    x_fp, x_pert = _f32(x_fp), _f32(x_pert)
+    tc = C.c_uint64(token_count)
+    sec = C.c_double()
+    _ck(lib().ocwref_accumulate_stats(_p(x_fp), _p(x_pert), x_fp.shape[0], x_fp.shape[1], _p(gram),
+                                      _p(cross), C.byref(tc), C.byref(sec)))
+    return (int(tc.value), sec.value) if timing else int(tc.value)
+
+
+def quantize_layer(w, gram, cross, method_gptq, bits, scheme, gran, group, mse=False,
+                   actorder=False, percdamp=0.01, block=32, qep=None):
+    w = _f32(w)
+    n, m = w.shape
+    ng = group_count(bits, scheme, gran, group, n, m)
+    codes = np.zeros((n, m), np.int16)
+    s, z = np.zeros(ng, np.float32), np.zeros(ng, np.int32)
+    alpha, eta = qep if qep is not None else (1.0, 0.01)
+    _ck(lib().ocwref_quantize_layer(_p(w), _p(np.ascontiguousarray(gram, np.float64)),
+                                    _p(None if cross is None else np.ascontiguousarray(cross, np.float64)),
+                                    n, m, int(method_gptq), bits, scheme, gran, group, int(mse),
+                                    int(actorder), percdamp, block, int(qep is not None), alpha, eta,
+                                    _p(codes), _p(s), _p(z)))
+    return codes, s, z
+
+
+def set_threads(n: int) -> None:
+    lib().ocwref_set_threads(int(n))
+
+
+def blas_name() -> str:
+    return lib().ocwref_blas_name().decode()

@@ -47,7 +47,7 @@ int guard(F&& f) {
 
 ocw::Matrix to_matrix(const float* p, size_t rows, size_t cols) {
   ocw::Matrix m(rows, cols);
-  if (rows * cols) std::memcpy(m.data.data(), p, rows * cols * sizeof(float));
+  if (rows * cols != 0) std::memcpy(m.data.data(), p, rows * cols * sizeof(float));
   return m;
 }
 

@@ -1,0 +1,476 @@
+"""B200-native GPTQ layer-quantize hot path of OneComp (arXiv 2603.28845).
+
+Python host mirror of the reference's ``ocw::`` quantizer interface
+(/root/reference/proj/include/ocw/{quant,stats,layerwise}.hpp), bound with
+ctypes to the C ABI of ``lib/libocwg.so`` (``include/ocwg.h``).  Same names,
+same argument meaning, same error classes as the reference:
+
+    ocw::calibrate_grids   -> calibrate_grids        (quant.cpp:168-196)
+    ocw::quantize_matrix   -> quantize_matrix        (quant.cpp:198-210)
+    ocw::dequantize        -> dequantize             (quant.cpp:212-218)
+    ocw::activation_objective -> activation_objective (quant.cpp:230-236)
+    ocw::accumulate_stats  -> accumulate_stats       (stats.cpp:10-19)
+    ocw::gptq_order        -> gptq_order             (layerwise.cpp:11-18)
+    ocw::gptq_quantize     -> gptq_quantize          (layerwise.cpp:20-93)
+    ocw::quantize_layer    -> quantize_layer         (layerwise.cpp:120-126)
+    tensor_payload (uniform) -> pack_uniform / unpack_uniform (container.cpp:129-139,168-199)
+
+plus the north_star's one-call ``quantize_layer_x`` (W + calibration tokens X).
+
+Orientation is the reference's: W is N x M (N = input rows), H is N x N.
+Every compute call runs CUDA kernels; there is no CPU fallback -- importing
+works without a GPU (for the ABI checks), but compute raises ``CudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from enum import IntEnum
+from pathlib import Path
+
+import numpy as np
+
+__all__ = [
+    "Scheme", "Granularity", "ScaleMode", "QuantConfig", "GptqOptions", "QuantizedMatrix",
+    "CalibStats", "LayerQuantOptions", "InvalidInput", "NumericError", "IoError", "CudaError",
+    "calibrate_grids", "quantize_matrix", "dequantize", "activation_objective",
+    "accumulate_stats", "hessian_bf16", "gptq_order", "gptq_quantize", "gptq_factor",
+    "quantize_layer", "quantize_layer_x", "pack_uniform", "unpack_uniform",
+    "uniform_storage_bytes", "storage_bytes", "quant_group_count", "lib", "context",
+]
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("OCWG_LIB", _HERE / "lib" / "libocwg.so"))
+
+
+# ------------------------------------------------------------------ errors (errors.hpp:9-21)
+class InvalidInput(ValueError):
+    """ocw::invalid_input."""
+
+
+class IoError(IOError):
+    """ocw::io_error."""
+
+
+class NumericError(RuntimeError):
+    """ocw::numeric_error."""
+
+
+class CudaError(RuntimeError):
+    """CUDA failure, or no usable GPU (there is no CPU fallback)."""
+
+
+class Unsupported(RuntimeError):
+    """Feature not built on the GPU path yet."""
+
+
+_ERRORS = {1: InvalidInput, 2: IoError, 3: NumericError, 16: CudaError, 17: Unsupported}
+
+
+# ------------------------------------------------------------------ config types (quant.hpp:12-63)
+class Scheme(IntEnum):
+    symmetric = 0
+    asymmetric = 1
+
+
+class Granularity(IntEnum):
+    per_tensor = 0
+    per_channel = 1
+    per_group = 2
+
+
+class ScaleMode(IntEnum):
+    minmax = 0
+    mse_grid = 1
+
+
+@dataclass
+class QuantConfig:
+    bits: int = 4
+    scheme: Scheme = Scheme.symmetric
+    granularity: Granularity = Granularity.per_group
+    group_size: int = 128
+
+    def _c(self) -> "_QCfg":
+        return _QCfg(int(self.bits), int(self.scheme), int(self.granularity), 0, int(self.group_size))
+
+
+@dataclass
+class GptqOptions:
+    """layerwise.hpp:11-15 (reference default block_cols = 32)."""
+    actorder: bool = False
+    percdamp: float = 0.01
+    block_cols: int = 32
+
+    def _c(self) -> "_GOpt":
+        return _GOpt(int(bool(self.actorder)), 0, float(self.percdamp), int(self.block_cols))
+
+
+@dataclass
+class QuantizedMatrix:
+    """quant.hpp:54-63; grids as structure-of-arrays (scales fp32, zeros int32)."""
+    rows: int
+    cols: int
+    config: QuantConfig
+    codes: np.ndarray            # int16 [rows, cols]
+    scales: np.ndarray           # float32 [groups]
+    zeros: np.ndarray            # int32 [groups]
+    w_hat: np.ndarray | None = None
+
+    @property
+    def qmin(self) -> int:
+        return 0 if self.config.scheme == Scheme.asymmetric else -((1 << (self.config.bits - 1)) - 1)
+
+    @property
+    def qmax(self) -> int:
+        b = self.config.bits
+        return (1 << b) - 1 if self.config.scheme == Scheme.asymmetric else (1 << (b - 1)) - 1
+
+    def group_count(self) -> int:
+        return quant_group_count(self.config, self.rows, self.cols)
+
+
+@dataclass
+class CalibStats:
+    """stats.hpp:13-27: fp64 gram / cross, streaming token count."""
+    gram: np.ndarray
+    cross: np.ndarray
+    token_count: int = 0
+
+    @staticmethod
+    def zeros(dim: int) -> "CalibStats":
+        return CalibStats(np.zeros((dim, dim)), np.zeros((dim, dim)), 0)
+
+    def dim(self) -> int:
+        return self.gram.shape[0]
+
+    def gram_matrix(self) -> np.ndarray:
+        """stats.cpp:7: fp64 -> fp32."""
+        return self.gram.astype(np.float32)
+
+
+@dataclass
+class LayerQuantOptions:
+    """layerwise.hpp:41-47 (QEP: next row, not built)."""
+    method: str = "gptq"
+    config: QuantConfig = field(default_factory=QuantConfig)
+    scale_mode: ScaleMode = ScaleMode.minmax
+    gptq: GptqOptions = field(default_factory=GptqOptions)
+    qep: object | None = None
+
+
+# ------------------------------------------------------------------ ctypes plumbing
+class _QCfg(C.Structure):
+    _fields_ = [("bits", C.c_int32), ("scheme", C.c_int32), ("granularity", C.c_int32),
+                ("reserved", C.c_int32), ("group_size", C.c_uint64)]
+
+
+class _GOpt(C.Structure):
+    _fields_ = [("actorder", C.c_int32), ("reserved", C.c_int32), ("percdamp", C.c_double),
+                ("block_cols", C.c_uint64)]
+
+
+_P = C.c_void_p
+_U64 = C.c_uint64
+_SIGS = {
+    "ocwg_last_error": (C.c_char_p, []),
+    "ocwg_version": (C.c_int, []),
+    "ocwg_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "ocwg_destroy": (C.c_int, [_P]),
+    "ocwg_set_stream": (C.c_int, [_P, _P]),
+    "ocwg_synchronize": (C.c_int, [_P]),
+    "ocwg_validate_config": (C.c_int, [C.POINTER(_QCfg)]),
+    "ocwg_group_count": (_U64, [C.POINTER(_QCfg), _U64, _U64]),
+    "ocwg_storage_bytes": (_U64, [C.POINTER(_QCfg), _U64, _U64]),
+    "ocwg_calibrate_grids": (C.c_int, [_P, _P, _U64, _U64, C.POINTER(_QCfg), C.c_int, _P, _P]),
+    "ocwg_quantize_matrix": (C.c_int, [_P, _P, _U64, _U64, C.POINTER(_QCfg), C.c_int, _P, _P, _P]),
+    "ocwg_dequantize": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.POINTER(_QCfg), _P]),
+    "ocwg_activation_objective": (C.c_int, [_P, _P, _P, _P, _U64, _U64, _P]),
+    "ocwg_pack_uniform": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.POINTER(_QCfg), _P, _U64]),
+    "ocwg_unpack_uniform": (C.c_int, [_P, _P, _U64, _U64, _U64, C.POINTER(_QCfg), _P, _P, _P]),
+    "ocwg_accumulate_stats": (C.c_int, [_P, _P, _P, _U64, _U64, _P, _P, _P]),
+    "ocwg_hessian_bf16": (C.c_int, [_P, _P, _U64, _U64, _P, C.c_int]),
+    "ocwg_gptq_order": (C.c_int, [_P, _P, _U64, C.c_int, _P]),
+    "ocwg_gptq_quantize": (C.c_int, [_P, _P, _P, _U64, _U64, C.POINTER(_QCfg), C.POINTER(_GOpt),
+                                     C.c_int, _P, _P, _P, _P]),
+    "ocwg_gptq_factor": (C.c_int, [_P, _P, _U64, C.c_int, C.c_double, _P, _P, _P, _P]),
+    "ocwg_quantize_layer": (C.c_int, [_P, _P, _P, _U64, _U64, C.c_int, C.POINTER(_QCfg),
+                                      C.POINTER(_GOpt), C.c_int, C.c_int, _P, _P, _P, _P]),
+    "ocwg_quantize_layer_x": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, C.POINTER(_QCfg),
+                                        C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P, _U64, _P]),
+    "ocwg_quantize_layer_x_dev": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, C.POINTER(_QCfg),
+                                            C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P, _P]),
+    "ocwg_hessian_bf16_dev": (C.c_int, [_P, _P, _U64, _U64, _P, C.c_int]),
+    "ocwg_gptq_quantize_dev": (C.c_int, [_P, _P, _U64, _P, _U64, _U64, C.POINTER(_QCfg),
+                                         C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P]),
+    "ocwg_pack_uniform_dev": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.POINTER(_QCfg), _P]),
+    "ocwg_debug_hessian_dev": (C.c_int, [_P, _P, _U64, _U64, _P, C.c_int, C.c_int]),
+    "ocwg_launch_count": (_U64, [_P]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libocwg.so (fails loudly when the CUDA library was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise CudaError(f"libocwg.so not built at {LIB_PATH}: run __graft_entry__.build()")
+        l = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(l, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = lib().ocwg_last_error().decode(errors="replace")
+        raise _ERRORS.get(status, CudaError)(msg)
+
+
+class Context:
+    """One ocwg context (CUDA device, stream, workspace) -- ocwg_create."""
+
+    def __init__(self, device: int = 0):
+        h = _P()
+        _check(lib().ocwg_create(int(device), C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.handle:
+            lib().ocwg_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_contexts: dict[int, Context] = {}
+
+
+def context(device: int = 0) -> Context:
+    if device not in _contexts:
+        _contexts[device] = Context(device)
+    return _contexts[device]
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+# ------------------------------------------------------------------ quant.hpp
+def quant_group_count(cfg: QuantConfig, rows: int, cols: int) -> int:
+    c = cfg._c()
+    return int(lib().ocwg_group_count(C.byref(c), rows, cols))
+
+
+def uniform_storage_bytes(cfg: QuantConfig, rows: int, cols: int) -> int:
+    c = cfg._c()
+    return int(lib().ocwg_storage_bytes(C.byref(c), rows, cols))
+
+
+def storage_bytes(q: QuantizedMatrix) -> int:
+    return uniform_storage_bytes(q.config, q.rows, q.cols)
+
+
+def validate_config(cfg: QuantConfig) -> None:
+    c = cfg._c()
+    _check(lib().ocwg_validate_config(C.byref(c)))
+
+
+def calibrate_grids(w, cfg: QuantConfig, mode: ScaleMode = ScaleMode.minmax, device: int = 0):
+    w = _f32(w)
+    rows, cols = w.shape
+    c = cfg._c()
+    ng = quant_group_count(cfg, rows, cols)
+    s = np.zeros(ng, np.float32)
+    z = np.zeros(ng, np.int32)
+    _check(lib().ocwg_calibrate_grids(context(device).handle, _ptr(w), rows, cols, C.byref(c),
+                                      int(mode), _ptr(s), _ptr(z)))
+    return s, z
+
+
+def quantize_matrix(w, cfg: QuantConfig, mode: ScaleMode = ScaleMode.minmax,
+                    device: int = 0) -> QuantizedMatrix:
+    w = _f32(w)
+    rows, cols = w.shape
+    c = cfg._c()
+    ng = quant_group_count(cfg, rows, cols)
+    codes = np.zeros((rows, cols), np.int16)
+    s = np.zeros(ng, np.float32)
+    z = np.zeros(ng, np.int32)
+    _check(lib().ocwg_quantize_matrix(context(device).handle, _ptr(w), rows, cols, C.byref(c),
+                                      int(mode), _ptr(codes), _ptr(s), _ptr(z)))
+    return QuantizedMatrix(rows, cols, cfg, codes, s, z)
+
+
+def dequantize(q: QuantizedMatrix, device: int = 0) -> np.ndarray:
+    c = q.config._c()
+    out = np.zeros((q.rows, q.cols), np.float32)
+    codes = np.ascontiguousarray(q.codes, np.int16)
+    s = np.ascontiguousarray(q.scales, np.float32)
+    z = np.ascontiguousarray(q.zeros, np.int32)
+    _check(lib().ocwg_dequantize(context(device).handle, _ptr(codes), _ptr(s), _ptr(z), q.rows,
+                                 q.cols, C.byref(c), _ptr(out)))
+    return out
+
+
+def activation_objective(w, w_hat, h, device: int = 0) -> float:
+    w, w_hat, h = _f32(w), _f32(w_hat), _f32(h)
+    if w.shape != w_hat.shape:
+        raise InvalidInput("activation_objective: shape mismatch")
+    if h.shape[0] != h.shape[1] or h.shape[0] != w.shape[0]:
+        raise InvalidInput("activation_objective: H must be N x N with N = rows of W")
+    out = C.c_double()
+    _check(lib().ocwg_activation_objective(context(device).handle, _ptr(w), _ptr(w_hat), _ptr(h),
+                                           w.shape[0], w.shape[1], C.byref(out)))
+    return float(out.value)
+
+
+# ------------------------------------------------------------------ OCW1 uniform payload
+def pack_uniform(q: QuantizedMatrix, device: int = 0) -> bytes:
+    c = q.config._c()
+    n = uniform_storage_bytes(q.config, q.rows, q.cols)
+    out = np.zeros(max(n, 1), np.uint8)
+    codes = np.ascontiguousarray(q.codes, np.int16)
+    _check(lib().ocwg_pack_uniform(context(device).handle, _ptr(codes), _ptr(_f32(q.scales)),
+                                   _ptr(np.ascontiguousarray(q.zeros, np.int32)), q.rows, q.cols,
+                                   C.byref(c), _ptr(out), n))
+    return out[:n].tobytes()
+
+
+def unpack_uniform(payload: bytes, rows: int, cols: int, cfg: QuantConfig,
+                   device: int = 0) -> QuantizedMatrix:
+    c = cfg._c()
+    buf = np.frombuffer(payload, np.uint8).copy()
+    ng = quant_group_count(cfg, rows, cols)
+    codes = np.zeros((rows, cols), np.int16)
+    s = np.zeros(ng, np.float32)
+    z = np.zeros(ng, np.int32)
+    _check(lib().ocwg_unpack_uniform(context(device).handle, _ptr(buf), len(payload), rows, cols,
+                                     C.byref(c), _ptr(codes), _ptr(s), _ptr(z)))
+    return QuantizedMatrix(rows, cols, cfg, codes, s, z)
+
+
+# ------------------------------------------------------------------ stats.hpp
+def accumulate_stats(stats: CalibStats, x_fp, x_pert, device: int = 0) -> None:
+    x_fp = _f32(x_fp)
+    same = x_pert is x_fp
+    x_pert = x_fp if same else _f32(x_pert)
+    if x_fp.shape != x_pert.shape:
+        raise InvalidInput(f"accumulate_stats: shape mismatch ({x_fp.shape} vs {x_pert.shape})")
+    if x_fp.shape[1] != stats.dim():
+        raise InvalidInput(f"accumulate_stats: stats dimension {stats.dim()} does not match "
+                           f"inputs with {x_fp.shape[1]} columns")
+    gram = np.ascontiguousarray(stats.gram, np.float64)
+    cross = np.ascontiguousarray(stats.cross, np.float64)
+    tc = C.c_uint64(stats.token_count)
+    _check(lib().ocwg_accumulate_stats(context(device).handle, _ptr(x_fp), _ptr(x_pert),
+                                       x_fp.shape[0], x_fp.shape[1], _ptr(gram), _ptr(cross),
+                                       C.byref(tc)))
+    stats.gram, stats.cross, stats.token_count = gram, cross, int(tc.value)
+
+
+def hessian_bf16(x_bf16_bits: np.ndarray, h: np.ndarray | None = None, device: int = 0) -> np.ndarray:
+    """H (+)= X^T X for bf16 tokens (uint16 bit patterns, T x N) on the tensor cores."""
+    x = np.ascontiguousarray(x_bf16_bits, np.uint16)
+    t, n = x.shape
+    acc = h is not None
+    out = np.ascontiguousarray(h, np.float32).copy() if acc else np.zeros((n, n), np.float32)
+    _check(lib().ocwg_hessian_bf16(context(device).handle, _ptr(x), t, n, _ptr(out), int(acc)))
+    return out
+
+
+# ------------------------------------------------------------------ layerwise.hpp
+def gptq_order(h, actorder: bool, device: int = 0) -> np.ndarray:
+    h = _f32(h)
+    n = h.shape[0]
+    out = np.zeros(n, np.int64)
+    _check(lib().ocwg_gptq_order(context(device).handle, _ptr(h), n, int(bool(actorder)), _ptr(out)))
+    return out
+
+
+def _check_shapes(w: np.ndarray, h: np.ndarray) -> None:
+    if h.ndim != 2 or h.shape[0] != h.shape[1] or h.shape[0] != w.shape[0]:
+        raise InvalidInput("gptq_quantize: H must be N x N with N = rows of W")
+
+
+def gptq_quantize(w, h, cfg: QuantConfig, opts: GptqOptions = GptqOptions(),
+                  mode: ScaleMode = ScaleMode.minmax, want_w_hat: bool = False,
+                  device: int = 0) -> QuantizedMatrix:
+    w, h = _f32(w), _f32(h)
+    validate_config(cfg)
+    _check_shapes(w, h)
+    n, m = w.shape
+    ng = quant_group_count(cfg, n, m)
+    codes = np.zeros((n, m), np.int16)
+    s = np.zeros(ng, np.float32)
+    z = np.zeros(ng, np.int32)
+    wh = np.zeros((n, m), np.float32) if want_w_hat else None
+    c, o = cfg._c(), opts._c()
+    _check(lib().ocwg_gptq_quantize(context(device).handle, _ptr(w), _ptr(h), n, m, C.byref(c),
+                                    C.byref(o), int(mode), _ptr(codes), _ptr(s), _ptr(z), _ptr(wh)))
+    return QuantizedMatrix(n, m, cfg, codes, s, z, wh)
+
+
+def gptq_factor(h, actorder: bool, percdamp: float, device: int = 0):
+    """(order, hinv, U, damp) of layerwise.cpp:29-51, computed on the GPU."""
+    h = _f32(h)
+    n = h.shape[0]
+    order = np.zeros(n, np.int64)
+    hinv = np.zeros((n, n), np.float64)
+    u = np.zeros((n, n), np.float64)
+    damp = C.c_double()
+    _check(lib().ocwg_gptq_factor(context(device).handle, _ptr(h), n, int(bool(actorder)),
+                                  float(percdamp), _ptr(order), _ptr(hinv), _ptr(u), C.byref(damp)))
+    return order, hinv, u, float(damp.value)
+
+
+def quantize_layer(w, stats: CalibStats, opts: LayerQuantOptions, device: int = 0) -> QuantizedMatrix:
+    """layerwise.cpp:120-126."""
+    if opts.qep is not None:
+        raise Unsupported("quantize_layer: QEP target correction not built yet")
+    if opts.method == "rtn":
+        return quantize_matrix(w, opts.config, opts.scale_mode, device)
+    if opts.method != "gptq":
+        raise InvalidInput(f"unknown quantization method: {opts.method}")
+    return gptq_quantize(w, stats.gram_matrix(), opts.config, opts.gptq, opts.scale_mode,
+                         device=device)
+
+
+def quantize_layer_x(w, x_bf16_bits, cfg: QuantConfig, opts: GptqOptions,
+                     mode: ScaleMode = ScaleMode.minmax, device: int = 0):
+    """The north_star's one-call layer quantize from host buffers:
+    W (N x M fp32) + calibration tokens X (T x N bf16 bits) ->
+    (QuantizedMatrix with w_hat, packed OCW1 payload bytes, H fp32)."""
+    w = _f32(w)
+    x = np.ascontiguousarray(x_bf16_bits, np.uint16)
+    n, m = w.shape
+    if x.shape[1] != n:
+        raise InvalidInput("quantize_layer_x: X must be T x N with N = rows of W")
+    ng = quant_group_count(cfg, n, m)
+    pb = uniform_storage_bytes(cfg, n, m)
+    codes = np.zeros((n, m), np.int16)
+    s = np.zeros(ng, np.float32)
+    z = np.zeros(ng, np.int32)
+    wh = np.zeros((n, m), np.float32)
+    payload = np.zeros(max(pb, 1), np.uint8)
+    h = np.zeros((n, n), np.float32)
+    c, o = cfg._c(), opts._c()
+    _check(lib().ocwg_quantize_layer_x(context(device).handle, _ptr(w), _ptr(x), x.shape[0], n, m,
+                                       C.byref(c), C.byref(o), int(mode), _ptr(codes), _ptr(s),
+                                       _ptr(z), _ptr(wh), _ptr(payload), pb, _ptr(h)))
+    return QuantizedMatrix(n, m, cfg, codes, s, z, wh), payload[:pb].tobytes(), h

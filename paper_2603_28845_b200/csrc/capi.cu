@@ -1,0 +1,747 @@
+// C ABI of libocwg.so (include/ocwg.h): context, workspace, error mapping and
+// the orchestration of the kernels into the reference's hot-path functions.
+// Validation order and error classes follow the reference exactly
+// (quant.cpp:19-25,168-171; layerwise.cpp:22-26,43-49; stats.cpp:11-15).
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ocwg.h"
+#include "kernels.h"
+
+namespace ocwg {
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+unsigned long long launches_issued() { return g_launches.load(std::memory_order_relaxed); }
+
+}  // namespace ocwg
+
+using namespace ocwg;
+
+struct ocwg_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  void* ws = nullptr;  // device arena
+  size_t ws_bytes = 0;
+  unsigned* flag = nullptr;  // device status word
+  unsigned* flag_host = nullptr;
+  std::mutex mu;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(OCWG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return OCWG_OK;
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return OCWG_CUDA_ERROR;
+  }
+}
+
+// ---------------------------------------------------------------- config
+void validate(const ocwg_quant_config* c) {  // QuantConfig::validate (quant.cpp:19-25)
+  if (!c) fail(OCWG_INVALID_INPUT, "QuantConfig: null");
+  if (c->bits < 1 || c->bits > 8) fail(OCWG_INVALID_INPUT, "QuantConfig: bits must be in [1,8]");
+  if (c->scheme == OCWG_SYMMETRIC && c->bits < 2)
+    fail(OCWG_INVALID_INPUT,
+         "QuantConfig: symmetric grids need bits >= 2 (1-bit signed range is empty)");
+  if (c->scheme != OCWG_SYMMETRIC && c->scheme != OCWG_ASYMMETRIC)
+    fail(OCWG_INVALID_INPUT, "QuantConfig: unknown scheme");
+  if (c->granularity < 0 || c->granularity > 2)
+    fail(OCWG_INVALID_INPUT, "QuantConfig: unknown granularity");
+  if (c->granularity == OCWG_PER_GROUP && c->group_size < 1)
+    fail(OCWG_INVALID_INPUT, "QuantConfig: group_size must be >= 1");
+}
+
+QCfg qcfg(const ocwg_quant_config* c, uint64_t cols) {
+  QCfg q;
+  q.bits = c->bits;
+  q.scheme = c->scheme;
+  q.gran = c->granularity;
+  q.group = c->granularity == OCWG_PER_GROUP ? (long long)c->group_size : 1;
+  q.qmin = c->scheme == OCWG_ASYMMETRIC ? 0 : -((1 << (c->bits - 1)) - 1);
+  q.qmax = c->scheme == OCWG_ASYMMETRIC ? (1 << c->bits) - 1 : (1 << (c->bits - 1)) - 1;
+  q.gpr = c->granularity == OCWG_PER_TENSOR ? 0
+          : c->granularity == OCWG_PER_CHANNEL ? 1
+                                               : (long long)((cols + c->group_size - 1) / c->group_size);
+  return q;
+}
+
+uint64_t group_count(const ocwg_quant_config* c, uint64_t rows, uint64_t cols) {
+  if (c->granularity == OCWG_PER_TENSOR) return 1;
+  if (c->granularity == OCWG_PER_CHANNEL) return rows;
+  return rows * ((cols + c->group_size - 1) / c->group_size);
+}
+
+uint64_t storage_bytes(const ocwg_quant_config* c, uint64_t rows, uint64_t cols) {
+  const uint64_t code_bits = rows * cols * uint64_t(c->bits);
+  const uint64_t meta = 2 + (c->scheme == OCWG_ASYMMETRIC ? 1 : 0);
+  return (code_bits + 7) / 8 + group_count(c, rows, cols) * meta;
+}
+
+// ---------------------------------------------------------------- workspace arena
+struct Arena {
+  ocwg_ctx* ctx;
+  size_t off = 0;
+  std::vector<std::pair<size_t, size_t>> reqs;
+  explicit Arena(ocwg_ctx* c) : ctx(c) {}
+  static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+  // two-phase: reserve sizes, then commit (grow once), then take pointers
+  size_t reserve(size_t bytes) {
+    const size_t o = off;
+    off += al(bytes);
+    return o;
+  }
+  void commit() {
+    if (off > ctx->ws_bytes) {
+      if (ctx->ws) cudaFree(ctx->ws);
+      ctx->ws = nullptr;
+      ctx->ws_bytes = 0;
+      ck(cudaMalloc(&ctx->ws, off), "cudaMalloc(workspace)");
+      ctx->ws_bytes = off;
+    }
+  }
+  template <typename T>
+  T* at(size_t o) const {
+    return reinterpret_cast<T*>(static_cast<char*>(ctx->ws) + o);
+  }
+};
+
+void begin(ocwg_ctx* ctx) {
+  if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  ck(cudaMemsetAsync(ctx->flag, 0, sizeof(unsigned), ctx->stream), "reset status");
+}
+
+// drain the stream; map device status bits to the reference's error classes
+void finish(ocwg_ctx* ctx, bool numeric_first = true) {
+  ck(cudaGetLastError(), "kernel launch");
+  ck(cudaMemcpyAsync(ctx->flag_host, ctx->flag, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "status D2H");
+  ck(cudaStreamSynchronize(ctx->stream), "stream synchronize");
+  const unsigned f = *ctx->flag_host;
+  if (numeric_first && (f & kFlagNotPD))
+    fail(OCWG_NUMERIC_ERROR, "gptq_quantize: Gram matrix is not positive definite after dampening");
+  if (f & kFlagNonFinite) fail(OCWG_INVALID_INPUT, "calibrate_grids: non-finite entry");
+  if (f & kFlagNotPD)
+    fail(OCWG_NUMERIC_ERROR, "gptq_quantize: Gram matrix is not positive definite after dampening");
+}
+
+void h2d(void* d, const void* h, size_t bytes, ocwg_ctx* ctx) {
+  if (bytes) ck(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+}
+void d2h(void* h, const void* d, size_t bytes, ocwg_ctx* ctx) {
+  if (bytes && h) ck(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+}
+
+// ---------------------------------------------------------------- GPTQ core (device pointers)
+struct GptqBufs {
+  int32_t* order;
+  double* damp;
+  double* a;
+  double* u;
+  double* fws;
+  double* wp;
+  double* err;
+};
+
+size_t gptq_reserve(Arena& ar, uint64_t n, uint64_t m, size_t* o) {
+  const uint64_t nblk = (n + 63) / 64;
+  o[0] = ar.reserve(n * sizeof(int32_t));
+  o[1] = ar.reserve(sizeof(double));
+  o[2] = ar.reserve(n * n * sizeof(double));
+  o[3] = ar.reserve(n * n * sizeof(double));
+  o[4] = ar.reserve((nblk * 64 * 64 + n * n) * sizeof(double));
+  o[5] = ar.reserve(n * m * sizeof(double));
+  o[6] = ar.reserve(128 * m * sizeof(double));
+  return 7;
+}
+GptqBufs gptq_bufs(const Arena& ar, const size_t* o) {
+  return {ar.at<int32_t>(o[0]), ar.at<double>(o[1]), ar.at<double>(o[2]), ar.at<double>(o[3]),
+          ar.at<double>(o[4]), ar.at<double>(o[5]), ar.at<double>(o[6])};
+}
+
+// order + damp + factorisation -> U (device); the reference's :29-51
+void run_factor(ocwg_ctx* ctx, const float* h_dev, uint64_t n, int actorder, double percdamp,
+                const GptqBufs& b) {
+  cudaStream_t st = ctx->stream;
+  launch_order(h_dev, (long long)n, actorder, b.order, st);
+  launch_build_factor_input(h_dev, (long long)n, b.order, percdamp, b.a, b.damp, st);
+  factor_upper_inverse(b.a, (long long)n, b.u, b.fws, ctx->flag, st);
+}
+
+// gptq_quantize on device buffers (w row stride ldw; codes/w_hat stride ldw)
+void run_gptq(ocwg_ctx* ctx, const float* w, uint64_t ldw, const float* h_dev, uint64_t n,
+              uint64_t m, const ocwg_quant_config* cfg, const ocwg_gptq_options* opts, int mode,
+              int16_t* codes, float* scales, int32_t* zeros, float* w_hat, const GptqBufs& b,
+              float* mm_ws) {
+  cudaStream_t st = ctx->stream;
+  const QCfg c = qcfg(cfg, m);
+  run_factor(ctx, h_dev, n, opts->actorder, opts->percdamp, b);
+  launch_calibrate_grids(w, (long long)n, (long long)m, (long long)ldw, c, mode, scales, zeros,
+                         ctx->flag, mm_ws, st);
+  launch_permute_rows_f64(w, (long long)n, (long long)m, (long long)ldw, b.order, b.wp, st);
+  gptq_sweep(b.wp, (long long)n, (long long)m, b.u, b.order, c, scales, zeros,
+             (long long)opts->block_cols, codes, w_hat, (long long)ldw, b.err, st);
+}
+
+void check_gptq_args(const ocwg_quant_config* cfg, const ocwg_gptq_options* opts, uint64_t n,
+                     uint64_t m) {
+  validate(cfg);  // layerwise.cpp:22
+  if (!opts) fail(OCWG_INVALID_INPUT, "gptq_quantize: null options");
+  if (!(opts->percdamp > 0.0) || opts->percdamp > 1.0)  // :25-26
+    fail(OCWG_INVALID_INPUT, "gptq_quantize: percdamp must be in (0, 1]");
+  (void)n;
+  (void)m;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ocwg_last_error(void) { return g_err.c_str(); }
+int ocwg_version(void) { return 1; }
+
+int ocwg_create(int device, ocwg_ctx** out) {
+  return guard([&] {
+    if (!out) fail(OCWG_INVALID_INPUT, "null out");
+    int n = 0;
+    ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) fail(OCWG_CUDA_ERROR, "no such CUDA device");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new ocwg_ctx;
+    c->device = device;
+    ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->stream = c->own;
+    ck(cudaMalloc(&c->flag, sizeof(unsigned)), "cudaMalloc(flag)");
+    ck(cudaMallocHost(&c->flag_host, sizeof(unsigned)), "cudaMallocHost(flag)");
+    *out = c;
+  });
+}
+
+int ocwg_destroy(ocwg_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->ws) cudaFree(ctx->ws);
+    cudaFree(ctx->flag);
+    cudaFreeHost(ctx->flag_host);
+    cudaStreamDestroy(ctx->own);
+    delete ctx;
+  });
+}
+
+int ocwg_set_stream(ocwg_ctx* ctx, void* s) {
+  return guard([&] {
+    if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+  });
+}
+
+int ocwg_synchronize(ocwg_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
+    ck(cudaStreamSynchronize(ctx->stream), "stream synchronize");
+  });
+}
+
+uint64_t ocwg_launch_count(ocwg_ctx*) { return launches_issued(); }
+
+int ocwg_validate_config(const ocwg_quant_config* cfg) {
+  return guard([&] { validate(cfg); });
+}
+uint64_t ocwg_group_count(const ocwg_quant_config* cfg, uint64_t rows, uint64_t cols) {
+  return group_count(cfg, rows, cols);
+}
+uint64_t ocwg_storage_bytes(const ocwg_quant_config* cfg, uint64_t rows, uint64_t cols) {
+  return storage_bytes(cfg, rows, cols);
+}
+
+// ------------------------------------------------------------------ quant.hpp
+int ocwg_calibrate_grids(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t cols,
+                         const ocwg_quant_config* cfg, int mode, float* scales, int32_t* zeros) {
+  return guard([&] {
+    validate(cfg);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    const uint64_t ng = group_count(cfg, rows, cols);
+    Arena ar(ctx);
+    const size_t ow = ar.reserve(rows * cols * 4), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4),
+                 om = ar.reserve(4096 * 4);
+    ar.commit();
+    h2d(ar.at<float>(ow), w, rows * cols * 4, ctx);
+    if (rows * cols > 0)
+      launch_calibrate_grids(ar.at<float>(ow), (long long)rows, (long long)cols, (long long)cols,
+                             qcfg(cfg, cols), mode, ar.at<float>(os), ar.at<int32_t>(oz),
+                             ctx->flag, ar.at<float>(om), ctx->stream);
+    finish(ctx);
+    if (rows == 0 || cols == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
+    d2h(scales, ar.at<float>(os), ng * 4, ctx);
+    d2h(zeros, ar.at<int32_t>(oz), ng * 4, ctx);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int ocwg_quantize_matrix(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t cols,
+                         const ocwg_quant_config* cfg, int mode, int16_t* codes, float* scales,
+                         int32_t* zeros) {
+  return guard([&] {
+    validate(cfg);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    const uint64_t ng = group_count(cfg, rows, cols);
+    Arena ar(ctx);
+    const size_t ow = ar.reserve(rows * cols * 4), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4),
+                 oc = ar.reserve(rows * cols * 2), om = ar.reserve(4096 * 4);
+    ar.commit();
+    const QCfg c = qcfg(cfg, cols);
+    h2d(ar.at<float>(ow), w, rows * cols * 4, ctx);
+    if (rows * cols > 0) {
+      launch_calibrate_grids(ar.at<float>(ow), (long long)rows, (long long)cols, (long long)cols, c,
+                             mode, ar.at<float>(os), ar.at<int32_t>(oz), ctx->flag,
+                             ar.at<float>(om), ctx->stream);
+      launch_quantize_rtn(ar.at<float>(ow), (long long)rows, (long long)cols, (long long)cols, c,
+                          ar.at<float>(os), ar.at<int32_t>(oz), ar.at<int16_t>(oc), nullptr,
+                          ctx->stream);
+    }
+    finish(ctx);
+    if (rows == 0 || cols == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
+    d2h(codes, ar.at<int16_t>(oc), rows * cols * 2, ctx);
+    d2h(scales, ar.at<float>(os), ng * 4, ctx);
+    d2h(zeros, ar.at<int32_t>(oz), ng * 4, ctx);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int ocwg_dequantize(ocwg_ctx* ctx, const int16_t* codes, const float* scales, const int32_t* zeros,
+                    uint64_t rows, uint64_t cols, const ocwg_quant_config* cfg, float* out) {
+  return guard([&] {
+    validate(cfg);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    const uint64_t ng = group_count(cfg, rows, cols);
+    Arena ar(ctx);
+    const size_t oc = ar.reserve(rows * cols * 2), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4),
+                 oo = ar.reserve(rows * cols * 4);
+    ar.commit();
+    h2d(ar.at<int16_t>(oc), codes, rows * cols * 2, ctx);
+    h2d(ar.at<float>(os), scales, ng * 4, ctx);
+    h2d(ar.at<int32_t>(oz), zeros, ng * 4, ctx);
+    if (rows * cols != 0)
+      launch_dequantize(ar.at<int16_t>(oc), (long long)rows, (long long)cols, qcfg(cfg, cols),
+                        ar.at<float>(os), ar.at<int32_t>(oz), ar.at<float>(oo), ctx->stream);
+    d2h(out, ar.at<float>(oo), rows * cols * 4, ctx);
+    finish(ctx);
+  });
+}
+
+int ocwg_activation_objective(ocwg_ctx* ctx, const float* w, const float* w_hat, const float* h,
+                              uint64_t n, uint64_t m, double* out) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    Arena ar(ctx);
+    const size_t ow = ar.reserve(n * m * 4), owh = ar.reserve(n * m * 4), oh = ar.reserve(n * n * 4),
+                 ows = ar.reserve(2 * n * m * 8), oo = ar.reserve(8);
+    ar.commit();
+    h2d(ar.at<float>(ow), w, n * m * 4, ctx);
+    h2d(ar.at<float>(owh), w_hat, n * m * 4, ctx);
+    h2d(ar.at<float>(oh), h, n * n * 4, ctx);
+    activation_objective(ar.at<float>(ow), ar.at<float>(owh), ar.at<float>(oh), (long long)n,
+                         (long long)m, ar.at<double>(oo), ar.at<double>(ows), ctx->stream);
+    d2h(out, ar.at<double>(oo), 8, ctx);
+    finish(ctx);
+  });
+}
+
+// ------------------------------------------------------------------ packing
+int ocwg_pack_uniform_dev(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
+                          const int32_t* zeros, uint64_t rows, uint64_t cols,
+                          const ocwg_quant_config* cfg, uint8_t* out) {
+  return guard([&] {
+    validate(cfg);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    launch_pack(codes, (long long)(rows * cols), (long long)group_count(cfg, rows, cols),
+                qcfg(cfg, cols), scales, zeros, out, ctx->stream);
+    finish(ctx);
+  });
+}
+
+int ocwg_pack_uniform(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
+                      const int32_t* zeros, uint64_t rows, uint64_t cols,
+                      const ocwg_quant_config* cfg, uint8_t* out, uint64_t out_len) {
+  return guard([&] {
+    validate(cfg);
+    const uint64_t need = storage_bytes(cfg, rows, cols);
+    if (out_len < need) fail(OCWG_INVALID_INPUT, "pack_uniform: output buffer too small");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    const uint64_t ng = group_count(cfg, rows, cols);
+    Arena ar(ctx);
+    const size_t oc = ar.reserve(rows * cols * 2), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4),
+                 oo = ar.reserve(need);
+    ar.commit();
+    h2d(ar.at<int16_t>(oc), codes, rows * cols * 2, ctx);
+    h2d(ar.at<float>(os), scales, ng * 4, ctx);
+    h2d(ar.at<int32_t>(oz), zeros, ng * 4, ctx);
+    launch_pack(ar.at<int16_t>(oc), (long long)(rows * cols), (long long)ng, qcfg(cfg, cols),
+                ar.at<float>(os), ar.at<int32_t>(oz), ar.at<uint8_t>(oo), ctx->stream);
+    d2h(out, ar.at<uint8_t>(oo), need, ctx);
+    finish(ctx);
+  });
+}
+
+int ocwg_unpack_uniform(ocwg_ctx* ctx, const uint8_t* payload, uint64_t len, uint64_t rows,
+                        uint64_t cols, const ocwg_quant_config* cfg, int16_t* codes, float* scales,
+                        int32_t* zeros) {
+  return guard([&] {
+    validate(cfg);
+    if (len != storage_bytes(cfg, rows, cols))  // container.cpp:197
+      fail(OCWG_IO_ERROR, "container: uniform payload size mismatch");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    const uint64_t ng = group_count(cfg, rows, cols);
+    Arena ar(ctx);
+    const size_t op = ar.reserve(len), oc = ar.reserve(rows * cols * 2), os = ar.reserve(ng * 4),
+                 oz = ar.reserve(ng * 4);
+    ar.commit();
+    h2d(ar.at<uint8_t>(op), payload, len, ctx);
+    launch_unpack(ar.at<uint8_t>(op), (long long)(rows * cols), (long long)ng, qcfg(cfg, cols),
+                  ar.at<int16_t>(oc), ar.at<float>(os), ar.at<int32_t>(oz), ctx->stream);
+    d2h(codes, ar.at<int16_t>(oc), rows * cols * 2, ctx);
+    d2h(scales, ar.at<float>(os), ng * 4, ctx);
+    d2h(zeros, ar.at<int32_t>(oz), ng * 4, ctx);
+    finish(ctx);
+  });
+}
+
+// ------------------------------------------------------------------ stats.hpp
+int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert, uint64_t rows,
+                          uint64_t dim, double* gram, double* cross, uint64_t* token_count) {
+  return guard([&] {
+    if (!gram) fail(OCWG_INVALID_INPUT, "accumulate_stats: null gram");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    const bool same = (x_fp == x_pert);
+    Arena ar(ctx);
+    const size_t of = ar.reserve(rows * dim * 4), op = ar.reserve(rows * dim * 4),
+                 og = ar.reserve(dim * dim * 8), oc = ar.reserve(dim * dim * 8),
+                 od = ar.reserve(rows * dim * 8);
+    ar.commit();
+    h2d(ar.at<float>(op), x_pert, rows * dim * 4, ctx);
+    if (!same) h2d(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
+    h2d(ar.at<double>(og), gram, dim * dim * 8, ctx);
+    if (cross) h2d(ar.at<double>(oc), cross, dim * dim * 8, ctx);
+    const float* xf = same ? ar.at<float>(op) : ar.at<float>(of);
+    // cross += Xp^T (X - Xp) is identically zero when X == Xp: skip the GEMM
+    accumulate_stats_f64(xf, ar.at<float>(op), (long long)rows, (long long)dim, ar.at<double>(og),
+                         (cross && !same) ? ar.at<double>(oc) : nullptr, ar.at<double>(od),
+                         ctx->stream);
+    d2h(gram, ar.at<double>(og), dim * dim * 8, ctx);
+    if (cross && !same) d2h(cross, ar.at<double>(oc), dim * dim * 8, ctx);
+    finish(ctx);
+    if (token_count) *token_count += rows;
+  });
+}
+
+int ocwg_hessian_bf16_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, uint64_t dim,
+                          float* h, int accumulate) {
+  return ocwg_debug_hessian_dev(ctx, x, tokens, dim, h, accumulate, 0);
+}
+
+int ocwg_debug_hessian_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, uint64_t dim,
+                           float* h, int accumulate, int impl) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    if (tokens == 0) {
+      if (!accumulate) ck(cudaMemsetAsync(h, 0, dim * dim * 4, ctx->stream), "memset");
+    } else if (impl == 1) {
+      hessian_simt(x, (long long)tokens, (long long)dim, h, accumulate, ctx->stream);
+    } else {
+      Arena ar(ctx);
+      const size_t bytes = hessian_tc_workspace_bytes((long long)tokens, (long long)dim);
+      const size_t o = ar.reserve(bytes);
+      ar.commit();
+      const int r = hessian_tc(x, (long long)tokens, (long long)dim, h, accumulate, ar.at<void>(o),
+                               bytes, ctx->stream);
+      if (r == -1)
+        fail(OCWG_UNSUPPORTED, "hessian: dim must be a multiple of 8 for the tensor-core path");
+      if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
+    }
+    finish(ctx);
+  });
+}
+
+int ocwg_hessian_bf16(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, uint64_t dim, float* h,
+                      int accumulate) {
+  return guard([&] {
+    float* hd = nullptr;
+    uint16_t* xd = nullptr;
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ck(cudaMalloc(&hd, dim * dim * 4), "cudaMalloc(H)");
+    ck(cudaMalloc(&xd, std::max<uint64_t>(1, tokens * dim * 2)), "cudaMalloc(X)");
+    h2d(xd, x, tokens * dim * 2, ctx);
+    if (accumulate) h2d(hd, h, dim * dim * 4, ctx);
+    const int r = ocwg_hessian_bf16_dev(ctx, xd, tokens, dim, hd, accumulate);
+    if (r == OCWG_OK) {
+      d2h(h, hd, dim * dim * 4, ctx);
+      cudaStreamSynchronize(ctx->stream);
+    }
+    cudaFree(hd);
+    cudaFree(xd);
+    if (r != OCWG_OK) fail(r, g_err);
+  });
+}
+
+// ------------------------------------------------------------------ layerwise.hpp
+int ocwg_gptq_order(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, int64_t* order) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    Arena ar(ctx);
+    const size_t oh = ar.reserve(n * n * 4), oo = ar.reserve(n * 4);
+    ar.commit();
+    h2d(ar.at<float>(oh), h, n * n * 4, ctx);
+    if (n) launch_order(ar.at<float>(oh), (long long)n, actorder, ar.at<int32_t>(oo), ctx->stream);
+    std::vector<int32_t> o(n);
+    d2h(o.data(), ar.at<int32_t>(oo), n * 4, ctx);
+    finish(ctx);
+    for (uint64_t i = 0; i < n; ++i) order[i] = o[i];
+  });
+}
+
+int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, double percdamp,
+                     int64_t* order, double* hinv, double* u, double* damp) {
+  return guard([&] {
+    if (!(percdamp > 0.0) || percdamp > 1.0)
+      fail(OCWG_INVALID_INPUT, "gptq_quantize: percdamp must be in (0, 1]");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    Arena ar(ctx);
+    size_t o[8];
+    gptq_reserve(ar, n, 1, o);
+    const size_t oh = ar.reserve(n * n * 4), ohi = ar.reserve(n * n * 8);
+    ar.commit();
+    const GptqBufs b = gptq_bufs(ar, o);
+    h2d(ar.at<float>(oh), h, n * n * 4, ctx);
+    run_factor(ctx, ar.at<float>(oh), n, actorder, percdamp, b);
+    if (hinv) launch_gram_upper(b.u, (long long)n, ar.at<double>(ohi), ctx->stream);
+    std::vector<int32_t> ord(n);
+    d2h(ord.data(), b.order, n * 4, ctx);
+    d2h(u, b.u, n * n * 8, ctx);
+    d2h(hinv, ar.at<double>(ohi), n * n * 8, ctx);
+    d2h(damp, b.damp, 8, ctx);
+    finish(ctx);
+    if (order)
+      for (uint64_t i = 0; i < n; ++i) order[i] = ord[i];
+  });
+}
+
+int ocwg_gptq_quantize_dev(ocwg_ctx* ctx, const float* w, uint64_t ldw, const float* h,
+                           uint64_t n, uint64_t m, const ocwg_quant_config* cfg,
+                           const ocwg_gptq_options* opts, int mode, int16_t* codes, float* scales,
+                           int32_t* zeros, float* w_hat) {
+  return guard([&] {
+    check_gptq_args(cfg, opts, n, m);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    Arena ar(ctx);
+    size_t o[8];
+    gptq_reserve(ar, n, m, o);
+    const size_t om = ar.reserve(4096 * 4);
+    ar.commit();
+    if (n && m)
+      run_gptq(ctx, w, ldw, h, n, m, cfg, opts, mode, codes, scales, zeros, w_hat,
+               gptq_bufs(ar, o), ar.at<float>(om));
+    else if (n)
+      run_factor(ctx, h, n, opts->actorder, opts->percdamp, gptq_bufs(ar, o));
+    finish(ctx);
+    if (n == 0 || m == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
+  });
+}
+
+int ocwg_gptq_quantize(ocwg_ctx* ctx, const float* w, const float* h, uint64_t n, uint64_t m,
+                       const ocwg_quant_config* cfg, const ocwg_gptq_options* opts, int mode,
+                       int16_t* codes, float* scales, int32_t* zeros, float* w_hat) {
+  return guard([&] {
+    check_gptq_args(cfg, opts, n, m);
+    const uint64_t ng = group_count(cfg, n, m);
+    void* blob = nullptr;
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const size_t bytes = n * m * 4 + n * n * 4 + n * m * 2 + ng * 8 + n * m * 4 + 4 * 256;
+    ck(cudaMalloc(&blob, bytes), "cudaMalloc(io)");
+    char* p = static_cast<char*>(blob);
+    auto take = [&](size_t b) {
+      char* r = p;
+      p += (b + 255) & ~size_t(255);
+      return r;
+    };
+    float* wd = reinterpret_cast<float*>(take(n * m * 4));
+    float* hd = reinterpret_cast<float*>(take(n * n * 4));
+    int16_t* cd = reinterpret_cast<int16_t*>(take(n * m * 2));
+    float* sd = reinterpret_cast<float*>(take(ng * 4));
+    int32_t* zd = reinterpret_cast<int32_t*>(take(ng * 4));
+    float* whd = reinterpret_cast<float*>(take(n * m * 4));
+    h2d(wd, w, n * m * 4, ctx);
+    h2d(hd, h, n * n * 4, ctx);
+    const int r = ocwg_gptq_quantize_dev(ctx, wd, m, hd, n, m, cfg, opts, mode, cd, sd, zd,
+                                         w_hat ? whd : nullptr);
+    if (r == OCWG_OK) {
+      d2h(codes, cd, n * m * 2, ctx);
+      d2h(scales, sd, ng * 4, ctx);
+      d2h(zeros, zd, ng * 4, ctx);
+      if (w_hat) d2h(w_hat, whd, n * m * 4, ctx);
+      cudaStreamSynchronize(ctx->stream);
+    }
+    const std::string msg = g_err;
+    cudaFree(blob);
+    if (r != OCWG_OK) fail(r, msg);
+  });
+}
+
+int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, uint64_t n, uint64_t m,
+                        int method, const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
+                        int mode, int qep, int16_t* codes, float* scales, int32_t* zeros,
+                        float* w_hat) {
+  return guard([&] {
+    if (qep) fail(OCWG_UNSUPPORTED, "quantize_layer: QEP target correction not built yet");
+    if (method == 0) {
+      const int r = ocwg_quantize_matrix(ctx, w, n, m, cfg, mode, codes, scales, zeros);
+      if (r != OCWG_OK) fail(r, g_err);
+      if (w_hat) {
+        const int r2 = ocwg_dequantize(ctx, codes, scales, zeros, n, m, cfg, w_hat);
+        if (r2 != OCWG_OK) fail(r2, g_err);
+      }
+      return;
+    }
+    // stats.gram_matrix(): fp64 -> fp32 (stats.cpp:7)
+    std::vector<float> hf(n * n);
+    for (uint64_t i = 0; i < n * n; ++i) hf[i] = float(gram[i]);
+    const int r = ocwg_gptq_quantize(ctx, w, hf.data(), n, m, cfg, opts, mode, codes, scales, zeros,
+                                     w_hat);
+    if (r != OCWG_OK) fail(r, g_err);
+  });
+}
+
+// ------------------------------------------------------------------ end to end
+int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint64_t tokens,
+                              uint64_t n, uint64_t m, const ocwg_quant_config* cfg,
+                              const ocwg_gptq_options* opts, int mode, int16_t* codes,
+                              float* scales, int32_t* zeros, float* w_hat, uint8_t* payload,
+                              float* h_out) {
+  return guard([&] {
+    check_gptq_args(cfg, opts, n, m);
+    if (n == 0 || m == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    const uint64_t ng = group_count(cfg, n, m);
+    Arena ar(ctx);
+    size_t o[8];
+    gptq_reserve(ar, n, m, o);
+    const size_t om = ar.reserve(4096 * 4);
+    const size_t oh = ar.reserve(n * n * 4);
+    const size_t hws = hessian_tc_workspace_bytes((long long)tokens, (long long)n);
+    const size_t ohw = ar.reserve(hws);
+    const size_t oc = ar.reserve(n * m * 2), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4);
+    ar.commit();
+    float* h = h_out ? h_out : ar.at<float>(oh);
+    int16_t* cd = codes ? codes : ar.at<int16_t>(oc);
+    float* sd = scales ? scales : ar.at<float>(os);
+    int32_t* zd = zeros ? zeros : ar.at<int32_t>(oz);
+    if (tokens == 0) {
+      ck(cudaMemsetAsync(h, 0, n * n * 4, ctx->stream), "memset");
+    } else {
+      const int r = hessian_tc(x, (long long)tokens, (long long)n, h, 0, ar.at<void>(ohw), hws,
+                               ctx->stream);
+      if (r == -1) hessian_simt(x, (long long)tokens, (long long)n, h, 0, ctx->stream);
+      else if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
+    }
+    run_gptq(ctx, w, m, h, n, m, cfg, opts, mode, cd, sd, zd, w_hat, gptq_bufs(ar, o),
+             ar.at<float>(om));
+    if (payload) launch_pack(cd, (long long)(n * m), (long long)ng, qcfg(cfg, m), sd, zd, payload,
+                             ctx->stream);
+    finish(ctx);
+  });
+}
+
+int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint64_t tokens,
+                          uint64_t n, uint64_t m, const ocwg_quant_config* cfg,
+                          const ocwg_gptq_options* opts, int mode, int16_t* codes, float* scales,
+                          int32_t* zeros, float* w_hat, uint8_t* payload, uint64_t payload_len,
+                          float* h_out) {
+  return guard([&] {
+    check_gptq_args(cfg, opts, n, m);
+    validate(cfg);
+    const uint64_t ng = group_count(cfg, n, m), pb = storage_bytes(cfg, n, m);
+    if (payload && payload_len < pb) fail(OCWG_INVALID_INPUT, "payload buffer too small");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    std::vector<void*> bufs;
+    auto dalloc = [&](size_t b) {
+      void* p = nullptr;
+      ck(cudaMalloc(&p, std::max<size_t>(b, 1)), "cudaMalloc(io)");
+      bufs.push_back(p);
+      return p;
+    };
+    int r = OCWG_OK;
+    std::string msg;
+    try {
+      float* wd = static_cast<float*>(dalloc(n * m * 4));
+      uint16_t* xd = static_cast<uint16_t*>(dalloc(tokens * n * 2));
+      int16_t* cd = static_cast<int16_t*>(dalloc(n * m * 2));
+      float* sd = static_cast<float*>(dalloc(ng * 4));
+      int32_t* zd = static_cast<int32_t*>(dalloc(ng * 4));
+      float* whd = w_hat ? static_cast<float*>(dalloc(n * m * 4)) : nullptr;
+      uint8_t* pd = payload ? static_cast<uint8_t*>(dalloc(pb)) : nullptr;
+      float* hd = h_out ? static_cast<float*>(dalloc(n * n * 4)) : nullptr;
+      h2d(wd, w, n * m * 4, ctx);
+      h2d(xd, x, tokens * n * 2, ctx);
+      r = ocwg_quantize_layer_x_dev(ctx, wd, xd, tokens, n, m, cfg, opts, mode, cd, sd, zd, whd, pd,
+                                    hd);
+      msg = g_err;
+      if (r == OCWG_OK) {
+        d2h(codes, cd, n * m * 2, ctx);
+        d2h(scales, sd, ng * 4, ctx);
+        d2h(zeros, zd, ng * 4, ctx);
+        if (w_hat) d2h(w_hat, whd, n * m * 4, ctx);
+        if (payload) d2h(payload, pd, pb, ctx);
+        if (h_out) d2h(h_out, hd, n * n * 4, ctx);
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+      }
+    } catch (const Error& e) {
+      r = e.code;
+      msg = e.msg;
+    }
+    for (void* p : bufs) cudaFree(p);
+    if (r != OCWG_OK) fail(r, msg);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// Internal launch interface between the C-ABI host layer (capi.cu) and the
+// kernels.  All pointers are device pointers; all launches are async on
+// `st`.  Nothing here is exported from libocwg.so.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace ocwg {
+
+// Kernel launches issued by this library (for the bench's gpu_launches claim).
+void count_launches(unsigned long long n);
+unsigned long long launches_issued();
+
+// Device-side status word written by kernels (0 = ok).  Bits:
+enum DevFlag : unsigned {
+  kFlagNonFinite = 1u,     // calibrate_grids saw NaN/Inf   -> invalid_input
+  kFlagNotPD = 2u,         // Cholesky pivot <= 0 / NaN     -> numeric_error
+  kFlagEmptyGroup = 4u,    // never expected
+};
+
+// ---- grids / RTN / pack (quant.cu) -------------------------------------
+// Per-group min/max -> (scale, zero), minmax or 100-candidate MSE search
+// (quant.cpp:51-74, 96-140, 168-196).  W is rows x cols row-major fp32.
+void launch_calibrate_grids(const float* w, long long rows, long long cols, long long ld,
+                            const QCfg& c, int mse, float* scales, int32_t* zeros, unsigned* flag,
+                            float* ws_minmax, cudaStream_t st);
+// codes[i*cols+j] = quantize(w[i,j], grid(i,j)); optional w_hat (quant.cpp:198-210, 212-218)
+void launch_quantize_rtn(const float* w, long long rows, long long cols, long long ld,
+                         const QCfg& c,
+                         const float* scales, const int32_t* zeros, int16_t* codes,
+                         float* w_hat, cudaStream_t st);
+void launch_dequantize(const int16_t* codes, long long rows, long long cols, const QCfg& c,
+                       const float* scales, const int32_t* zeros, float* out, cudaStream_t st);
+// OCW1 uniform payload (container.cpp:15-35, 66-70, 129-139)
+void launch_pack(const int16_t* codes, long long n_codes, long long n_groups, const QCfg& c,
+                 const float* scales, const int32_t* zeros, uint8_t* out, cudaStream_t st);
+void launch_unpack(const uint8_t* payload, long long n_codes, long long n_groups, const QCfg& c,
+                   int16_t* codes, float* scales, int32_t* zeros, cudaStream_t st);
+// act-order: stable descending sort of diag(H) (layerwise.cpp:11-18)
+void launch_order(const float* h, long long n, int actorder, int32_t* order, cudaStream_t st);
+
+// ---- factorisation (factor.cu) -----------------------------------------
+// A = reversed-permuted, dampened fp64 copy of H (layerwise.cpp:31-41):
+//   A[i][j] = double(H[o(i)][o(j)]) + (i==j) * damp,  o(i) = order[n-1-i]
+// damp = percdamp * mean(diag(double(H))) computed on device into *damp.
+void launch_build_factor_input(const float* h, long long n, const int32_t* order,
+                               double percdamp, double* a, double* damp, cudaStream_t st);
+// In-place lower Cholesky of A (n x n, row-major, lower used), then
+// U = (J L J)^-1 written to u (n x n row-major upper, zero below).
+// Sets kFlagNotPD in *flag on breakdown.  ws: n*n doubles workspace.
+void factor_upper_inverse(double* a, long long n, double* u, double* ws, unsigned* flag,
+                          cudaStream_t st);
+// hinv = U^T U (parity artefact: (H_p + damp I)^-1 in processing order)
+void launch_gram_upper(const double* u, long long n, double* hinv, cudaStream_t st);
+
+// ---- generic fp64 GEMM (dgemm.cu) --------------------------------------
+// C[m x n] = beta*C + alpha * op(A) * op(B); op(A)[i][k] = A[i*lda + k] or
+// (transA) A[k*lda + i]; same for B.  lower_only: skip output tiles that lie
+// strictly above the diagonal.  A/B element type float or double.
+template <typename TA, typename TB>
+void dgemm(long long m, long long n, long long k, double alpha, const TA* a, long long lda,
+           bool ta, const TB* b, long long ldb, bool tb, double beta, double* c, long long ldc,
+           bool lower_only, cudaStream_t st);
+
+// ---- GPTQ sweep (sweep.cu) ---------------------------------------------
+// wp: n x m fp64 permuted working weights (rows in processing order)
+// w has row stride ldw; wp is contiguous n x m
+void launch_permute_rows_f64(const float* w, long long n, long long m, long long ldw,
+                             const int32_t* order, double* wp, cudaStream_t st);
+// codes / w_hat are written with row stride ldo (original row order)
+void gptq_sweep(double* wp, long long n, long long m, const double* u, const int32_t* order,
+                const QCfg& c, const float* scales, const int32_t* zeros, long long block,
+                int16_t* codes, float* w_hat, long long ldo, double* err_ws, cudaStream_t st);
+
+// ---- statistics (stats.cu, hessian_tc.cu) -------------------------------
+// fp64 accumulate_stats for fp32 inputs (stats.cpp:10-19): gram += Xp^T Xp,
+// cross += Xp^T (Xf - Xp).  diff_ws: rows*dim doubles.
+void accumulate_stats_f64(const float* x_fp, const float* x_pert, long long rows, long long dim,
+                          double* gram, double* cross, double* diff_ws, cudaStream_t st);
+// bf16 X (tokens x dim, row-major) -> H (dim x dim fp32, symmetric, full).
+// accumulate: H += X^T X else H = X^T X.  tcgen05/TMEM/TMA kernel.
+size_t hessian_tc_workspace_bytes(long long tokens, long long dim);
+int hessian_tc(const uint16_t* x, long long tokens, long long dim, float* h, int accumulate,
+               void* ws, size_t ws_bytes, cudaStream_t st);
+// SIMT cross-check kernel (same contract), used by tests to validate hessian_tc.
+void hessian_simt(const uint16_t* x, long long tokens, long long dim, float* h, int accumulate,
+                  cudaStream_t st);
+// fp32 -> bf16 (RNE) conversion, and "all values bf16-exact" check
+void launch_f32_to_bf16(const float* x, long long n, uint16_t* out, unsigned* inexact,
+                        cudaStream_t st);
+
+// ---- misc ----------------------------------------------------------------
+void launch_f64_to_f32(const double* in, long long n, float* out, cudaStream_t st);
+void launch_f32_to_f64(const float* in, long long n, double* out, cudaStream_t st);
+// objective: sum_ij D[i][j] * (H D)[i][j], D = w_hat - w (quant.cpp:230-236)
+void activation_objective(const float* w, const float* w_hat, const float* h, long long n,
+                          long long m, double* out_dev, double* ws, cudaStream_t st);
+
+}  // namespace ocwg

@@ -1,0 +1,394 @@
+// HBM-bound quantisation kernels: grid calibration, RTN quantise/dequantise,
+// OCW1 uniform payload pack/unpack and the act-order sort.
+// Reference: proj/src/quant.cpp, proj/src/container.cpp:15-35,129-139,168-199,
+// proj/src/layerwise.cpp:11-18.
+#include <cfloat>
+#include <cmath>
+
+#include "kernels.h"
+
+namespace ocwg {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+
+// warp-wide min/max of one segment w[base + k*stride], k < len
+struct Seg {
+  long long base, stride, len;
+};
+
+__device__ inline Seg segment_of(long long g, long long rows, long long cols, long long ld,
+                                const QCfg& c) {
+  if (c.gran == 0) return {0, 1, rows * cols};  // per-tensor requires ld == cols
+  if (c.gran == 1) return {g * ld, 1, cols};
+  const long long r = g / c.gpr, gg = g % c.gpr;
+  const long long j0 = gg * c.group;
+  const long long len = min(c.group, cols - j0);
+  return {r * ld + j0, 1, len};
+}
+
+// asymmetric_from_extremes / symmetric_from_extremes (quant.cpp:51-74)
+__device__ inline void grid_from_extremes(float lo, float hi, const QCfg& c, float& s, int& z) {
+  if (c.scheme == 1) {
+    if (hi == lo) {
+      s = 1.0f;
+      z = clamp_code((long long)ref_rint_to_int(__fsub_rn(float(c.qmin), lo)), c.qmin, c.qmax);
+      return;
+    }
+    s = positive_fp16(__fdiv_rn(__fsub_rn(hi, lo), float(c.qmax - c.qmin)));
+    z = clamp_code((long long)ref_rint_to_int(__fsub_rn(float(c.qmin), __fdiv_rn(lo, s))), c.qmin,
+                   c.qmax);
+  } else {
+    const float amax = fmaxf(fabsf(lo), fabsf(hi));
+    s = amax == 0.0f ? 1.0f : positive_fp16(__fdiv_rn(amax, float(c.qmax)));
+    z = 0;
+  }
+}
+
+// grid_sq_error (quant.cpp:85-92): fp64 sum in element order
+__device__ inline double seq_sq_error(const float* w, const Seg& sg, float s, int z, int qmin,
+                                      int qmax) {
+  double e = 0.0;
+  for (long long k = 0; k < sg.len; ++k) {
+    const float v = w[sg.base + k * sg.stride];
+    const float wh = dequantize_code(quantize_code(v, s, z, qmin, qmax), s, z);
+    const double d = double(__fsub_rn(v, wh));
+    e = __dadd_rn(e, __dmul_rn(d, d));
+  }
+  return e;
+}
+
+// One warp per group (per_group / per_channel).  Per-tensor goes through
+// the two-pass path below.
+__global__ void calibrate_groups_kernel(const float* __restrict__ w, long long rows,
+                                        long long cols, long long ld, QCfg c, int mse, long long ngroups,
+                                        float* scales, int32_t* zeros, unsigned* flag,
+                                        const float* pre_minmax) {
+  const long long g = (long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (g >= ngroups) return;
+  const unsigned lane = lane_id();
+  const Seg sg = segment_of(g, rows, cols, ld, c);
+  float lo, hi;
+  if (pre_minmax) {  // per-tensor: extremes from the two-pass reduction
+    lo = pre_minmax[0];
+    hi = pre_minmax[1];
+  } else {
+    lo = FLT_MAX;
+    hi = -FLT_MAX;
+    bool bad = false;
+    for (long long k = lane; k < sg.len; k += 32) {
+      const float v = w[sg.base + k * sg.stride];
+      bad |= !isfinite(v);
+      lo = fminf(lo, v);
+      hi = fmaxf(hi, v);
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0) atomicOr(flag, kFlagNonFinite);
+      return;
+    }
+    for (int o = 16; o; o >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+  }
+  float s;
+  int z;
+  grid_from_extremes(lo, hi, c, s, z);
+  if (mse) {
+    // calibrate_grid_mse (quant.cpp:114-140): candidates c = 0..99 split over
+    // lanes; each lane sums its candidate's error sequentially (same order as
+    // the reference), then first-strict-minimum selection.
+    const bool degenerate = c.scheme == 1 ? (hi == lo) : (fmaxf(fabsf(lo), fabsf(hi)) == 0.0f);
+    if (!degenerate) {
+      const float raw = c.scheme == 1
+                            ? __fdiv_rn(__fsub_rn(hi, lo), float(c.qmax - c.qmin))
+                            : __fdiv_rn(fmaxf(fabsf(lo), fabsf(hi)), float(c.qmax));
+      const double base_err = seq_sq_error(w, sg, s, z, c.qmin, c.qmax);
+      double best = INFINITY;
+      int best_c = 1 << 30;
+      float best_s = s;
+      int best_z = z;
+      for (int cand = lane; cand < 100; cand += 32) {
+        const float mult = __fadd_rn(0.3f, __fdiv_rn(__fmul_rn(0.7f, float(cand)), 99.0f));
+        const float cs = positive_fp16(__fmul_rn(mult, raw));
+        int cz = z;
+        if (c.scheme == 1)
+          cz = clamp_code((long long)ref_rint_to_int(__fsub_rn(float(c.qmin), __fdiv_rn(lo, cs))),
+                          c.qmin, c.qmax);
+        const double e = seq_sq_error(w, sg, cs, cz, c.qmin, c.qmax);
+        if (e < best) {  // candidates visited in increasing order per lane
+          best = e;
+          best_c = cand;
+          best_s = cs;
+          best_z = cz;
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, best_c, o);
+        const float os = __shfl_xor_sync(0xffffffffu, best_s, o);
+        const int oz = __shfl_xor_sync(0xffffffffu, best_z, o);
+        if (ob < best || (ob == best && oc < best_c)) {
+          best = ob;
+          best_c = oc;
+          best_s = os;
+          best_z = oz;
+        }
+      }
+      if (best < base_err) {
+        s = best_s;
+        z = best_z;
+      }
+    }
+  }
+  if (lane == 0) {
+    scales[g] = s;
+    zeros[g] = z;
+  }
+}
+
+// per-tensor extremes, pass 1: per-block partials; pass 2: one block
+__global__ void minmax_partial_kernel(const float* __restrict__ w, long long n, float* part,
+                                      unsigned* flag) {
+  float lo = FLT_MAX, hi = -FLT_MAX;
+  bool bad = false;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const float v = w[k];
+    bad |= !isfinite(v);
+    lo = fminf(lo, v);
+    hi = fmaxf(hi, v);
+  }
+  if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(flag, kFlagNonFinite);
+  for (int o = 16; o; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ float slo[32], shi[32];
+  const int wid = threadIdx.x >> 5;
+  if (lane_id() == 0) {
+    slo[wid] = lo;
+    shi[wid] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < int(blockDim.x >> 5); ++i) {
+      lo = fminf(lo, slo[i]);
+      hi = fmaxf(hi, shi[i]);
+    }
+    part[2 * blockIdx.x] = lo;
+    part[2 * blockIdx.x + 1] = hi;
+  }
+}
+
+__global__ void minmax_final_kernel(float* part, int nparts) {
+  if (threadIdx.x != 0) return;
+  float lo = part[0], hi = part[1];
+  for (int i = 1; i < nparts; ++i) {
+    lo = fminf(lo, part[2 * i]);
+    hi = fmaxf(hi, part[2 * i + 1]);
+  }
+  part[0] = lo;
+  part[1] = hi;
+}
+
+__global__ void quantize_rtn_kernel(const float* __restrict__ w, long long rows, long long cols,
+                                    long long ld, QCfg c, const float* __restrict__ scales,
+                                    const int32_t* __restrict__ zeros, int16_t* codes,
+                                    float* w_hat) {
+  const long long n = rows * cols;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / cols, j = e % cols;
+    const long long g = group_of(c, i, j);
+    const float s = scales[g];
+    const int z = zeros[g];
+    const long long o = i * ld + j;
+    const int q = quantize_code(w[o], s, z, c.qmin, c.qmax);
+    codes[o] = int16_t(q);
+    if (w_hat) w_hat[o] = dequantize_code(q, s, z);
+  }
+}
+
+__global__ void dequantize_kernel(const int16_t* __restrict__ codes, long long rows, long long cols,
+                                  QCfg c, const float* __restrict__ scales,
+                                  const int32_t* __restrict__ zeros, float* out) {
+  const long long n = rows * cols;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long g = group_of(c, e / cols, e % cols);
+    out[e] = dequantize_code(int(codes[e]), scales[g], zeros[g]);
+  }
+}
+
+// Pack: thread t owns codes [32t, 32t+32) = exactly 4*bits bytes of the
+// LSB-first stream (container.cpp:15-35 BitWriter); emitted as `bits`
+// 32-bit words.  The stream's final partial byte is zero-padded (flush()).
+__global__ void pack_codes_kernel(const int16_t* __restrict__ codes, long long n_codes, int bits,
+                                  int qmin, uint8_t* out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long c0 = t * 32;
+  if (c0 >= n_codes) return;
+  const uint32_t mask = (1u << bits) - 1u;
+  uint32_t words[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) words[i] = 0;
+  const int cnt = int(min(32LL, n_codes - c0));
+  for (int k = 0; k < cnt; ++k) {
+    const uint32_t v = uint32_t(int(codes[c0 + k]) - qmin) & mask;
+    const int bit = k * bits;
+    const int wi = bit >> 5, sh = bit & 31;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i == wi) words[i] |= v << sh;
+      if (i == wi + 1 && sh + bits > 32) words[i] |= v >> (32 - sh);
+    }
+  }
+  const long long byte0 = t * 4LL * bits;
+  const long long nbytes_total = (n_codes * bits + 7) / 8;
+  if (cnt == 32 && ((byte0 & 3) == 0)) {
+    uint32_t* o = reinterpret_cast<uint32_t*>(out + byte0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < bits) o[i] = words[i];
+  } else {
+    const long long nb = min(4LL * bits, nbytes_total - byte0);
+    for (long long b = 0; b < nb; ++b) out[byte0 + b] = uint8_t(words[b >> 2] >> (8 * (b & 3)));
+  }
+}
+
+__global__ void pack_meta_kernel(long long n_groups, int asym, const float* __restrict__ scales,
+                                 const int32_t* __restrict__ zeros, uint8_t* meta) {
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n_groups;
+       g += (long long)gridDim.x * blockDim.x) {
+    const uint16_t h = fp16_encode(scales[g]);  // put_fp16 (container.cpp:66-70)
+    meta[2 * g] = uint8_t(h & 0xff);
+    meta[2 * g + 1] = uint8_t(h >> 8);
+    if (asym) meta[2 * n_groups + g] = uint8_t(zeros[g]);
+  }
+}
+
+__global__ void unpack_codes_kernel(const uint8_t* __restrict__ in, long long n_codes, int bits,
+                                    int qmin, int16_t* codes) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n_codes;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long bit = e * bits;
+    const long long byte = bit >> 3;
+    const int sh = int(bit & 7);
+    uint32_t v = in[byte];
+    if (sh + bits > 8) v |= uint32_t(in[byte + 1]) << 8;
+    codes[e] = int16_t(int((v >> sh) & ((1u << bits) - 1u)) + qmin);
+  }
+}
+
+__global__ void unpack_meta_kernel(const uint8_t* __restrict__ meta, long long n_groups, int asym,
+                                   float* scales, int32_t* zeros) {
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n_groups;
+       g += (long long)gridDim.x * blockDim.x) {
+    scales[g] = fp16_decode(uint16_t(meta[2 * g] | (uint16_t(meta[2 * g + 1]) << 8)));
+    zeros[g] = asym ? int(meta[2 * n_groups + g]) : 0;
+  }
+}
+
+// Stable descending rank of diag(H): rank_i = #{j: d_j > d_i} + #{j < i: d_j == d_i}.
+// O(n^2) comparisons, tiled through shared memory; bit-exact with
+// std::stable_sort(order, h[a][a] > h[b][b]) for NaN-free diagonals.
+__global__ void order_rank_kernel(const float* __restrict__ h, long long n, int32_t* order) {
+  __shared__ float tile[1024];
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const float di = i < n ? h[i * n + i] : 0.0f;
+  long long rank = 0;
+  for (long long j0 = 0; j0 < n; j0 += 1024) {
+    __syncthreads();
+    for (long long t = threadIdx.x; t < 1024 && j0 + t < n; t += blockDim.x)
+      tile[t] = h[(j0 + t) * n + (j0 + t)];
+    __syncthreads();
+    const long long cnt = min(1024LL, n - j0);
+    if (i < n)
+      for (long long t = 0; t < cnt; ++t) {
+        const float dj = tile[t];
+        rank += (dj > di) || (dj == di && j0 + t < i);
+      }
+  }
+  if (i < n) order[rank] = int32_t(i);
+}
+
+__global__ void iota_kernel(long long n, int32_t* order) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    order[i] = int32_t(i);
+}
+
+inline int grid_for(long long n, int threads, int cap = 148 * 16) {
+  long long g = (n + threads - 1) / threads;
+  return int(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+void launch_calibrate_grids(const float* w, long long rows, long long cols, long long ld,
+                            const QCfg& c, int mse, float* scales, int32_t* zeros, unsigned* flag, float* ws_minmax,
+                            cudaStream_t st) {
+  const long long ng = c.gran == 0 ? 1 : (c.gran == 1 ? rows : rows * c.gpr);
+  const float* pre = nullptr;
+  if (c.gran == 0) {
+    const int parts = grid_for(rows * cols, 256, 512);
+    minmax_partial_kernel<<<parts, 256, 0, st>>>(w, rows * cols, ws_minmax, flag);
+    minmax_final_kernel<<<1, 32, 0, st>>>(ws_minmax, parts);
+    pre = ws_minmax;
+    count_launches(2);
+  }
+  count_launches(1);
+  const int blocks = int((ng + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  calibrate_groups_kernel<<<blocks, 32 * kWarpsPerBlock, 0, st>>>(w, rows, cols, ld, c, mse, ng, scales,
+                                                                  zeros, flag, pre);
+}
+
+void launch_quantize_rtn(const float* w, long long rows, long long cols, long long ld,
+                         const QCfg& c, const float* scales, const int32_t* zeros, int16_t* codes,
+                         float* w_hat, cudaStream_t st) {
+  count_launches(1);
+  quantize_rtn_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(w, rows, cols, ld, c, scales,
+                                                                   zeros, codes, w_hat);
+}
+
+void launch_dequantize(const int16_t* codes, long long rows, long long cols, const QCfg& c,
+                       const float* scales, const int32_t* zeros, float* out, cudaStream_t st) {
+  count_launches(1);
+  dequantize_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(codes, rows, cols, c, scales, zeros,
+                                                                 out);
+}
+
+void launch_pack(const int16_t* codes, long long n_codes, long long n_groups, const QCfg& c,
+                 const float* scales, const int32_t* zeros, uint8_t* out, cudaStream_t st) {
+  count_launches(2);
+  const long long threads = (n_codes + 31) / 32;
+  if (threads > 0)
+    pack_codes_kernel<<<int((threads + 255) / 256), 256, 0, st>>>(codes, n_codes, c.bits, c.qmin,
+                                                                  out);
+  const long long code_bytes = (n_codes * c.bits + 7) / 8;
+  pack_meta_kernel<<<grid_for(n_groups, 256), 256, 0, st>>>(n_groups, c.scheme == 1, scales, zeros,
+                                                             out + code_bytes);
+}
+
+void launch_unpack(const uint8_t* payload, long long n_codes, long long n_groups, const QCfg& c,
+                   int16_t* codes, float* scales, int32_t* zeros, cudaStream_t st) {
+  count_launches(2);
+  unpack_codes_kernel<<<grid_for(n_codes, 256), 256, 0, st>>>(payload, n_codes, c.bits, c.qmin,
+                                                               codes);
+  const long long code_bytes = (n_codes * c.bits + 7) / 8;
+  unpack_meta_kernel<<<grid_for(n_groups, 256), 256, 0, st>>>(payload + code_bytes, n_groups,
+                                                               c.scheme == 1, scales, zeros);
+}
+
+void launch_order(const float* h, long long n, int actorder, int32_t* order, cudaStream_t st) {
+  count_launches(1);
+  if (!actorder) {
+    iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, order);
+    return;
+  }
+  order_rank_kernel<<<int((n + 255) / 256), 256, 0, st>>>(h, n, order);
+}
+
+}  // namespace ocwg

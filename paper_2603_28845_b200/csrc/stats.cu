@@ -1,0 +1,150 @@
+// Calibration statistics for the general (fp32-input) API, plus small
+// conversion / metric kernels.
+//   accumulate_stats_f64: stats.cpp:10-19 in fp64 (gram += Xp^T Xp,
+//                         cross += Xp^T (X - Xp)), on the FP64 pipe.
+//   hessian_simt:         fp64-accumulated X^T X of bf16 X, a test-only
+//                         cross-check for the tcgen05 kernel (hessian_tc.cu).
+#include "kernels.h"
+
+namespace ocwg {
+namespace {
+
+inline int blocks_for(long long n) {
+  long long g = (n + 255) / 256;
+  return int(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
+}
+
+__global__ void diff_kernel(const float* __restrict__ xf, const float* __restrict__ xp, long long n,
+                            double* d) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    d[e] = __dsub_rn(double(xf[e]), double(xp[e]));
+}
+
+__device__ inline float bf16_to_f32(uint16_t v) { return __uint_as_float(uint32_t(v) << 16); }
+
+// 32x32 output tile per block, fp64 accumulation over all tokens
+__global__ void hessian_simt_kernel(const uint16_t* __restrict__ x, long long t, long long d,
+                                    float* h, int accumulate) {
+  __shared__ float xa[32][33], xb[32][33];
+  const long long i0 = (long long)blockIdx.y * 32, j0 = (long long)blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  double acc[4] = {0, 0, 0, 0};
+  for (long long k0 = 0; k0 < t; k0 += 32) {
+    for (int r = ty; r < 32; r += 8) {
+      const long long k = k0 + r;
+      xa[r][tx] = (k < t && i0 + tx < d) ? bf16_to_f32(x[k * d + i0 + tx]) : 0.f;
+      xb[r][tx] = (k < t && j0 + tx < d) ? bf16_to_f32(x[k * d + j0 + tx]) : 0.f;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < 32; ++kk)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        acc[q] += double(xa[kk][ty + 8 * q]) * double(xb[kk][tx]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const long long i = i0 + ty + 8 * q, j = j0 + tx;
+    if (i < d && j < d) {
+      float* p = h + i * d + j;
+      *p = accumulate ? float(double(*p) + acc[q]) : float(acc[q]);
+    }
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ x, long long n, uint16_t* out,
+                                   unsigned* inexact) {
+  bool bad = false;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const uint32_t u = __float_as_uint(x[e]);
+    const uint32_t lsb = (u >> 16) & 1u;
+    const uint32_t r = u + 0x7fffu + lsb;  // RNE (finite inputs)
+    out[e] = uint16_t(r >> 16);
+    bad |= (u & 0xffffu) != 0 || !isfinite(x[e]);
+  }
+  if (inexact && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(inexact, 1u);
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ in, long long n, float* out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = float(in[e]);
+}
+__global__ void f32_to_f64_kernel(const float* __restrict__ in, long long n, double* out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = double(in[e]);
+}
+
+__global__ void delta_kernel(const float* __restrict__ w, const float* __restrict__ wh, long long n,
+                             double* d) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    d[e] = __dsub_rn(double(wh[e]), double(w[e]));
+}
+
+// out = sum_e a[e]*b[e] (single block, fixed order -> deterministic)
+__global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                           double* out) {
+  __shared__ double part[32];
+  double s = 0.0;
+  for (long long e = threadIdx.x; e < n; e += blockDim.x) s += a[e] * b[e];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += part[w];
+    *out = t;
+  }
+}
+
+}  // namespace
+
+void accumulate_stats_f64(const float* x_fp, const float* x_pert, long long rows, long long dim,
+                          double* gram, double* cross, double* diff_ws, cudaStream_t st) {
+  dgemm<float, float>(dim, dim, rows, 1.0, x_pert, dim, true, x_pert, dim, false, 1.0, gram, dim,
+                      false, st);
+  if (cross) {
+    count_launches(1);
+    diff_kernel<<<blocks_for(rows * dim), 256, 0, st>>>(x_fp, x_pert, rows * dim, diff_ws);
+    dgemm<float, double>(dim, dim, rows, 1.0, x_pert, dim, true, diff_ws, dim, false, 1.0, cross,
+                         dim, false, st);
+  }
+}
+
+void hessian_simt(const uint16_t* x, long long tokens, long long dim, float* h, int accumulate,
+                  cudaStream_t st) {
+  dim3 grid(unsigned((dim + 31) / 32), unsigned((dim + 31) / 32));
+  count_launches(1);
+  hessian_simt_kernel<<<grid, 256, 0, st>>>(x, tokens, dim, h, accumulate);
+}
+
+void launch_f32_to_bf16(const float* x, long long n, uint16_t* out, unsigned* inexact,
+                        cudaStream_t st) {
+  count_launches(1);
+  f32_to_bf16_kernel<<<blocks_for(n), 256, 0, st>>>(x, n, out, inexact);
+}
+void launch_f64_to_f32(const double* in, long long n, float* out, cudaStream_t st) {
+  count_launches(1);
+  f64_to_f32_kernel<<<blocks_for(n), 256, 0, st>>>(in, n, out);
+}
+void launch_f32_to_f64(const float* in, long long n, double* out, cudaStream_t st) {
+  count_launches(1);
+  f32_to_f64_kernel<<<blocks_for(n), 256, 0, st>>>(in, n, out);
+}
+
+// ws: 2*n*m doubles
+void activation_objective(const float* w, const float* w_hat, const float* h, long long n,
+                          long long m, double* out_dev, double* ws, cudaStream_t st) {
+  double* d = ws;
+  double* hd = ws + n * m;
+  count_launches(2);
+  delta_kernel<<<blocks_for(n * m), 256, 0, st>>>(w, w_hat, n * m, d);
+  dgemm<float, double>(n, m, n, 1.0, h, n, false, d, m, false, 0.0, hd, m, false, st);
+  dot_kernel<<<1, 1024, 0, st>>>(d, hd, n * m, out_dev);
+}
+
+}  // namespace ocwg

@@ -1,0 +1,84 @@
+"""Device-resident entry points (inputs already in HBM), for the sharded /
+multi-GPU driver and the benchmark.  Tensors are torch CUDA tensors used
+purely as device memory + stream plumbing; all compute is libocwg.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import (GptqOptions, QuantConfig, ScaleMode, _check, context, lib, quant_group_count,
+               uniform_storage_bytes)
+
+
+def _bind_stream(device: int):
+    ctx = context(device)
+    _check(lib().ocwg_set_stream(ctx.handle, C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+    return ctx
+
+
+class LayerBuffers:
+    """Output buffers of one layer quantize, allocated once (N x M)."""
+
+    def __init__(self, n: int, m: int, cfg: QuantConfig, device: int, w_hat: bool = True,
+                 payload: bool = True):
+        dev = torch.device("cuda", device)
+        ng = quant_group_count(cfg, n, m)
+        self.codes = torch.empty((n, m), dtype=torch.int16, device=dev)
+        self.scales = torch.empty(ng, dtype=torch.float32, device=dev)
+        self.zeros = torch.empty(ng, dtype=torch.int32, device=dev)
+        self.w_hat = torch.empty((n, m), dtype=torch.float32, device=dev) if w_hat else None
+        self.payload_bytes = uniform_storage_bytes(cfg, n, m)
+        self.payload = torch.empty(self.payload_bytes, dtype=torch.uint8, device=dev) if payload else None
+        self.h = torch.empty((n, n), dtype=torch.float32, device=dev)
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def hessian(x_bf16: torch.Tensor, h: torch.Tensor, accumulate: bool = False) -> None:
+    """H (+)= X^T X on the tensor cores (tcgen05)."""
+    t, n = x_bf16.shape
+    ctx = _bind_stream(x_bf16.device.index)
+    _check(lib().ocwg_hessian_bf16_dev(ctx.handle, _p(x_bf16), t, n, _p(h), int(accumulate)))
+
+
+def gptq(w: torch.Tensor, h: torch.Tensor, cfg: QuantConfig, opts: GptqOptions, out: LayerBuffers,
+         mode: ScaleMode = ScaleMode.minmax, col0: int = 0, ncols: int | None = None) -> None:
+    """GPTQ on (a group-aligned column slab of) a device-resident W."""
+    n, m = w.shape
+    ncols = m - col0 if ncols is None else ncols
+    ctx = _bind_stream(w.device.index)
+    c, o = cfg._c(), opts._c()
+    esz = 4
+    w_ptr = C.c_void_p(w.data_ptr() + col0 * esz)
+    codes_ptr = C.c_void_p(out.codes.data_ptr() + col0 * 2)
+    wh_ptr = None if out.w_hat is None else C.c_void_p(out.w_hat.data_ptr() + col0 * 4)
+    _check(lib().ocwg_gptq_quantize_dev(ctx.handle, w_ptr, m, _p(h), n, ncols, C.byref(c), C.byref(o),
+                                        int(mode), codes_ptr, _p(out.scales), _p(out.zeros), wh_ptr))
+
+
+def pack(out: LayerBuffers, cfg: QuantConfig) -> None:
+    n, m = out.codes.shape
+    ctx = _bind_stream(out.codes.device.index)
+    c = cfg._c()
+    _check(lib().ocwg_pack_uniform_dev(ctx.handle, _p(out.codes), _p(out.scales), _p(out.zeros), n, m,
+                                       C.byref(c), _p(out.payload)))
+
+
+def quantize_layer_x(w: torch.Tensor, x_bf16: torch.Tensor, cfg: QuantConfig, opts: GptqOptions,
+                     out: LayerBuffers, mode: ScaleMode = ScaleMode.minmax) -> None:
+    """One call: Hessian -> factorisation -> GPTQ sweep -> pack, all on device."""
+    n, m = w.shape
+    ctx = _bind_stream(w.device.index)
+    c, o = cfg._c(), opts._c()
+    _check(lib().ocwg_quantize_layer_x_dev(ctx.handle, _p(w), _p(x_bf16), x_bf16.shape[0], n, m,
+                                           C.byref(c), C.byref(o), int(mode), _p(out.codes),
+                                           _p(out.scales), _p(out.zeros), _p(out.w_hat),
+                                           _p(out.payload), _p(out.h)))
+
+
+def launch_count() -> int:
+    return int(lib().ocwg_launch_count(None))
