@@ -52,6 +52,11 @@ extern "C" {
 #define OCWG_MINMAX 0
 #define OCWG_MSE_GRID 1
 
+/* arithmetic of the factorisation + GPTQ sweep (the reference uses fp64,
+ * layerwise.cpp:31-90; fp32 keeps >= 99.99 % identical codes) */
+#define OCWG_FP32 0
+#define OCWG_FP64 1
+
 /* QuantConfig (quant.hpp:21-28) */
 typedef struct ocwg_quant_config {
   int32_t bits;        /* [1, 8] */
@@ -77,6 +82,8 @@ int ocwg_version(void);
 /* Context on one CUDA device: stream, workspace pool, device status word. */
 int ocwg_create(int device, ocwg_ctx** out);
 int ocwg_destroy(ocwg_ctx* ctx);
+/* OCWG_FP32 (default, fast) or OCWG_FP64 (reference arithmetic class). */
+int ocwg_set_precision(ocwg_ctx* ctx, int precision);
 /* Run subsequent work on an external cudaStream_t (NULL = the context's own). */
 int ocwg_set_stream(ocwg_ctx* ctx, void* cuda_stream);
 int ocwg_synchronize(ocwg_ctx* ctx);

@@ -179,6 +179,7 @@ _SIGS = {
     "ocwg_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
     "ocwg_destroy": (C.c_int, [_P]),
     "ocwg_set_stream": (C.c_int, [_P, _P]),
+    "ocwg_set_precision": (C.c_int, [_P, C.c_int]),
     "ocwg_synchronize": (C.c_int, [_P]),
     "ocwg_validate_config": (C.c_int, [C.POINTER(_QCfg)]),
     "ocwg_group_count": (_U64, [C.POINTER(_QCfg), _U64, _U64]),
@@ -261,6 +262,15 @@ def context(device: int = 0) -> Context:
     if device not in _contexts:
         _contexts[device] = Context(device)
     return _contexts[device]
+
+
+FP32, FP64 = 0, 1
+
+
+def set_precision(precision: int, device: int = 0) -> None:
+    """Arithmetic of the factorisation + GPTQ sweep: FP32 (default, fast) or
+    FP64 (the reference's arithmetic class, layerwise.cpp:31-90)."""
+    _check(lib().ocwg_set_precision(context(device).handle, int(precision)))
 
 
 def _ptr(a: np.ndarray | None):

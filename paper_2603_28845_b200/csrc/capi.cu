@@ -30,6 +30,7 @@ struct ocwg_ctx {
   size_t ws_bytes = 0;
   unsigned* flag = nullptr;  // device status word
   unsigned* flag_host = nullptr;
+  int precision = OCWG_FP32;  // factorisation + sweep arithmetic
   std::mutex mu;
 };
 
@@ -163,36 +164,59 @@ void d2h(void* h, const void* d, size_t bytes, ocwg_ctx* ctx) {
 struct GptqBufs {
   int32_t* order;
   double* damp;
-  double* a;
-  double* u;
-  double* fws;
-  double* wp;
-  double* err;
+  void* a;    // n x n  T
+  void* u;    // n x n  T
+  void* fws;  // nblk*64*64 + n*n  T
+  void* wp;   // n x m  T
+  void* err;  // 128 x m T
 };
 
-size_t gptq_reserve(Arena& ar, uint64_t n, uint64_t m, size_t* o) {
+void gptq_reserve(Arena& ar, uint64_t n, uint64_t m, int precision, size_t* o) {
   const uint64_t nblk = (n + 63) / 64;
+  const size_t es = precision == OCWG_FP64 ? 8 : 4;
   o[0] = ar.reserve(n * sizeof(int32_t));
   o[1] = ar.reserve(sizeof(double));
-  o[2] = ar.reserve(n * n * sizeof(double));
-  o[3] = ar.reserve(n * n * sizeof(double));
-  o[4] = ar.reserve((nblk * 64 * 64 + n * n) * sizeof(double));
-  o[5] = ar.reserve(n * m * sizeof(double));
-  o[6] = ar.reserve(128 * m * sizeof(double));
-  return 7;
+  o[2] = ar.reserve(n * n * es);
+  o[3] = ar.reserve(n * n * es);
+  o[4] = ar.reserve((nblk * 64 * 64 + n * n) * es);
+  o[5] = ar.reserve(n * m * es);
+  o[6] = ar.reserve(kMaxSweepBlock * m * es);
 }
 GptqBufs gptq_bufs(const Arena& ar, const size_t* o) {
-  return {ar.at<int32_t>(o[0]), ar.at<double>(o[1]), ar.at<double>(o[2]), ar.at<double>(o[3]),
-          ar.at<double>(o[4]), ar.at<double>(o[5]), ar.at<double>(o[6])};
+  return {ar.at<int32_t>(o[0]), ar.at<double>(o[1]), ar.at<void>(o[2]), ar.at<void>(o[3]),
+          ar.at<void>(o[4]), ar.at<void>(o[5]), ar.at<void>(o[6])};
+}
+
+template <typename T>
+void run_factor_t(ocwg_ctx* ctx, const float* h_dev, uint64_t n, int actorder, double percdamp,
+                  const GptqBufs& b) {
+  cudaStream_t st = ctx->stream;
+  launch_order(h_dev, (long long)n, actorder, b.order, st);
+  launch_build_factor_input<T>(h_dev, (long long)n, b.order, percdamp, static_cast<T*>(b.a), b.damp,
+                               st);
+  factor_upper_inverse<T>(static_cast<T*>(b.a), (long long)n, static_cast<T*>(b.u),
+                          static_cast<T*>(b.fws), ctx->flag, st);
 }
 
 // order + damp + factorisation -> U (device); the reference's :29-51
 void run_factor(ocwg_ctx* ctx, const float* h_dev, uint64_t n, int actorder, double percdamp,
                 const GptqBufs& b) {
+  if (ctx->precision == OCWG_FP64)
+    run_factor_t<double>(ctx, h_dev, n, actorder, percdamp, b);
+  else
+    run_factor_t<float>(ctx, h_dev, n, actorder, percdamp, b);
+}
+
+template <typename T>
+void run_sweep_t(ocwg_ctx* ctx, const float* w, uint64_t ldw, uint64_t n, uint64_t m, const QCfg& c,
+                 const ocwg_gptq_options* opts, int16_t* codes, const float* scales,
+                 const int32_t* zeros, float* w_hat, const GptqBufs& b) {
   cudaStream_t st = ctx->stream;
-  launch_order(h_dev, (long long)n, actorder, b.order, st);
-  launch_build_factor_input(h_dev, (long long)n, b.order, percdamp, b.a, b.damp, st);
-  factor_upper_inverse(b.a, (long long)n, b.u, b.fws, ctx->flag, st);
+  launch_permute_rows<T>(w, (long long)n, (long long)m, (long long)ldw, b.order,
+                         static_cast<T*>(b.wp), st);
+  gptq_sweep<T>(static_cast<T*>(b.wp), (long long)n, (long long)m, static_cast<const T*>(b.u),
+                b.order, c, scales, zeros, (long long)opts->block_cols, codes, w_hat,
+                (long long)ldw, static_cast<T*>(b.err), st);
 }
 
 // gptq_quantize on device buffers (w row stride ldw; codes/w_hat stride ldw)
@@ -200,14 +224,14 @@ void run_gptq(ocwg_ctx* ctx, const float* w, uint64_t ldw, const float* h_dev, u
               uint64_t m, const ocwg_quant_config* cfg, const ocwg_gptq_options* opts, int mode,
               int16_t* codes, float* scales, int32_t* zeros, float* w_hat, const GptqBufs& b,
               float* mm_ws) {
-  cudaStream_t st = ctx->stream;
   const QCfg c = qcfg(cfg, m);
   run_factor(ctx, h_dev, n, opts->actorder, opts->percdamp, b);
   launch_calibrate_grids(w, (long long)n, (long long)m, (long long)ldw, c, mode, scales, zeros,
-                         ctx->flag, mm_ws, st);
-  launch_permute_rows_f64(w, (long long)n, (long long)m, (long long)ldw, b.order, b.wp, st);
-  gptq_sweep(b.wp, (long long)n, (long long)m, b.u, b.order, c, scales, zeros,
-             (long long)opts->block_cols, codes, w_hat, (long long)ldw, b.err, st);
+                         ctx->flag, mm_ws, ctx->stream);
+  if (ctx->precision == OCWG_FP64)
+    run_sweep_t<double>(ctx, w, ldw, n, m, c, opts, codes, scales, zeros, w_hat, b);
+  else
+    run_sweep_t<float>(ctx, w, ldw, n, m, c, opts, codes, scales, zeros, w_hat, b);
 }
 
 void check_gptq_args(const ocwg_quant_config* cfg, const ocwg_gptq_options* opts, uint64_t n,
@@ -254,6 +278,16 @@ int ocwg_destroy(ocwg_ctx* ctx) {
     cudaFreeHost(ctx->flag_host);
     cudaStreamDestroy(ctx->own);
     delete ctx;
+  });
+}
+
+int ocwg_set_precision(ocwg_ctx* ctx, int precision) {
+  return guard([&] {
+    if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
+    if (precision != OCWG_FP32 && precision != OCWG_FP64)
+      fail(OCWG_INVALID_INPUT, "precision must be OCWG_FP32 or OCWG_FP64");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->precision = precision;
   });
 }
 
@@ -547,16 +581,27 @@ int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, do
     begin(ctx);
     Arena ar(ctx);
     size_t o[8];
-    gptq_reserve(ar, n, 1, o);
-    const size_t oh = ar.reserve(n * n * 4), ohi = ar.reserve(n * n * 8);
+    gptq_reserve(ar, n, 1, ctx->precision, o);
+    const size_t oh = ar.reserve(n * n * 4), ohi = ar.reserve(n * n * 8),
+                 ou64 = ar.reserve(n * n * 8);
     ar.commit();
     const GptqBufs b = gptq_bufs(ar, o);
     h2d(ar.at<float>(oh), h, n * n * 4, ctx);
     run_factor(ctx, ar.at<float>(oh), n, actorder, percdamp, b);
-    if (hinv) launch_gram_upper(b.u, (long long)n, ar.at<double>(ohi), ctx->stream);
+    if (ctx->precision == OCWG_FP64) {
+      if (hinv) launch_gram_upper<double>(static_cast<double*>(b.u), (long long)n,
+                                          ar.at<double>(ohi), ctx->stream);
+      d2h(u, b.u, n * n * 8, ctx);
+    } else {
+      if (hinv) launch_gram_upper<float>(static_cast<float*>(b.u), (long long)n,
+                                         ar.at<double>(ohi), ctx->stream);
+      // U is fp32 on the fast path: widen for the fp64 ABI
+      launch_f32_to_f64(static_cast<float*>(b.u), (long long)(n * n), ar.at<double>(ou64),
+                        ctx->stream);
+      d2h(u, ar.at<double>(ou64), n * n * 8, ctx);
+    }
     std::vector<int32_t> ord(n);
     d2h(ord.data(), b.order, n * 4, ctx);
-    d2h(u, b.u, n * n * 8, ctx);
     d2h(hinv, ar.at<double>(ohi), n * n * 8, ctx);
     d2h(damp, b.damp, 8, ctx);
     finish(ctx);
@@ -575,7 +620,7 @@ int ocwg_gptq_quantize_dev(ocwg_ctx* ctx, const float* w, uint64_t ldw, const fl
     begin(ctx);
     Arena ar(ctx);
     size_t o[8];
-    gptq_reserve(ar, n, m, o);
+    gptq_reserve(ar, n, m, ctx->precision, o);
     const size_t om = ar.reserve(4096 * 4);
     ar.commit();
     if (n && m)
@@ -665,7 +710,7 @@ int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, 
     const uint64_t ng = group_count(cfg, n, m);
     Arena ar(ctx);
     size_t o[8];
-    gptq_reserve(ar, n, m, o);
+    gptq_reserve(ar, n, m, ctx->precision, o);
     const size_t om = ar.reserve(4096 * 4);
     const size_t oh = ar.reserve(n * n * 4);
     const size_t hws = hessian_tc_workspace_bytes((long long)tokens, (long long)n);

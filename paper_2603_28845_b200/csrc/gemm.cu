@@ -1,0 +1,157 @@
+// SIMT GEMM for the factorisation and the GPTQ trailing update, templated on
+// the compute type T (float: default fast path; double: reference-exact
+// arithmetic class, the reference runs GPTQ in Eigen MatrixXd).
+//
+//   C[m x n] = beta*C + alpha * op(A) * op(B)
+//   op(A)[i][k] = ta ? A[k*lda + i] : A[i*lda + k]   (same for B with tb)
+//
+// fp32: 128x128 CTA tile, BK 8, 256 threads, 8x8 outputs per thread.
+// fp64: 64x64 CTA tile, BK 16, 256 threads, 4x4 outputs per thread.
+// Thread->element mapping is strided so shared-memory reads broadcast;
+// tiles are double buffered through registers.
+#include "kernels.h"
+
+namespace ocwg {
+namespace {
+
+template <typename T>
+struct Tile;
+template <>
+struct Tile<float> {
+  static constexpr int BM = 128, BN = 128, BK = 8, TM = 8, TN = 8;
+};
+template <>
+struct Tile<double> {
+  static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
+};
+
+template <typename T, typename S>
+__device__ __forceinline__ T ldg_as(const S* p) {
+  return T(__ldg(p));
+}
+
+template <typename T, typename TA, typename TB>
+__global__ void __launch_bounds__(256) gemm_kernel(long long m, long long n, long long k, T alpha,
+                                                   const TA* __restrict__ a, long long lda, int ta,
+                                                   const TB* __restrict__ b, long long ldb, int tb,
+                                                   T beta, T* __restrict__ c, long long ldc,
+                                                   int lower_only) {
+  constexpr int BM = Tile<T>::BM, BN = Tile<T>::BN, BK = Tile<T>::BK;
+  constexpr int TM = Tile<T>::TM, TN = Tile<T>::TN;
+  constexpr int TX = BN / TN, TY = BM / TM;  // 16 x 16 threads
+  static_assert(TX * TY == 256, "256 threads");
+  constexpr int LA = BM * BK / 256, LB = BN * BK / 256;  // loads per thread per k-tile
+  const long long row0 = (long long)blockIdx.y * BM, col0 = (long long)blockIdx.x * BN;
+  if (lower_only && col0 > row0 + BM - 1) return;
+  __shared__ T As[2][BK][BM + 4];
+  __shared__ T Bs[2][BK][BN + 4];
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+
+  T ra[LA], rb[LB];
+  auto load = [&](long long k0) {
+#pragma unroll
+    for (int q = 0; q < LA; ++q) {
+      const int l = tid + q * 256;
+      int ii, kk;
+      if (ta) { ii = l % BM; kk = l / BM; } else { ii = l / BK; kk = l % BK; }
+      const long long gi = row0 + ii, gk = k0 + kk;
+      T v = T(0);
+      if (gi < m && gk < k) v = ta ? ldg_as<T>(a + gk * lda + gi) : ldg_as<T>(a + gi * lda + gk);
+      ra[q] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int l = tid + q * 256;
+      int jj, kk;
+      if (tb) { jj = l / BK; kk = l % BK; } else { jj = l % BN; kk = l / BN; }
+      const long long gj = col0 + jj, gk = k0 + kk;
+      T v = T(0);
+      if (gj < n && gk < k) v = tb ? ldg_as<T>(b + gj * ldb + gk) : ldg_as<T>(b + gk * ldb + gj);
+      rb[q] = v;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < LA; ++q) {
+      const int l = tid + q * 256;
+      int ii, kk;
+      if (ta) { ii = l % BM; kk = l / BM; } else { ii = l / BK; kk = l % BK; }
+      As[buf][kk][ii] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int l = tid + q * 256;
+      int jj, kk;
+      if (tb) { jj = l / BK; kk = l % BK; } else { jj = l % BN; kk = l / BN; }
+      Bs[buf][kk][jj] = rb[q];
+    }
+  };
+
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+  const long long nk = (k + BK - 1) / BK;
+  if (nk > 0) {
+    load(0);
+    store(0);
+  }
+  __syncthreads();
+  for (long long kt = 0; kt < nk; ++kt) {
+    const int buf = int(kt & 1);
+    if (kt + 1 < nk) load((kt + 1) * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T av[TM], bv[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) av[i] = As[buf][kk][ty + TY * i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) bv[j] = Bs[buf][kk][tx + TX * j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) store(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const long long gi = row0 + ty + TY * i;
+    if (gi >= m) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const long long gj = col0 + tx + TX * j;
+      if (gj >= n) continue;
+      T* p = c + gi * ldc + gj;
+      *p = beta == T(0) ? alpha * acc[i][j] : fma(alpha, acc[i][j], beta * *p);
+    }
+  }
+}
+
+}  // namespace
+
+template <typename T, typename TA, typename TB>
+void gemm(long long m, long long n, long long k, double alpha, const TA* a, long long lda, bool ta,
+          const TB* b, long long ldb, bool tb, double beta, T* c, long long ldc, bool lower_only,
+          cudaStream_t st) {
+  if (m <= 0 || n <= 0) return;
+  constexpr int BM = Tile<T>::BM, BN = Tile<T>::BN;
+  dim3 grid(unsigned((n + BN - 1) / BN), unsigned((m + BM - 1) / BM));
+  count_launches(1);
+  gemm_kernel<T, TA, TB><<<grid, 256, 0, st>>>(m, n, k, T(alpha), a, lda, ta ? 1 : 0, b, ldb,
+                                               tb ? 1 : 0, T(beta), c, ldc, lower_only ? 1 : 0);
+}
+
+#define OCWG_GEMM_INST(T, TA, TB)                                                              \
+  template void gemm<T, TA, TB>(long long, long long, long long, double, const TA*, long long, \
+                                bool, const TB*, long long, bool, double, T*, long long, bool, \
+                                cudaStream_t);
+OCWG_GEMM_INST(double, double, double)
+OCWG_GEMM_INST(double, float, float)
+OCWG_GEMM_INST(double, float, double)
+OCWG_GEMM_INST(float, float, float)
+
+}  // namespace ocwg

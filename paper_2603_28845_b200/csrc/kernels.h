@@ -43,38 +43,43 @@ void launch_unpack(const uint8_t* payload, long long n_codes, long long n_groups
 // act-order: stable descending sort of diag(H) (layerwise.cpp:11-18)
 void launch_order(const float* h, long long n, int actorder, int32_t* order, cudaStream_t st);
 
-// ---- factorisation (factor.cu) -----------------------------------------
-// A = reversed-permuted, dampened fp64 copy of H (layerwise.cpp:31-41):
-//   A[i][j] = double(H[o(i)][o(j)]) + (i==j) * damp,  o(i) = order[n-1-i]
+// ---- factorisation (factor.cu), T = float (default) or double ---------------
+// A = reversed-permuted, dampened copy of H (layerwise.cpp:31-41):
+//   A[i][j] = T(double(H[o(i)][o(j)]) + (i==j) * damp),  o(i) = order[n-1-i]
 // damp = percdamp * mean(diag(double(H))) computed on device into *damp.
+template <typename T>
 void launch_build_factor_input(const float* h, long long n, const int32_t* order,
-                               double percdamp, double* a, double* damp, cudaStream_t st);
+                               double percdamp, T* a, double* damp, cudaStream_t st);
 // In-place lower Cholesky of A (n x n, row-major, lower used), then
 // U = (J L J)^-1 written to u (n x n row-major upper, zero below).
-// Sets kFlagNotPD in *flag on breakdown.  ws: n*n doubles workspace.
-void factor_upper_inverse(double* a, long long n, double* u, double* ws, unsigned* flag,
-                          cudaStream_t st);
-// hinv = U^T U (parity artefact: (H_p + damp I)^-1 in processing order)
-void launch_gram_upper(const double* u, long long n, double* hinv, cudaStream_t st);
+// Sets kFlagNotPD in *flag on breakdown.  ws: nblk*64*64 + n*n elements.
+template <typename T>
+void factor_upper_inverse(T* a, long long n, T* u, T* ws, unsigned* flag, cudaStream_t st);
+// hinv = U^T U in fp64 (parity artefact: (H_p + damp I)^-1 in processing order)
+template <typename T>
+void launch_gram_upper(const T* u, long long n, double* hinv, cudaStream_t st);
 
-// ---- generic fp64 GEMM (dgemm.cu) --------------------------------------
+// ---- SIMT GEMM (gemm.cu) ---------------------------------------------------
 // C[m x n] = beta*C + alpha * op(A) * op(B); op(A)[i][k] = A[i*lda + k] or
-// (transA) A[k*lda + i]; same for B.  lower_only: skip output tiles that lie
-// strictly above the diagonal.  A/B element type float or double.
-template <typename TA, typename TB>
-void dgemm(long long m, long long n, long long k, double alpha, const TA* a, long long lda,
-           bool ta, const TB* b, long long ldb, bool tb, double beta, double* c, long long ldc,
-           bool lower_only, cudaStream_t st);
+// (transA) A[k*lda + i]; same for B.  lower_only: skip output tiles strictly
+// above the diagonal.  Compute type T; A/B element types TA/TB.
+template <typename T, typename TA, typename TB>
+void gemm(long long m, long long n, long long k, double alpha, const TA* a, long long lda,
+          bool ta, const TB* b, long long ldb, bool tb, double beta, T* c, long long ldc,
+          bool lower_only, cudaStream_t st);
 
 // ---- GPTQ sweep (sweep.cu) ---------------------------------------------
-// wp: n x m fp64 permuted working weights (rows in processing order)
-// w has row stride ldw; wp is contiguous n x m
-void launch_permute_rows_f64(const float* w, long long n, long long m, long long ldw,
-                             const int32_t* order, double* wp, cudaStream_t st);
-// codes / w_hat are written with row stride ldo (original row order)
-void gptq_sweep(double* wp, long long n, long long m, const double* u, const int32_t* order,
-                const QCfg& c, const float* scales, const int32_t* zeros, long long block,
-                int16_t* codes, float* w_hat, long long ldo, double* err_ws, cudaStream_t st);
+constexpr long long kMaxSweepBlock = 128;
+// w has row stride ldw; wp is contiguous n x m (rows in processing order)
+template <typename T>
+void launch_permute_rows(const float* w, long long n, long long m, long long ldw,
+                         const int32_t* order, T* wp, cudaStream_t st);
+// codes / w_hat are written with row stride ldo (original row order);
+// err_ws: kMaxSweepBlock * m elements
+template <typename T>
+void gptq_sweep(T* wp, long long n, long long m, const T* u, const int32_t* order, const QCfg& c,
+                const float* scales, const int32_t* zeros, long long block, int16_t* codes,
+                float* w_hat, long long ldo, T* err_ws, cudaStream_t st);
 
 // ---- statistics (stats.cu, hessian_tc.cu) -------------------------------
 // fp64 accumulate_stats for fp32 inputs (stats.cpp:10-19): gram += Xp^T Xp,

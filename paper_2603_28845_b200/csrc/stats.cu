@@ -105,12 +105,12 @@ __global__ void dot_kernel(const double* __restrict__ a, const double* __restric
 
 void accumulate_stats_f64(const float* x_fp, const float* x_pert, long long rows, long long dim,
                           double* gram, double* cross, double* diff_ws, cudaStream_t st) {
-  dgemm<float, float>(dim, dim, rows, 1.0, x_pert, dim, true, x_pert, dim, false, 1.0, gram, dim,
+  gemm<double, float, float>(dim, dim, rows, 1.0, x_pert, dim, true, x_pert, dim, false, 1.0, gram, dim,
                       false, st);
   if (cross) {
     count_launches(1);
     diff_kernel<<<blocks_for(rows * dim), 256, 0, st>>>(x_fp, x_pert, rows * dim, diff_ws);
-    dgemm<float, double>(dim, dim, rows, 1.0, x_pert, dim, true, diff_ws, dim, false, 1.0, cross,
+    gemm<double, float, double>(dim, dim, rows, 1.0, x_pert, dim, true, diff_ws, dim, false, 1.0, cross,
                          dim, false, st);
   }
 }
@@ -143,7 +143,7 @@ void activation_objective(const float* w, const float* w_hat, const float* h, lo
   double* hd = ws + n * m;
   count_launches(2);
   delta_kernel<<<blocks_for(n * m), 256, 0, st>>>(w, w_hat, n * m, d);
-  dgemm<float, double>(n, m, n, 1.0, h, n, false, d, m, false, 0.0, hd, m, false, st);
+  gemm<double, float, double>(n, m, n, 1.0, h, n, false, d, m, false, 0.0, hd, m, false, st);
   dot_kernel<<<1, 1024, 0, st>>>(d, hd, n * m, out_dev);
 }
 
