@@ -126,6 +126,7 @@ def cpu_reference(steps: int, warmup: int, chunk: int = 1024):
     from oracle import ref
     threads = os.cpu_count() or 1
     os.environ["OCW_SHIM_THREADS"] = str(threads)
+    ref.use_blas(True)
     ref.set_threads(threads)
     rng = np.random.default_rng(SEED_W)
     w = orc.bf16_round((rng.standard_normal((N_IN, M_OUT), dtype=np.float32) * 0.02))
@@ -219,6 +220,9 @@ def main():
 
     for _ in range(args.warmup):
         step()
+    dev.profile(True)
+    step()
+    phases = dev.profile(False)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -294,7 +298,7 @@ def main():
                                "(1% outlier channels x20), W4 asym g128, act-order, damp 0.01, block 128",
                    "l2": "inputs larger than L2 (X = 2 GiB), no flush",
                    "parallelism": f"{world} independent layers" if world > 1 else "single GPU"},
-        "breakdown_ms": {"hessian": t_h, "gptq": t_q, "pack": t_p},
+        "breakdown_ms": {"hessian": t_h, "gptq": t_q, "pack": t_p, "gptq_phases": phases},
         "hessian_tflops": achieved,
         "roofline": {"bound": "tensor", "kernel": "hessian_tc_kernel (+finalize)", "achieved": achieved,
                      "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved / peak_tf,

@@ -185,6 +185,14 @@ int ocwg_pack_uniform_dev(ocwg_ctx* ctx, const int16_t* codes, const float* scal
 /* impl: 0 = tcgen05 kernel (product), 1 = SIMT fp64-accumulate cross-check */
 int ocwg_debug_hessian_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, uint64_t dim,
                            float* h, int accumulate, int impl);
+/* Phase timing of gptq (CUDA events): on != 0 enables recording; phase_ms
+ * (may be NULL) receives the last run's [order+damp+permute-H, Cholesky,
+ * triangular inverse, grids, sweep] in milliseconds. */
+int ocwg_debug_profile(ocwg_ctx* ctx, int on, double* phase_ms);
+/* GEMM micro-benchmark hook (device pointers): C = beta C + alpha op(A) op(B). */
+int ocwg_debug_gemm(ocwg_ctx* ctx, int precision, uint64_t m, uint64_t n, uint64_t k, double alpha,
+                    const void* a, uint64_t lda, int ta, const void* b, uint64_t ldb, int tb,
+                    double beta, void* c, uint64_t ldc, int lower_only, int reps, double* ms);
 /* Number of kernels this library launched on the context so far. */
 uint64_t ocwg_launch_count(ocwg_ctx* ctx);
 

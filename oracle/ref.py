@@ -22,6 +22,7 @@ _SIGS = {
     "ocwref_last_error": (C.c_char_p, []),
     "ocwref_blas_name": (C.c_char_p, []),
     "ocwref_set_threads": (None, [_I]),
+    "ocwref_use_blas": (None, [_I]),
     "ocwref_group_count": (_U64, [_I, _I, _I, _U64, _U64, _U64]),
     "ocwref_storage_bytes": (_U64, [_I, _I, _I, _U64, _U64, _U64]),
     "ocwref_random_gaussian": (_I, [_U64, _U64, _U64, C.c_float, _P]),
@@ -187,6 +188,11 @@ def quantize_layer(w, gram, cross, method_gptq, bits, scheme, gran, group, mse=F
                                     int(actorder), percdamp, block, int(qep is not None), alpha, eta,
                                     _p(codes), _p(s), _p(z)))
     return codes, s, z
+
+
+def use_blas(on: bool) -> None:
+    """BLAS-backed shim GEMM/LLT (fast) vs fixed-order loops (bit-portable)."""
+    lib().ocwref_use_blas(int(bool(on)))
 
 
 def set_threads(n: int) -> None:

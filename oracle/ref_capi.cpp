@@ -94,6 +94,7 @@ extern "C" {
 
 const char* ocwref_last_error() { return g_err.c_str(); }
 const char* ocwref_blas_name() { return Eigen::shim::blas_name(); }
+void ocwref_use_blas(int on) { Eigen::shim::blas_enabled() = on != 0; }
 void ocwref_set_threads(int n) {
   if (Eigen::shim::blas().set_threads) Eigen::shim::blas().set_threads(n);
 }

@@ -208,6 +208,9 @@ _SIGS = {
     "ocwg_pack_uniform_dev": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.POINTER(_QCfg), _P]),
     "ocwg_debug_hessian_dev": (C.c_int, [_P, _P, _U64, _U64, _P, C.c_int, C.c_int]),
     "ocwg_launch_count": (_U64, [_P]),
+    "ocwg_debug_profile": (C.c_int, [_P, C.c_int, _P]),
+    "ocwg_debug_gemm": (C.c_int, [_P, C.c_int, _U64, _U64, _U64, C.c_double, _P, _U64, C.c_int, _P,
+                                  _U64, C.c_int, C.c_double, _P, _U64, C.c_int, C.c_int, _P]),
 }
 
 _lib = None

@@ -2,6 +2,7 @@
 // the orchestration of the kernels into the reference's hot-path functions.
 // Validation order and error classes follow the reference exactly
 // (quant.cpp:19-25,168-171; layerwise.cpp:22-26,43-49; stats.cpp:11-15).
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -31,6 +32,10 @@ struct ocwg_ctx {
   unsigned* flag = nullptr;  // device status word
   unsigned* flag_host = nullptr;
   int precision = OCWG_FP32;  // factorisation + sweep arithmetic
+  bool profile = false;       // record phase events in run_gptq
+  bool tensor_core_gemm = true;  // fp32 GEMMs on tcgen05 (3xTF32) vs SIMT
+  cudaEvent_t ev[6] = {};
+  double phase_ms[5] = {};
   std::mutex mu;
 };
 
@@ -169,7 +174,18 @@ struct GptqBufs {
   void* fws;  // nblk*64*64 + n*n  T
   void* wp;   // n x m  T
   void* err;  // 128 x m T
+  float* tcws;
+  size_t tcws_floats;
 };
+
+size_t tc_ws_floats(uint64_t n, uint64_t m) {
+  // largest fp32 GEMM operand pair of the factorisation / sweep
+  const long long nn = (long long)n, mm_ = (long long)std::max<uint64_t>(m, 1);
+  // sweep trailing (n x m x 128), Cholesky SYRK (n x n x 64), inverse doubling
+  // (batched, <= 2 * n * n operand floats in total per level)
+  return std::max({tc_gemm_workspace_floats(nn, mm_, kMaxSweepBlock),
+                   tc_gemm_workspace_floats(nn, nn, 64), size_t(2 * nn * nn + 4 * nn * 4 + 64)});
+}
 
 void gptq_reserve(Arena& ar, uint64_t n, uint64_t m, int precision, size_t* o) {
   const uint64_t nblk = (n + 63) / 64;
@@ -181,21 +197,27 @@ void gptq_reserve(Arena& ar, uint64_t n, uint64_t m, int precision, size_t* o) {
   o[4] = ar.reserve((nblk * 64 * 64 + n * n) * es);
   o[5] = ar.reserve(n * m * es);
   o[6] = ar.reserve(kMaxSweepBlock * m * es);
+  o[7] = ar.reserve(tc_ws_floats(n, m) * sizeof(float));
 }
-GptqBufs gptq_bufs(const Arena& ar, const size_t* o) {
+GptqBufs gptq_bufs(const Arena& ar, const size_t* o, uint64_t n, uint64_t m) {
   return {ar.at<int32_t>(o[0]), ar.at<double>(o[1]), ar.at<void>(o[2]), ar.at<void>(o[3]),
-          ar.at<void>(o[4]), ar.at<void>(o[5]), ar.at<void>(o[6])};
+          ar.at<void>(o[4]), ar.at<void>(o[5]), ar.at<void>(o[6]), ar.at<float>(o[7]),
+          tc_ws_floats(n, m)};
 }
 
 template <typename T>
 void run_factor_t(ocwg_ctx* ctx, const float* h_dev, uint64_t n, int actorder, double percdamp,
                   const GptqBufs& b) {
   cudaStream_t st = ctx->stream;
+  set_tc_workspace(ctx->tensor_core_gemm ? b.tcws : nullptr, b.tcws_floats);
   launch_order(h_dev, (long long)n, actorder, b.order, st);
   launch_build_factor_input<T>(h_dev, (long long)n, b.order, percdamp, static_cast<T*>(b.a), b.damp,
                                st);
+  if (ctx->profile) cudaEventRecord(ctx->ev[1], st);
   factor_upper_inverse<T>(static_cast<T*>(b.a), (long long)n, static_cast<T*>(b.u),
-                          static_cast<T*>(b.fws), ctx->flag, st);
+                          static_cast<T*>(b.fws), ctx->flag, st,
+                          ctx->profile ? ctx->ev[2] : nullptr);
+  if (ctx->profile) cudaEventRecord(ctx->ev[3], st);
 }
 
 // order + damp + factorisation -> U (device); the reference's :29-51
@@ -212,6 +234,7 @@ void run_sweep_t(ocwg_ctx* ctx, const float* w, uint64_t ldw, uint64_t n, uint64
                  const ocwg_gptq_options* opts, int16_t* codes, const float* scales,
                  const int32_t* zeros, float* w_hat, const GptqBufs& b) {
   cudaStream_t st = ctx->stream;
+  set_tc_workspace(ctx->tensor_core_gemm ? b.tcws : nullptr, b.tcws_floats);
   launch_permute_rows<T>(w, (long long)n, (long long)m, (long long)ldw, b.order,
                          static_cast<T*>(b.wp), st);
   gptq_sweep<T>(static_cast<T*>(b.wp), (long long)n, (long long)m, static_cast<const T*>(b.u),
@@ -225,13 +248,24 @@ void run_gptq(ocwg_ctx* ctx, const float* w, uint64_t ldw, const float* h_dev, u
               int16_t* codes, float* scales, int32_t* zeros, float* w_hat, const GptqBufs& b,
               float* mm_ws) {
   const QCfg c = qcfg(cfg, m);
+  if (ctx->profile) cudaEventRecord(ctx->ev[0], ctx->stream);
   run_factor(ctx, h_dev, n, opts->actorder, opts->percdamp, b);
   launch_calibrate_grids(w, (long long)n, (long long)m, (long long)ldw, c, mode, scales, zeros,
                          ctx->flag, mm_ws, ctx->stream);
+  if (ctx->profile) cudaEventRecord(ctx->ev[4], ctx->stream);
   if (ctx->precision == OCWG_FP64)
     run_sweep_t<double>(ctx, w, ldw, n, m, c, opts, codes, scales, zeros, w_hat, b);
   else
     run_sweep_t<float>(ctx, w, ldw, n, m, c, opts, codes, scales, zeros, w_hat, b);
+  if (ctx->profile) {
+    cudaEventRecord(ctx->ev[5], ctx->stream);
+    cudaEventSynchronize(ctx->ev[5]);
+    for (int k = 0; k < 5; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]);
+      ctx->phase_ms[k] = ms;
+    }
+  }
 }
 
 void check_gptq_args(const ocwg_quant_config* cfg, const ocwg_gptq_options* opts, uint64_t n,
@@ -291,6 +325,18 @@ int ocwg_set_precision(ocwg_ctx* ctx, int precision) {
   });
 }
 
+int ocwg_debug_profile(ocwg_ctx* ctx, int on, double* phase_ms) {
+  return guard([&] {
+    if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (on && !ctx->ev[0])
+      for (auto& e : ctx->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
+    ctx->profile = on != 0;
+    if (phase_ms)
+      for (int k = 0; k < 5; ++k) phase_ms[k] = ctx->phase_ms[k];
+  });
+}
+
 int ocwg_set_stream(ocwg_ctx* ctx, void* s) {
   return guard([&] {
     if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
@@ -306,6 +352,56 @@ int ocwg_synchronize(ocwg_ctx* ctx) {
 }
 
 uint64_t ocwg_launch_count(ocwg_ctx*) { return launches_issued(); }
+
+int ocwg_debug_gemm(ocwg_ctx* ctx, int precision, uint64_t m, uint64_t n, uint64_t k, double alpha,
+                    const void* a, uint64_t lda, int ta, const void* b, uint64_t ldb, int tb,
+                    double beta, void* c, uint64_t ldc, int lower_only, int reps, double* ms) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    ck(cudaEventRecord(e0, ctx->stream), "event");
+    float* tcws = nullptr;
+    size_t tcf = 0;
+    if (precision == 2) {  // tcgen05 3xTF32 path
+      tcf = tc_gemm_workspace_floats((long long)m, (long long)n, (long long)k);
+      Arena ar(ctx);
+      const size_t o = ar.reserve(tcf * 4);
+      ar.commit();
+      tcws = ar.at<float>(o);
+    }
+    for (int r = 0; r < reps; ++r) {
+      if (precision == 2) {
+        if (!tc_gemm_tf32x3(1, (long long)m, (long long)n, (long long)k, float(alpha),
+                            static_cast<const float*>(a), (long long)lda, 0, ta != 0,
+                            static_cast<const float*>(b), (long long)ldb, 0, tb != 0, float(beta),
+                            static_cast<float*>(c), (long long)ldc, 0, lower_only != 0, tcws, tcf,
+                            ctx->stream))
+          fail(OCWG_UNSUPPORTED, "tc_gemm_tf32x3 rejected the shape");
+      } else if (precision == OCWG_FP64)
+        gemm<double, double, double>((long long)m, (long long)n, (long long)k, alpha,
+                                     static_cast<const double*>(a), (long long)lda, ta != 0,
+                                     static_cast<const double*>(b), (long long)ldb, tb != 0, beta,
+                                     static_cast<double*>(c), (long long)ldc, lower_only != 0,
+                                     ctx->stream);
+      else
+        gemm<float, float, float>((long long)m, (long long)n, (long long)k, alpha,
+                                  static_cast<const float*>(a), (long long)lda, ta != 0,
+                                  static_cast<const float*>(b), (long long)ldb, tb != 0, beta,
+                                  static_cast<float*>(c), (long long)ldc, lower_only != 0,
+                                  ctx->stream);
+    }
+    ck(cudaEventRecord(e1, ctx->stream), "event");
+    finish(ctx);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    if (ms) *ms = t / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
 
 int ocwg_validate_config(const ocwg_quant_config* cfg) {
   return guard([&] { validate(cfg); });
@@ -585,7 +681,7 @@ int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, do
     const size_t oh = ar.reserve(n * n * 4), ohi = ar.reserve(n * n * 8),
                  ou64 = ar.reserve(n * n * 8);
     ar.commit();
-    const GptqBufs b = gptq_bufs(ar, o);
+    const GptqBufs b = gptq_bufs(ar, o, n, 1);
     h2d(ar.at<float>(oh), h, n * n * 4, ctx);
     run_factor(ctx, ar.at<float>(oh), n, actorder, percdamp, b);
     if (ctx->precision == OCWG_FP64) {
@@ -625,9 +721,9 @@ int ocwg_gptq_quantize_dev(ocwg_ctx* ctx, const float* w, uint64_t ldw, const fl
     ar.commit();
     if (n && m)
       run_gptq(ctx, w, ldw, h, n, m, cfg, opts, mode, codes, scales, zeros, w_hat,
-               gptq_bufs(ar, o), ar.at<float>(om));
+               gptq_bufs(ar, o, n, m), ar.at<float>(om));
     else if (n)
-      run_factor(ctx, h, n, opts->actorder, opts->percdamp, gptq_bufs(ar, o));
+      run_factor(ctx, h, n, opts->actorder, opts->percdamp, gptq_bufs(ar, o, n, m));
     finish(ctx);
     if (n == 0 || m == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
   });
@@ -729,7 +825,7 @@ int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, 
       if (r == -1) hessian_simt(x, (long long)tokens, (long long)n, h, 0, ctx->stream);
       else if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
     }
-    run_gptq(ctx, w, m, h, n, m, cfg, opts, mode, cd, sd, zd, w_hat, gptq_bufs(ar, o),
+    run_gptq(ctx, w, m, h, n, m, cfg, opts, mode, cd, sd, zd, w_hat, gptq_bufs(ar, o, n, m),
              ar.at<float>(om));
     if (payload) launch_pack(cd, (long long)(n * m), (long long)ng, qcfg(cfg, m), sd, zd, payload,
                              ctx->stream);

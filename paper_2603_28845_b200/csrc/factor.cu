@@ -2,10 +2,19 @@
 //   hd = fp64(H); damp = percdamp*mean(diag(hd)); hd += damp*I;
 //   hp = P hd P^T;  hinv = hp^-1;  U = upper Cholesky factor of hinv.
 // Computed as  A = J hp J = L L^T (lower, blocked right-looking),
-//              U = J L^-1 J  (blocked triangular inverse).
+//              U = J L^-1 J.
 // Mathematically identical to the reference's LLT -> solve(I) -> LLT (by the
-// uniqueness of the Cholesky factor of hinv), 2n^3/3 flops instead of 8n^3/3.
-// Templated on the compute type T (float default, double reference-class).
+// uniqueness of the Cholesky factor of hinv), with 2n^3/3 (Cholesky n^3/3 +
+// inverse) instead of 8n^3/3 flops.  Templated on the compute type T (float
+// default, double = the reference's arithmetic class).
+//
+// Cholesky: one fused launch per 64-column panel (every CTA factors + inverts
+// the 64x64 diagonal block in shared memory; CTA 0 stores L_kk and L_kk^-1,
+// CTA c >= 1 solves its 64-row slice of the panel), then one trailing SYRK
+// (tensor cores in fp32 mode).  Triangular inverse: log-depth recursive
+// doubling over the diagonal blocks,
+//   inv([A 0; B C]) = [A^-1 0; -C^-1 (B A^-1), C^-1],
+// each level two batched GEMMs (6 levels for n = 4096).
 #include <cmath>
 
 #include "kernels.h"
@@ -13,7 +22,7 @@
 namespace ocwg {
 namespace {
 
-constexpr int NB = 64;  // panel width
+constexpr int NB = 64;  // panel width / base block
 
 // A[i][j] = T(double(H[o(i)][o(j)]) + (i==j)*damp), o(i) = order[n-1-i]; lower only
 template <typename T>
@@ -47,81 +56,184 @@ __global__ void damp_kernel(const float* __restrict__ h, long long n, double per
   }
 }
 
-// Factor the nb x nb diagonal block at (k0,k0) in shared memory with one
-// barrier per column (every thread rescales column j itself from the unscaled
-// values; the scaled column is written to a separate array), then invert it.
-// Writes L_kk back into A and L_kk^-1 into dinv (NB x NB row-major).
+// Fused panel step at column k0 (block width nb <= 64).
+// Every CTA factors and inverts the (already updated) 64x64 diagonal block
+// with a 16x16 grid of threads, each holding a 4x4 register tile (static
+// register indices, two barriers per elimination step: publish column/row j,
+// then rank-1 update).  Rows/cols >= nb are identity padding.  CTA 0 stores
+// L_kk (into A) and L_kk^-1 (dinv); CTA c >= 1 computes its 64-row panel slice
+// L_slice = A_slice * L_kk^-T and writes it back into A.
 template <typename T>
-__global__ void __launch_bounds__(256) potrf_diag_kernel(T* a, long long n, long long k0, T* dinv,
-                                                         unsigned* flag) {
+__device__ __forceinline__ T pick4(const T (&v)[4], int i) {
+  return i == 0 ? v[0] : (i == 1 ? v[1] : (i == 2 ? v[2] : v[3]));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) panel_kernel(T* a, long long n, long long k0, T* dinv,
+                                                    unsigned* flag) {
   extern __shared__ __align__(16) unsigned char dsm_raw[];
-  T(*s)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(dsm_raw);
-  T(*l)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(dsm_raw + sizeof(T) * NB * (NB + 1));
-  T(*x)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(dsm_raw + 2 * sizeof(T) * NB * (NB + 1));
+  T(*lb)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(dsm_raw);                              // L
+  T(*xb)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(dsm_raw + sizeof(T) * NB * (NB + 1));  // L^-1
+  T(*ps)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(dsm_raw + 2 * sizeof(T) * NB * (NB + 1));
+  T* diag = reinterpret_cast<T*>(dsm_raw + 3 * sizeof(T) * NB * (NB + 1));
+  T* vec = diag + NB;  // column j of L / row j of L^-1 being published
   const int nb = int(min((long long)NB, n - k0));
-  const int tid = threadIdx.x;
-  for (int e = tid; e < NB * NB; e += 256) {
-    const int i = e / NB, j = e % NB;
-    s[i][j] = (i < nb && j < nb && j <= i) ? a[(k0 + i) * n + k0 + j] : T(i == j ? 1 : 0);
-    l[i][j] = T(0);
-    x[i][j] = T(i == j ? 1 : 0);
-  }
+  const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
+  const long long r0 = k0 + nb + (long long)(blockIdx.x - 1) * NB;  // panel slice rows
+  const int pr = blockIdx.x == 0 ? 0 : int(min((long long)NB, n - r0));
+
+  T t[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int r = 4 * ti + u, c = 4 * tj + v;
+      T val = T(0);
+      if (r < nb && c < nb) {
+        if (c <= r) val = a[(k0 + r) * n + k0 + c];
+      } else if (r == c) {
+        val = T(1);
+      }
+      t[u][v] = val;
+      if (r == c) diag[r] = val;
+    }
+  if (blockIdx.x > 0)
+    for (int e = tid; e < NB * NB; e += 256) {
+      const int r = e / NB, c = e % NB;
+      ps[r][c] = (r < pr && c < nb) ? a[(r0 + r) * n + k0 + c] : T(0);
+    }
   __syncthreads();
+
+  // ---- Cholesky of the block (right-looking, lower)
   bool bad = false;
-  for (int j = 0; j < nb; ++j) {
-    const T piv = s[j][j];
-    bad |= !(piv > T(0));  // Eigen: x <= 0 -> NumericalIssue (NaN rejected too)
+  for (int j = 0; j < NB; ++j) {
+    const T piv = diag[j];
     const T d = sqrt(piv);
     const T rd = T(1) / d;
-    for (int e = tid; e < NB * NB; e += 256) {
-      const int i = e / NB, c = e % NB;
-      if (i <= j || i >= nb) continue;
-      if (c == j) {
-        l[i][j] = s[i][j] * rd;
-      } else if (c > j && c <= i) {
-        s[i][c] -= (s[i][j] * rd) * (s[c][j] * rd);
+    if (tid == 0 && j < nb) bad |= !(piv > T(0));  // Eigen: x <= 0 -> NumericalIssue
+    if (tj == (j >> 2) && ti >= tj) {
+      const int jj = j & 3;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = 4 * ti + u;
+        if (r > j) {
+          const T lv = pick4(t[u], jj) * rd;
+          vec[r] = lv;
+          lb[r][j] = lv;
+        } else if (r == j) {
+          lb[j][j] = d;
+        }
       }
     }
-    if (tid == 0) l[j][j] = d;
+    __syncthreads();
+    if (ti >= tj && 4 * ti + 3 > j && 4 * tj + 3 > j) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = 4 * ti + u;
+        if (r <= j) continue;
+        const T lr = vec[r];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c = 4 * tj + v;
+          if (c > j && c <= r) t[u][v] -= lr * vec[c];
+        }
+        if (ti == tj) diag[r] = t[u][u];
+      }
+    }
     __syncthreads();
   }
-  // X = L^-1: for each j, rows i > j -= L_ij * (row j / L_jj); then row j /= L_jj
-  for (int j = 0; j < nb; ++j) {
-    const T rl = T(1) / l[j][j];
+  // ---- X = L^-1 (right-looking): publish row j of X scaled by 1/L_jj, update rows below
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) t[u][v] = T((4 * ti + u) == (4 * tj + v) ? 1 : 0);
+  for (int j = 0; j < NB; ++j) {
+    const T rl = T(1) / lb[j][j];
+    if (ti == (j >> 2) && 4 * tj <= j) {
+      const int jj = j & 3;
+#pragma unroll
+      for (int uu = 0; uu < 4; ++uu) {
+        if (uu != jj) continue;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c = 4 * tj + v;
+          if (c <= j) {
+            t[uu][v] *= rl;
+            vec[c] = t[uu][v];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (ti >= (j >> 2) && 4 * tj <= j) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = 4 * ti + u;
+        if (r <= j) continue;
+        const T lr = lb[r][j];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c = 4 * tj + v;
+          if (c <= j) t[u][v] -= lr * vec[c];
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int r = 4 * ti + u, c = 4 * tj + v;
+      xb[r][c] = (c <= r) ? t[u][v] : T(0);
+    }
+  __syncthreads();
+  if (blockIdx.x == 0) {
     for (int e = tid; e < NB * NB; e += 256) {
-      const int i = e / NB, c = e % NB;
-      if (c > j || i <= j || i >= nb) continue;
-      x[i][c] -= l[i][j] * (x[j][c] * rl);
+      const int r = e / NB, c = e % NB;
+      if (r < nb && c < nb) {
+        if (c <= r) a[(k0 + r) * n + k0 + c] = lb[r][c];
+        dinv[r * NB + c] = xb[r][c];
+      }
     }
-    __syncthreads();
-    if (tid <= j) x[j][tid] *= rl;
-    __syncthreads();
+    if (tid == 0 && bad) atomicOr(flag, kFlagNotPD);
+    return;
   }
-  for (int e = tid; e < NB * NB; e += 256) {
-    const int i = e / NB, c = e % NB;
-    if (i < nb && c < nb) {
-      if (c <= i) a[(k0 + i) * n + k0 + c] = l[i][c];
-      dinv[i * NB + c] = (c <= i) ? x[i][c] : T(0);
+  // ---- panel slice: out[r][c] = sum_k P[r][k] * X[c][k]
+  T acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = T(0);
+  for (int k = 0; k < NB; ++k) {
+    T pv[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pv[u] = ps[4 * ti + u][k];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) xv[v] = xb[4 * tj + v][k];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] += pv[u] * xv[v];
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int r = 4 * ti + u, c = 4 * tj + v;
+      if (r < pr && c < nb) a[(r0 + r) * n + k0 + c] = acc[u][v];
     }
-  }
-  if (bad) atomicOr(flag, kFlagNotPD);
 }
 
+// X = blockdiag(dinv_k), zero elsewhere (lower block triangle is filled by the doubling)
 template <typename T>
-__global__ void copy_block_kernel(const T* __restrict__ src, long long lds, T* dst, long long ldd,
-                                  long long rows, long long cols) {
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long i = e / cols, j = e % cols;
-    dst[i * ldd + j] = src[i * lds + j];
-  }
-}
-
-template <typename T>
-__global__ void identity_kernel(T* x, long long n) {
+__global__ void init_inverse_kernel(T* x, long long n, const T* __restrict__ dinv) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n * n;
-       e += (long long)gridDim.x * blockDim.x)
-    x[e] = T((e / n == e % n) ? 1 : 0);
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / n, c = e % n;
+    const long long br = r / NB, bc = c / NB;
+    x[e] = (br == bc) ? dinv[br * NB * NB + (r % NB) * NB + (c % NB)] : T(0);
+  }
 }
 
 // U[r][c] = X[n-1-r][n-1-c] for r <= c (X = L^-1 lower), else 0
@@ -140,8 +252,8 @@ inline int blocks_for(long long n) {
 }
 
 template <typename T>
-constexpr int potrf_smem() {
-  return 3 * NB * (NB + 1) * int(sizeof(T));
+constexpr int panel_smem() {
+  return (3 * NB * (NB + 1) + 2 * NB) * int(sizeof(T));
 }
 
 }  // namespace
@@ -156,42 +268,53 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
 
 // ws layout: [nblk*NB*NB dinv blocks][n*n scratch]
 template <typename T>
-void factor_upper_inverse(T* a, long long n, T* u, T* ws, unsigned* flag, cudaStream_t st) {
+void factor_upper_inverse(T* a, long long n, T* u, T* ws, unsigned* flag, cudaStream_t st,
+                          cudaEvent_t mid) {
   static const bool attr = [] {
-    cudaFuncSetAttribute(potrf_diag_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         potrf_smem<T>());
+    cudaFuncSetAttribute(panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         panel_smem<T>());
     return true;
   }();
   (void)attr;
   const long long nblk = (n + NB - 1) / NB;
   T* dinv = ws;
   T* tmp = ws + nblk * NB * NB;
+  // ---- Cholesky: fused panel kernel + trailing SYRK per 64 columns
   for (long long kb = 0; kb < nblk; ++kb) {
     const long long k0 = kb * NB, w = std::min<long long>(NB, n - k0), rest = n - k0 - w;
     count_launches(1);
-    potrf_diag_kernel<T><<<1, 256, potrf_smem<T>(), st>>>(a, n, k0, dinv + kb * NB * NB, flag);
-    if (rest <= 0) continue;
-    gemm<T, T, T>(rest, w, w, 1.0, a + (k0 + w) * n + k0, n, false, dinv + kb * NB * NB, NB, true,
-                  0.0, tmp, NB, false, st);
-    count_launches(1);
-    copy_block_kernel<T><<<blocks_for(rest * w), 256, 0, st>>>(tmp, NB, a + (k0 + w) * n + k0, n,
-                                                               rest, w);
-    gemm<T, T, T>(rest, rest, w, -1.0, tmp, NB, false, tmp, NB, true, 1.0,
-                  a + (k0 + w) * n + (k0 + w), n, true, st);
+    panel_kernel<T><<<unsigned(1 + (rest + NB - 1) / NB), 256, panel_smem<T>(), st>>>(
+        a, n, k0, dinv + kb * NB * NB, flag);
+    if (rest > 0)
+      mm<T>(rest, rest, w, -1.0, a + (k0 + w) * n + k0, n, false, a + (k0 + w) * n + k0, n, true,
+            1.0, a + (k0 + w) * n + (k0 + w), n, true, st);
   }
+  if (mid) cudaEventRecord(mid, st);
+  // ---- X = L^-1 by recursive doubling over the diagonal blocks (in u)
   T* x = u;
   count_launches(2);
-  identity_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(x, n);
-  for (long long ib = 0; ib < nblk; ++ib) {
-    const long long i0 = ib * NB, w = std::min<long long>(NB, n - i0);
-    const long long cols = i0 + w, rest = n - i0 - w;
-    gemm<T, T, T>(w, cols, w, 1.0, dinv + ib * NB * NB, NB, false, x + i0 * n, n, false, 0.0, tmp,
-                  cols, false, st);
-    count_launches(1);
-    copy_block_kernel<T><<<blocks_for(w * cols), 256, 0, st>>>(tmp, cols, x + i0 * n, n, w, cols);
-    if (rest > 0)
-      gemm<T, T, T>(rest, cols, w, -1.0, a + (i0 + w) * n + i0, n, false, x + i0 * n, n, false,
-                    1.0, x + (i0 + w) * n, n, false, st);
+  init_inverse_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(x, n, dinv);
+  for (long long s = 2 * NB; s < 2 * n; s *= 2) {
+    const long long h = s / 2;
+    const long long full = n / s;  // pairs with a full-size second half
+    // batched full pairs: base row/col p*s; A-block [p*s, p*s+h), C-block [p*s+h, p*s+s)
+    if (full > 0) {
+      const long long stride = s * (n + 1);
+      // tmp_p = L[C, A] * X[A, A]         (h x h x h)
+      mm<T>(h, h, h, 1.0, a + h * n, n, false, x, n, false, 0.0, tmp, h, false, st, int(full),
+            stride, stride, h * h);
+      // X[C, A] = -X[C, C] * tmp_p         (h x h x h)
+      mm<T>(h, h, h, -1.0, x + h * n + h, n, false, tmp, h, false, 0.0, x + h * n, n, false, st,
+            int(full), stride, h * h, stride);
+    }
+    // a trailing partial pair: A-block [p0, p0+h), C-block [p0+h, n) with 0 < n-p0-h < h
+    const long long p0 = full * s, c2 = n - p0 - h;
+    if (c2 > 0) {
+      mm<T>(c2, h, h, 1.0, a + (p0 + h) * n + p0, n, false, x + p0 * n + p0, n, false, 0.0, tmp, h,
+            false, st);
+      mm<T>(c2, h, c2, -1.0, x + (p0 + h) * n + (p0 + h), n, false, tmp, h, false, 0.0,
+            x + (p0 + h) * n + p0, n, false, st);
+    }
   }
   reverse_to_upper_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(x, n, tmp);
   cudaMemcpyAsync(u, tmp, size_t(n * n) * sizeof(T), cudaMemcpyDeviceToDevice, st);
@@ -207,9 +330,9 @@ template void launch_build_factor_input<float>(const float*, long long, const in
 template void launch_build_factor_input<double>(const float*, long long, const int32_t*, double,
                                                 double*, double*, cudaStream_t);
 template void factor_upper_inverse<float>(float*, long long, float*, float*, unsigned*,
-                                          cudaStream_t);
+                                          cudaStream_t, cudaEvent_t);
 template void factor_upper_inverse<double>(double*, long long, double*, double*, unsigned*,
-                                           cudaStream_t);
+                                           cudaStream_t, cudaEvent_t);
 template void launch_gram_upper<float>(const float*, long long, double*, cudaStream_t);
 template void launch_gram_upper<double>(const double*, long long, double*, cudaStream_t);
 

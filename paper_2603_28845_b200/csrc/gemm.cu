@@ -35,7 +35,11 @@ __global__ void __launch_bounds__(256) gemm_kernel(long long m, long long n, lon
                                                    const TA* __restrict__ a, long long lda, int ta,
                                                    const TB* __restrict__ b, long long ldb, int tb,
                                                    T beta, T* __restrict__ c, long long ldc,
-                                                   int lower_only) {
+                                                   int lower_only, long long sa, long long sb,
+                                                   long long sc) {
+  a += (long long)blockIdx.z * sa;
+  b += (long long)blockIdx.z * sb;
+  c += (long long)blockIdx.z * sc;
   constexpr int BM = Tile<T>::BM, BN = Tile<T>::BN, BK = Tile<T>::BK;
   constexpr int TM = Tile<T>::TM, TN = Tile<T>::TN;
   constexpr int TX = BN / TN, TY = BM / TM;  // 16 x 16 threads
@@ -136,19 +140,56 @@ __global__ void __launch_bounds__(256) gemm_kernel(long long m, long long n, lon
 template <typename T, typename TA, typename TB>
 void gemm(long long m, long long n, long long k, double alpha, const TA* a, long long lda, bool ta,
           const TB* b, long long ldb, bool tb, double beta, T* c, long long ldc, bool lower_only,
-          cudaStream_t st) {
-  if (m <= 0 || n <= 0) return;
+          cudaStream_t st, int batch, long long sa, long long sb, long long sc) {
+  if (m <= 0 || n <= 0 || batch <= 0) return;
   constexpr int BM = Tile<T>::BM, BN = Tile<T>::BN;
-  dim3 grid(unsigned((n + BN - 1) / BN), unsigned((m + BM - 1) / BM));
+  dim3 grid(unsigned((n + BN - 1) / BN), unsigned((m + BM - 1) / BM), unsigned(batch));
   count_launches(1);
   gemm_kernel<T, TA, TB><<<grid, 256, 0, st>>>(m, n, k, T(alpha), a, lda, ta ? 1 : 0, b, ldb,
-                                               tb ? 1 : 0, T(beta), c, ldc, lower_only ? 1 : 0);
+                                               tb ? 1 : 0, T(beta), c, ldc, lower_only ? 1 : 0, sa,
+                                               sb, sc);
+}
+
+namespace {
+thread_local float* g_tc_ws = nullptr;
+thread_local size_t g_tc_ws_floats = 0;
+}  // namespace
+
+void set_tc_workspace(float* ws, size_t floats) {
+  g_tc_ws = ws;
+  g_tc_ws_floats = floats;
+}
+
+template <>
+void mm<float>(long long m, long long n, long long k, double alpha, const float* a, long long lda,
+               bool ta, const float* b, long long ldb, bool tb, double beta, float* c,
+               long long ldc, bool lower_only, cudaStream_t st, int batch, long long sa,
+               long long sb, long long sc) {
+  if (m <= 0 || n <= 0 || batch <= 0) return;
+  // tiny problems are latency bound: the SIMT kernel is one launch, the tensor
+  // core path is three (split A, split B, MMA)
+  const bool big = double(m) * double(n) * double(k) * batch >= double(1 << 22);
+  if (g_tc_ws && k > 0 && big &&
+      tc_gemm_tf32x3(batch, m, n, k, float(alpha), a, lda, sa, ta, b, ldb, sb, tb, float(beta), c,
+                     ldc, sc, lower_only, g_tc_ws, g_tc_ws_floats, st))
+    return;
+  gemm<float, float, float>(m, n, k, alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, lower_only, st,
+                            batch, sa, sb, sc);
+}
+
+template <>
+void mm<double>(long long m, long long n, long long k, double alpha, const double* a,
+                long long lda, bool ta, const double* b, long long ldb, bool tb, double beta,
+                double* c, long long ldc, bool lower_only, cudaStream_t st, int batch,
+                long long sa, long long sb, long long sc) {
+  gemm<double, double, double>(m, n, k, alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, lower_only,
+                               st, batch, sa, sb, sc);
 }
 
 #define OCWG_GEMM_INST(T, TA, TB)                                                              \
   template void gemm<T, TA, TB>(long long, long long, long long, double, const TA*, long long, \
                                 bool, const TB*, long long, bool, double, T*, long long, bool, \
-                                cudaStream_t);
+                                cudaStream_t, int, long long, long long, long long);
 OCWG_GEMM_INST(double, double, double)
 OCWG_GEMM_INST(double, float, float)
 OCWG_GEMM_INST(double, float, double)

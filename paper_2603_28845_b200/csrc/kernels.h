@@ -53,8 +53,10 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
 // In-place lower Cholesky of A (n x n, row-major, lower used), then
 // U = (J L J)^-1 written to u (n x n row-major upper, zero below).
 // Sets kFlagNotPD in *flag on breakdown.  ws: nblk*64*64 + n*n elements.
+// mid (optional): event recorded between the Cholesky and the inverse.
 template <typename T>
-void factor_upper_inverse(T* a, long long n, T* u, T* ws, unsigned* flag, cudaStream_t st);
+void factor_upper_inverse(T* a, long long n, T* u, T* ws, unsigned* flag, cudaStream_t st,
+                          cudaEvent_t mid = nullptr);
 // hinv = U^T U in fp64 (parity artefact: (H_p + damp I)^-1 in processing order)
 template <typename T>
 void launch_gram_upper(const T* u, long long n, double* hinv, cudaStream_t st);
@@ -62,11 +64,29 @@ void launch_gram_upper(const T* u, long long n, double* hinv, cudaStream_t st);
 // ---- SIMT GEMM (gemm.cu) ---------------------------------------------------
 // C[m x n] = beta*C + alpha * op(A) * op(B); op(A)[i][k] = A[i*lda + k] or
 // (transA) A[k*lda + i]; same for B.  lower_only: skip output tiles strictly
-// above the diagonal.  Compute type T; A/B element types TA/TB.
+// above the diagonal.  Compute type T; A/B element types TA/TB.  Batched
+// form: batch b uses A + b*sa, B + b*sb, C + b*sc.
 template <typename T, typename TA, typename TB>
 void gemm(long long m, long long n, long long k, double alpha, const TA* a, long long lda,
           bool ta, const TB* b, long long ldb, bool tb, double beta, T* c, long long ldc,
-          bool lower_only, cudaStream_t st);
+          bool lower_only, cudaStream_t st, int batch = 1, long long sa = 0, long long sb = 0,
+          long long sc = 0);
+
+// ---- tensor-core fp32-accurate GEMM (tc_gemm.cu): 3xTF32 on tcgen05 ---------
+size_t tc_gemm_workspace_floats(long long m, long long n, long long k, int batch = 1);
+bool tc_gemm_tf32x3(int batch, long long m, long long n, long long k, float alpha, const float* a,
+                    long long lda, long long sa, bool ta, const float* b, long long ldb,
+                    long long sb, bool tb, float beta, float* c, long long ldc, long long sc,
+                    bool lower_only, float* ws, size_t ws_floats, cudaStream_t st);
+// Workspace for the fp32 GEMMs of the factorisation / sweep (set by the C ABI
+// per call).  With a workspace set, fp32 GEMMs run on the tensor cores.
+void set_tc_workspace(float* ws, size_t floats);
+// Dispatch: T = float -> tcgen05 3xTF32 (when a workspace is set and the
+// problem is big enough to fill tiles), else SIMT.
+template <typename T>
+void mm(long long m, long long n, long long k, double alpha, const T* a, long long lda, bool ta,
+        const T* b, long long ldb, bool tb, double beta, T* c, long long ldc, bool lower_only,
+        cudaStream_t st, int batch = 1, long long sa = 0, long long sb = 0, long long sc = 0);
 
 // ---- GPTQ sweep (sweep.cu) ---------------------------------------------
 constexpr long long kMaxSweepBlock = 128;

@@ -101,7 +101,11 @@ __global__ void __launch_bounds__(256) inblock_kernel(
     const int li = rg + 8 * t;
     r[t] = (col_ok && li < bsz) ? wp[(ib + li) * m + j] : T(0);
   }
-#pragma unroll
+  // Rows li = 8t + o.  r[] is rotated down by one slot after every group of
+  // 8 rows, so the owner's value is always r[0] and every register index is
+  // a compile-time constant while only the 8-row group body is unrolled
+  // (keeps the kernel inside the instruction cache).
+#pragma unroll 1
   for (int t = 0; t < RPT; ++t) {
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
@@ -111,9 +115,9 @@ __global__ void __launch_bounds__(256) inblock_kernel(
       if (rg == o) {
         const float s = gs[li * kCols + cj];
         const int z = gz[li * kCols + cj];
-        const int q = quantize_code(float(r[t]), s, z, c.qmin, c.qmax);  // row_f (:70)
+        const int q = quantize_code(float(r[0]), s, z, c.qmin, c.qmax);  // row_f (:70)
         const float wh = dequantize_code(q, s, z);
-        e = err_of<T>(r[t], wh, us[li * (B + 1) + li]);
+        e = err_of<T>(r[0], wh, us[li * (B + 1) + li]);
         if (col_ok) {
           const long long orig = og[li];
           codes[orig * ldo + j] = int16_t(q);  // original row order (:75)
@@ -122,11 +126,14 @@ __global__ void __launch_bounds__(256) inblock_kernel(
         }
       }
       e = __shfl_sync(0xffffffffu, e, cc + 4 * o);
+      const T* urow = us + li * (B + 1) + rg + 8 * t;
 #pragma unroll
-      for (int t2 = t; t2 < RPT; ++t2) {
-        if (t2 > t || rg > o) r[t2] = upd<T>(r[t2], us[li * (B + 1) + rg + 8 * t2], e);
+      for (int k = 0; k < RPT; ++k) {
+        if ((k > 0 || rg > o) && t + k < RPT) r[k] = upd<T>(r[k], urow[8 * k], e);
       }
     }
+#pragma unroll
+    for (int k = 0; k + 1 < RPT; ++k) r[k] = r[k + 1];
   }
 }
 
@@ -182,7 +189,7 @@ void gptq_sweep(T* wp, long long n, long long m, const T* u, const int32_t* orde
       launch_inblock<T, 16>(wp, n, m, u, order, c, scales, zeros, ib, bsz, codes, w_hat, ldo,
                             err_ws, st);
     if (ie < n)
-      gemm<T, T, T>(n - ie, m, bsz, -1.0, u + ib * n + ie, n, true, err_ws, m, false, 1.0,
+      mm<T>(n - ie, m, bsz, -1.0, u + ib * n + ie, n, true, err_ws, m, false, 1.0,
                     wp + ie * m, m, false, st);
   }
 }

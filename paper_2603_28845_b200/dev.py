@@ -80,5 +80,13 @@ def quantize_layer_x(w: torch.Tensor, x_bf16: torch.Tensor, cfg: QuantConfig, op
                                            _p(out.payload), _p(out.h)))
 
 
+def profile(on: bool, device: int = 0):
+    """Enable gptq phase events; returns the last run's phase times (ms)."""
+    import numpy as np
+    out = np.zeros(5, np.float64)
+    _check(lib().ocwg_debug_profile(context(device).handle, int(on), C.c_void_p(out.ctypes.data)))
+    return dict(zip(["order_damp_build", "cholesky", "inverse", "grids", "sweep"], out.tolist()))
+
+
 def launch_count() -> int:
     return int(lib().ocwg_launch_count(None))
