@@ -19,7 +19,8 @@
  *     (thread-local).
  *   - Host-pointer entry points are synchronous (value semantics, like the
  *     reference).  *_dev entry points take DEVICE pointers, run on the
- *     context's stream and return after the stream has drained.
+ *     context's stream and return after the stream has drained (or, with
+ *     ocwg_set_async, right after enqueueing).
  *   - Grids are passed structure-of-arrays: scales (fp32 value of the
  *     reference-fp16-rounded scale) and int32 zero points, in group-index order
  *     (QuantizedMatrix::grids, quant.hpp:54-63).  qmin/qmax follow from the config.
@@ -84,8 +85,14 @@ int ocwg_create(int device, ocwg_ctx** out);
 int ocwg_destroy(ocwg_ctx* ctx);
 /* OCWG_FP32 (default, fast) or OCWG_FP64 (reference arithmetic class). */
 int ocwg_set_precision(ocwg_ctx* ctx, int precision);
-/* Run subsequent work on an external cudaStream_t (NULL = the context's own). */
+/* Run subsequent work on an external cudaStream_t (NULL = the CUDA legacy
+ * default stream).  A new context uses its own non-blocking stream. */
 int ocwg_set_stream(ocwg_ctx* ctx, void* cuda_stream);
+/* on != 0: *_dev entry points return as soon as their work is enqueued;
+ * device-side errors (not positive definite, non-finite W) stay latched in the
+ * context and are reported by the next ocwg_synchronize. */
+int ocwg_set_async(ocwg_ctx* ctx, int on);
+/* Drain the context's stream; returns the latched status of async calls. */
 int ocwg_synchronize(ocwg_ctx* ctx);
 
 /* ---- quant.hpp --------------------------------------------------------- */

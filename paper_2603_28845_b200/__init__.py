@@ -181,6 +181,7 @@ _SIGS = {
     "ocwg_set_stream": (C.c_int, [_P, _P]),
     "ocwg_set_precision": (C.c_int, [_P, C.c_int]),
     "ocwg_synchronize": (C.c_int, [_P]),
+    "ocwg_set_async": (C.c_int, [_P, C.c_int]),
     "ocwg_validate_config": (C.c_int, [C.POINTER(_QCfg)]),
     "ocwg_group_count": (_U64, [C.POINTER(_QCfg), _U64, _U64]),
     "ocwg_storage_bytes": (_U64, [C.POINTER(_QCfg), _U64, _U64]),

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -34,8 +35,15 @@ struct ocwg_ctx {
   int precision = OCWG_FP32;  // factorisation + sweep arithmetic
   bool profile = false;       // record phase events in run_gptq
   bool tensor_core_gemm = true;  // fp32 GEMMs on tcgen05 (3xTF32) vs SIMT
+  bool async_dev = false;        // *_dev calls return without draining the stream
   cudaEvent_t ev[6] = {};
   double phase_ms[5] = {};
+  cudaStream_t aux = nullptr;      // second stream: the sweep's trailing GEMMs
+  cudaEvent_t sev[5] = {};         // sweep fork / in-block / trailing x2 / join
+  cudaStream_t cpy = nullptr;      // host <-> device copies of the host-pointer calls
+  void* io = nullptr;              // grow-only device buffers of the host-pointer calls
+  size_t io_bytes = 0;
+  std::vector<cudaEvent_t> cev;    // per-chunk copy events
   std::mutex mu;
 };
 
@@ -137,10 +145,12 @@ struct Arena {
   }
 };
 
-void begin(ocwg_ctx* ctx) {
+void begin(ocwg_ctx* ctx, bool dev_call = false) {
   if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-  ck(cudaMemsetAsync(ctx->flag, 0, sizeof(unsigned), ctx->stream), "reset status");
+  // async device calls keep the status word sticky until ocwg_synchronize
+  if (!(dev_call && ctx->async_dev))
+    ck(cudaMemsetAsync(ctx->flag, 0, sizeof(unsigned), ctx->stream), "reset status");
 }
 
 // drain the stream; map device status bits to the reference's error classes
@@ -158,6 +168,15 @@ void finish(ocwg_ctx* ctx, bool numeric_first = true) {
     fail(OCWG_NUMERIC_ERROR, "gptq_quantize: Gram matrix is not positive definite after dampening");
 }
 
+// device-pointer entry points: drain (and map the status word) unless async
+void finish_dev(ocwg_ctx* ctx) {
+  if (ctx->async_dev) {
+    ck(cudaGetLastError(), "kernel launch");
+    return;
+  }
+  finish(ctx);
+}
+
 void h2d(void* d, const void* h, size_t bytes, ocwg_ctx* ctx) {
   if (bytes) ck(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D");
 }
@@ -169,40 +188,74 @@ void d2h(void* h, const void* d, size_t bytes, ocwg_ctx* ctx) {
 struct GptqBufs {
   int32_t* order;
   double* damp;
-  void* a;    // n x n  T
-  void* u;    // n x n  T
-  void* fws;  // nblk*64*64 + n*n  T
-  void* wp;   // n x m  T
-  void* err;  // 128 x m T
+  void* a;     // n x n  T: factor input, overwritten by L
+  void* ghi;   // n x n  T: G (tf32 hi part when split)
+  float* glo;  // n x n  fp32 lo part (null: plain G in ghi)
+  void* gpl;   // n x n  T: plain G (== ghi when not split)
+  int* flags;  // Cholesky tile flags
+  void* acc;   // n x m  T: sweep partial sums
+  void* dpl[2];   // D (m x 128 T), by block parity
+  float* dhi[2];  // D tf32 hi / lo (split only)
+  float* dlo[2];
   float* tcws;
   size_t tcws_floats;
 };
 
-size_t tc_ws_floats(uint64_t n, uint64_t m) {
-  // largest fp32 GEMM operand pair of the factorisation / sweep
-  const long long nn = (long long)n, mm_ = (long long)std::max<uint64_t>(m, 1);
-  // sweep trailing (n x m x 128), Cholesky SYRK (n x n x 64), inverse doubling
-  // (batched, <= 2 * n * n operand floats in total per level)
-  return std::max({tc_gemm_workspace_floats(nn, mm_, kMaxSweepBlock),
-                   tc_gemm_workspace_floats(nn, nn, 64), size_t(2 * nn * nn + 4 * nn * 4 + 64)});
+long long chol_macro_cols(uint64_t n) {
+  if (const char* e = getenv("OCWG_CHOL_MACRO")) return atoll(e);
+  return n <= 4608 ? 0 : 2048;
 }
 
-void gptq_reserve(Arena& ar, uint64_t n, uint64_t m, int precision, size_t* o) {
-  const uint64_t nblk = (n + 63) / 64;
-  const size_t es = precision == OCWG_FP64 ? 8 : 4;
+// G / D stored as tf32 hi/lo pairs for the tcgen05 3xTF32 trailing GEMM
+bool split_g(const ocwg_ctx* ctx, uint64_t n) {
+  return ctx->precision == OCWG_FP32 && ctx->tensor_core_gemm && n % 4 == 0;
+}
+
+size_t tc_ws_floats(uint64_t n) {
+  // largest mm<float> of the factorisation: the macro-panel trailing SYRK
+  // (n x n x macro) and the parity-artefact inverse doubling (<= 2 n^2 per level)
+  const long long nn = (long long)n;
+  const long long mc = std::max<long long>(64, chol_macro_cols(n) > 0 ? chol_macro_cols(n) : 64);
+  return std::max(tc_gemm_workspace_floats(nn, nn, mc), size_t(2 * nn * nn + 4 * nn * 4 + 64));
+}
+
+void gptq_reserve(Arena& ar, const ocwg_ctx* ctx, uint64_t n, uint64_t m, size_t* o) {
+  const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
+  const bool split = split_g(ctx, n);
+  const size_t de = sweep_delta_elems((long long)std::max<uint64_t>(m, 1));
   o[0] = ar.reserve(n * sizeof(int32_t));
   o[1] = ar.reserve(sizeof(double));
   o[2] = ar.reserve(n * n * es);
   o[3] = ar.reserve(n * n * es);
-  o[4] = ar.reserve((nblk * 64 * 64 + n * n) * es);
-  o[5] = ar.reserve(n * m * es);
-  o[6] = ar.reserve(kMaxSweepBlock * m * es);
-  o[7] = ar.reserve(tc_ws_floats(n, m) * sizeof(float));
+  o[4] = ar.reserve(split ? 2 * n * n * 4 : 0);
+  o[5] = ar.reserve(cholesky_flag_ints((long long)n) * sizeof(int));
+  o[6] = ar.reserve(n * std::max<uint64_t>(m, 1) * es);
+  o[7] = ar.reserve(2 * de * es);
+  o[8] = ar.reserve(split ? 4 * de * 4 : 0);
+  o[9] = ar.reserve(tc_ws_floats(n) * sizeof(float));
 }
-GptqBufs gptq_bufs(const Arena& ar, const size_t* o, uint64_t n, uint64_t m) {
-  return {ar.at<int32_t>(o[0]), ar.at<double>(o[1]), ar.at<void>(o[2]), ar.at<void>(o[3]),
-          ar.at<void>(o[4]), ar.at<void>(o[5]), ar.at<void>(o[6]), ar.at<float>(o[7]),
-          tc_ws_floats(n, m)};
+GptqBufs gptq_bufs(const Arena& ar, const ocwg_ctx* ctx, const size_t* o, uint64_t n, uint64_t m) {
+  const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
+  const bool split = split_g(ctx, n);
+  const size_t de = sweep_delta_elems((long long)std::max<uint64_t>(m, 1));
+  GptqBufs b;
+  b.order = ar.at<int32_t>(o[0]);
+  b.damp = ar.at<double>(o[1]);
+  b.a = ar.at<void>(o[2]);
+  b.ghi = ar.at<void>(o[3]);
+  b.glo = split ? ar.at<float>(o[4]) : nullptr;
+  b.gpl = split ? static_cast<void*>(ar.at<float>(o[4]) + n * n) : b.ghi;
+  b.flags = ar.at<int>(o[5]);
+  b.acc = ar.at<void>(o[6]);
+  b.dpl[0] = ar.at<char>(o[7]);
+  b.dpl[1] = ar.at<char>(o[7]) + de * es;
+  for (int k = 0; k < 2; ++k) {
+    b.dhi[k] = split ? ar.at<float>(o[8]) + (2 * k) * de : nullptr;
+    b.dlo[k] = split ? ar.at<float>(o[8]) + (2 * k + 1) * de : nullptr;
+  }
+  b.tcws = ar.at<float>(o[9]);
+  b.tcws_floats = tc_ws_floats(n);
+  return b;
 }
 
 template <typename T>
@@ -214,13 +267,16 @@ void run_factor_t(ocwg_ctx* ctx, const float* h_dev, uint64_t n, int actorder, d
   launch_build_factor_input<T>(h_dev, (long long)n, b.order, percdamp, static_cast<T*>(b.a), b.damp,
                                st);
   if (ctx->profile) cudaEventRecord(ctx->ev[1], st);
-  factor_upper_inverse<T>(static_cast<T*>(b.a), (long long)n, static_cast<T*>(b.u),
-                          static_cast<T*>(b.fws), ctx->flag, st,
-                          ctx->profile ? ctx->ev[2] : nullptr);
-  if (ctx->profile) cudaEventRecord(ctx->ev[3], st);
+  cholesky_g<T>(static_cast<T*>(b.a), (long long)n, static_cast<T*>(b.ghi), b.glo,
+                b.glo ? static_cast<float*>(b.gpl) : nullptr, b.flags, ctx->flag,
+                chol_macro_cols(n), st);
+  if (ctx->profile) {
+    cudaEventRecord(ctx->ev[2], st);
+    cudaEventRecord(ctx->ev[3], st);  // (no triangular inverse on the hot path)
+  }
 }
 
-// order + damp + factorisation -> U (device); the reference's :29-51
+// order + damp + Cholesky (L, G) on device; the reference's :29-51
 void run_factor(ocwg_ctx* ctx, const float* h_dev, uint64_t n, int actorder, double percdamp,
                 const GptqBufs& b) {
   if (ctx->precision == OCWG_FP64)
@@ -233,13 +289,13 @@ template <typename T>
 void run_sweep_t(ocwg_ctx* ctx, const float* w, uint64_t ldw, uint64_t n, uint64_t m, const QCfg& c,
                  const ocwg_gptq_options* opts, int16_t* codes, const float* scales,
                  const int32_t* zeros, float* w_hat, const GptqBufs& b) {
-  cudaStream_t st = ctx->stream;
-  set_tc_workspace(ctx->tensor_core_gemm ? b.tcws : nullptr, b.tcws_floats);
-  launch_permute_rows<T>(w, (long long)n, (long long)m, (long long)ldw, b.order,
-                         static_cast<T*>(b.wp), st);
-  gptq_sweep<T>(static_cast<T*>(b.wp), (long long)n, (long long)m, static_cast<const T*>(b.u),
-                b.order, c, scales, zeros, (long long)opts->block_cols, codes, w_hat,
-                (long long)ldw, static_cast<T*>(b.err), st);
+  T* const dp[2] = {static_cast<T*>(b.dpl[0]), static_cast<T*>(b.dpl[1])};
+  float* const dh[2] = {b.dhi[0], b.dhi[1]};
+  float* const dl[2] = {b.dlo[0], b.dlo[1]};
+  gptq_sweep_g<T>(w, (long long)ldw, (long long)n, (long long)m, static_cast<const T*>(b.gpl),
+                  static_cast<const T*>(b.ghi), b.glo, b.order, c, scales, zeros,
+                  (long long)opts->block_cols, codes, w_hat, (long long)ldw, static_cast<T*>(b.acc),
+                  dp, dh, dl, ctx->stream, ctx->aux, ctx->sev);
 }
 
 // gptq_quantize on device buffers (w row stride ldw; codes/w_hat stride ldw)
@@ -296,6 +352,9 @@ int ocwg_create(int device, ocwg_ctx** out) {
     c->device = device;
     ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own;
+    ck(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking), "cudaStreamCreate(aux)");
+    ck(cudaStreamCreateWithFlags(&c->cpy, cudaStreamNonBlocking), "cudaStreamCreate(cpy)");
+    for (auto& e : c->sev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaMalloc(&c->flag, sizeof(unsigned)), "cudaMalloc(flag)");
     ck(cudaMallocHost(&c->flag_host, sizeof(unsigned)), "cudaMallocHost(flag)");
     *out = c;
@@ -310,6 +369,15 @@ int ocwg_destroy(ocwg_ctx* ctx) {
     if (ctx->ws) cudaFree(ctx->ws);
     cudaFree(ctx->flag);
     cudaFreeHost(ctx->flag_host);
+    cudaStreamSynchronize(ctx->aux);
+    for (auto& e : ctx->sev) cudaEventDestroy(e);
+    for (auto& e : ctx->ev)
+      if (e) cudaEventDestroy(e);
+    cudaStreamSynchronize(ctx->cpy);
+    for (auto& e : ctx->cev) cudaEventDestroy(e);
+    if (ctx->io) cudaFree(ctx->io);
+    cudaStreamDestroy(ctx->cpy);
+    cudaStreamDestroy(ctx->aux);
     cudaStreamDestroy(ctx->own);
     delete ctx;
   });
@@ -340,14 +408,35 @@ int ocwg_debug_profile(ocwg_ctx* ctx, int on, double* phase_ms) {
 int ocwg_set_stream(ocwg_ctx* ctx, void* s) {
   return guard([&] {
     if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
-    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->stream = static_cast<cudaStream_t>(s);  // NULL = the legacy default stream
+  });
+}
+
+int ocwg_set_async(ocwg_ctx* ctx, int on) {
+  return guard([&] {
+    if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->async_dev = on != 0;
   });
 }
 
 int ocwg_synchronize(ocwg_ctx* ctx) {
   return guard([&] {
     if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    // drain, read and clear the (sticky) status word of async device calls
+    ck(cudaGetLastError(), "kernel launch");
+    ck(cudaMemcpyAsync(ctx->flag_host, ctx->flag, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                       ctx->stream),
+       "status D2H");
+    ck(cudaMemsetAsync(ctx->flag, 0, sizeof(unsigned), ctx->stream), "reset status");
     ck(cudaStreamSynchronize(ctx->stream), "stream synchronize");
+    const unsigned f = *ctx->flag_host;
+    if (f & kFlagNotPD)
+      fail(OCWG_NUMERIC_ERROR, "gptq_quantize: Gram matrix is not positive definite after dampening");
+    if (f & kFlagNonFinite) fail(OCWG_INVALID_INPUT, "calibrate_grids: non-finite entry");
   });
 }
 
@@ -517,10 +606,10 @@ int ocwg_pack_uniform_dev(ocwg_ctx* ctx, const int16_t* codes, const float* scal
   return guard([&] {
     validate(cfg);
     std::lock_guard<std::mutex> lk(ctx->mu);
-    begin(ctx);
+    begin(ctx, true);
     launch_pack(codes, (long long)(rows * cols), (long long)group_count(cfg, rows, cols),
                 qcfg(cfg, cols), scales, zeros, out, ctx->stream);
-    finish(ctx);
+    finish_dev(ctx);
   });
 }
 
@@ -610,7 +699,7 @@ int ocwg_debug_hessian_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, ui
                            float* h, int accumulate, int impl) {
   return guard([&] {
     std::lock_guard<std::mutex> lk(ctx->mu);
-    begin(ctx);
+    begin(ctx, true);
     if (tokens == 0) {
       if (!accumulate) ck(cudaMemsetAsync(h, 0, dim * dim * 4, ctx->stream), "memset");
     } else if (impl == 1) {
@@ -626,7 +715,7 @@ int ocwg_debug_hessian_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, ui
         fail(OCWG_UNSUPPORTED, "hessian: dim must be a multiple of 8 for the tensor-core path");
       if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
     }
-    finish(ctx);
+    finish_dev(ctx);
   });
 }
 
@@ -640,14 +729,20 @@ int ocwg_hessian_bf16(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, uint64_
     ck(cudaMalloc(&xd, std::max<uint64_t>(1, tokens * dim * 2)), "cudaMalloc(X)");
     h2d(xd, x, tokens * dim * 2, ctx);
     if (accumulate) h2d(hd, h, dim * dim * 4, ctx);
-    const int r = ocwg_hessian_bf16_dev(ctx, xd, tokens, dim, hd, accumulate);
+    int r = ocwg_hessian_bf16_dev(ctx, xd, tokens, dim, hd, accumulate);
+    std::string msg = g_err;
     if (r == OCWG_OK) {
       d2h(h, hd, dim * dim * 4, ctx);
-      cudaStreamSynchronize(ctx->stream);
+      try {
+        finish(ctx);  // host entry points always drain and report
+      } catch (const Error& e) {
+        r = e.code;
+        msg = e.msg;
+      }
     }
     cudaFree(hd);
     cudaFree(xd);
-    if (r != OCWG_OK) fail(r, g_err);
+    if (r != OCWG_OK) fail(r, msg);
   });
 }
 
@@ -675,25 +770,31 @@ int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, do
       fail(OCWG_INVALID_INPUT, "gptq_quantize: percdamp must be in (0, 1]");
     std::lock_guard<std::mutex> lk(ctx->mu);
     begin(ctx);
+    const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
+    const uint64_t nblk = (n + 63) / 64;
     Arena ar(ctx);
-    size_t o[8];
-    gptq_reserve(ar, n, 1, ctx->precision, o);
+    size_t o[10];
+    gptq_reserve(ar, ctx, n, 1, o);
     const size_t oh = ar.reserve(n * n * 4), ohi = ar.reserve(n * n * 8),
-                 ou64 = ar.reserve(n * n * 8);
+                 ou64 = ar.reserve(n * n * 8), ou = ar.reserve(n * n * es),
+                 ouw = ar.reserve((nblk * 64 * 64 + n * n) * es);
     ar.commit();
-    const GptqBufs b = gptq_bufs(ar, o, n, 1);
+    const GptqBufs b = gptq_bufs(ar, ctx, o, n, 1);
     h2d(ar.at<float>(oh), h, n * n * 4, ctx);
     run_factor(ctx, ar.at<float>(oh), n, actorder, percdamp, b);
     if (ctx->precision == OCWG_FP64) {
-      if (hinv) launch_gram_upper<double>(static_cast<double*>(b.u), (long long)n,
-                                          ar.at<double>(ohi), ctx->stream);
-      d2h(u, b.u, n * n * 8, ctx);
+      double* ud = ar.at<double>(ou);
+      upper_from_cholesky<double>(static_cast<double*>(b.a), (long long)n, ud, ar.at<double>(ouw),
+                                  ctx->stream);
+      if (hinv) launch_gram_upper<double>(ud, (long long)n, ar.at<double>(ohi), ctx->stream);
+      d2h(u, ud, n * n * 8, ctx);
     } else {
-      if (hinv) launch_gram_upper<float>(static_cast<float*>(b.u), (long long)n,
-                                         ar.at<double>(ohi), ctx->stream);
+      float* uf = ar.at<float>(ou);
+      upper_from_cholesky<float>(static_cast<float*>(b.a), (long long)n, uf, ar.at<float>(ouw),
+                                 ctx->stream);
+      if (hinv) launch_gram_upper<float>(uf, (long long)n, ar.at<double>(ohi), ctx->stream);
       // U is fp32 on the fast path: widen for the fp64 ABI
-      launch_f32_to_f64(static_cast<float*>(b.u), (long long)(n * n), ar.at<double>(ou64),
-                        ctx->stream);
+      launch_f32_to_f64(uf, (long long)(n * n), ar.at<double>(ou64), ctx->stream);
       d2h(u, ar.at<double>(ou64), n * n * 8, ctx);
     }
     std::vector<int32_t> ord(n);
@@ -713,18 +814,18 @@ int ocwg_gptq_quantize_dev(ocwg_ctx* ctx, const float* w, uint64_t ldw, const fl
   return guard([&] {
     check_gptq_args(cfg, opts, n, m);
     std::lock_guard<std::mutex> lk(ctx->mu);
-    begin(ctx);
+    begin(ctx, true);
     Arena ar(ctx);
-    size_t o[8];
-    gptq_reserve(ar, n, m, ctx->precision, o);
+    size_t o[10];
+    gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     ar.commit();
     if (n && m)
       run_gptq(ctx, w, ldw, h, n, m, cfg, opts, mode, codes, scales, zeros, w_hat,
-               gptq_bufs(ar, o, n, m), ar.at<float>(om));
+               gptq_bufs(ar, ctx, o, n, m), ar.at<float>(om));
     else if (n)
-      run_factor(ctx, h, n, opts->actorder, opts->percdamp, gptq_bufs(ar, o, n, m));
-    finish(ctx);
+      run_factor(ctx, h, n, opts->actorder, opts->percdamp, gptq_bufs(ar, ctx, o, n, m));
+    finish_dev(ctx);
     if (n == 0 || m == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
   });
 }
@@ -753,16 +854,21 @@ int ocwg_gptq_quantize(ocwg_ctx* ctx, const float* w, const float* h, uint64_t n
     float* whd = reinterpret_cast<float*>(take(n * m * 4));
     h2d(wd, w, n * m * 4, ctx);
     h2d(hd, h, n * n * 4, ctx);
-    const int r = ocwg_gptq_quantize_dev(ctx, wd, m, hd, n, m, cfg, opts, mode, cd, sd, zd,
-                                         w_hat ? whd : nullptr);
+    int r = ocwg_gptq_quantize_dev(ctx, wd, m, hd, n, m, cfg, opts, mode, cd, sd, zd,
+                                   w_hat ? whd : nullptr);
+    std::string msg = g_err;
     if (r == OCWG_OK) {
       d2h(codes, cd, n * m * 2, ctx);
       d2h(scales, sd, ng * 4, ctx);
       d2h(zeros, zd, ng * 4, ctx);
       if (w_hat) d2h(w_hat, whd, n * m * 4, ctx);
-      cudaStreamSynchronize(ctx->stream);
+      try {
+        finish(ctx);  // host entry points always drain and report
+      } catch (const Error& e) {
+        r = e.code;
+        msg = e.msg;
+      }
     }
-    const std::string msg = g_err;
     cudaFree(blob);
     if (r != OCWG_OK) fail(r, msg);
   });
@@ -802,11 +908,11 @@ int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, 
     check_gptq_args(cfg, opts, n, m);
     if (n == 0 || m == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
     std::lock_guard<std::mutex> lk(ctx->mu);
-    begin(ctx);
+    begin(ctx, true);
     const uint64_t ng = group_count(cfg, n, m);
     Arena ar(ctx);
-    size_t o[8];
-    gptq_reserve(ar, n, m, ctx->precision, o);
+    size_t o[10];
+    gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const size_t oh = ar.reserve(n * n * 4);
     const size_t hws = hessian_tc_workspace_bytes((long long)tokens, (long long)n);
@@ -825,14 +931,19 @@ int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, 
       if (r == -1) hessian_simt(x, (long long)tokens, (long long)n, h, 0, ctx->stream);
       else if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
     }
-    run_gptq(ctx, w, m, h, n, m, cfg, opts, mode, cd, sd, zd, w_hat, gptq_bufs(ar, o, n, m),
+    run_gptq(ctx, w, m, h, n, m, cfg, opts, mode, cd, sd, zd, w_hat, gptq_bufs(ar, ctx, o, n, m),
              ar.at<float>(om));
     if (payload) launch_pack(cd, (long long)(n * m), (long long)ng, qcfg(cfg, m), sd, zd, payload,
                              ctx->stream);
-    finish(ctx);
+    finish_dev(ctx);
   });
 }
 
+// Host buffers in, host buffers out.  X streams to the device in token chunks
+// on the copy stream while the tensor cores accumulate H chunk by chunk
+// (accumulate_stats' streaming contract, stats.cpp:10-19 / test_core.cpp:280-293),
+// so the PCIe transfer overlaps the Hessian; device buffers are context-owned
+// and reused across calls.
 int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint64_t tokens,
                           uint64_t n, uint64_t m, const ocwg_quant_config* cfg,
                           const ocwg_gptq_options* opts, int mode, int16_t* codes, float* scales,
@@ -840,48 +951,84 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
                           float* h_out) {
   return guard([&] {
     check_gptq_args(cfg, opts, n, m);
-    validate(cfg);
+    if (n == 0 || m == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
     const uint64_t ng = group_count(cfg, n, m), pb = storage_bytes(cfg, n, m);
     if (payload && payload_len < pb) fail(OCWG_INVALID_INPUT, "payload buffer too small");
-    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-    std::vector<void*> bufs;
-    auto dalloc = [&](size_t b) {
-      void* p = nullptr;
-      ck(cudaMalloc(&p, std::max<size_t>(b, 1)), "cudaMalloc(io)");
-      bufs.push_back(p);
-      return p;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    cudaStream_t st = ctx->stream;
+    // ---- context-owned io buffers (grow only)
+    size_t off = 0;
+    auto take = [&](size_t b) {
+      const size_t o = off;
+      off += (b + 255) & ~size_t(255);
+      return o;
     };
-    int r = OCWG_OK;
-    std::string msg;
-    try {
-      float* wd = static_cast<float*>(dalloc(n * m * 4));
-      uint16_t* xd = static_cast<uint16_t*>(dalloc(tokens * n * 2));
-      int16_t* cd = static_cast<int16_t*>(dalloc(n * m * 2));
-      float* sd = static_cast<float*>(dalloc(ng * 4));
-      int32_t* zd = static_cast<int32_t*>(dalloc(ng * 4));
-      float* whd = w_hat ? static_cast<float*>(dalloc(n * m * 4)) : nullptr;
-      uint8_t* pd = payload ? static_cast<uint8_t*>(dalloc(pb)) : nullptr;
-      float* hd = h_out ? static_cast<float*>(dalloc(n * n * 4)) : nullptr;
-      h2d(wd, w, n * m * 4, ctx);
-      h2d(xd, x, tokens * n * 2, ctx);
-      r = ocwg_quantize_layer_x_dev(ctx, wd, xd, tokens, n, m, cfg, opts, mode, cd, sd, zd, whd, pd,
-                                    hd);
-      msg = g_err;
-      if (r == OCWG_OK) {
-        d2h(codes, cd, n * m * 2, ctx);
-        d2h(scales, sd, ng * 4, ctx);
-        d2h(zeros, zd, ng * 4, ctx);
-        if (w_hat) d2h(w_hat, whd, n * m * 4, ctx);
-        if (payload) d2h(payload, pd, pb, ctx);
-        if (h_out) d2h(h_out, hd, n * n * 4, ctx);
-        ck(cudaStreamSynchronize(ctx->stream), "sync");
-      }
-    } catch (const Error& e) {
-      r = e.code;
-      msg = e.msg;
+    const size_t ow = take(n * m * 4), ox = take(std::max<uint64_t>(1, tokens) * n * 2),
+                 oc = take(n * m * 2), os = take(ng * 4), oz = take(ng * 4),
+                 owh = take(n * m * 4), opl = take(pb), oh = take(n * n * 4);
+    if (off > ctx->io_bytes) {
+      ck(cudaStreamSynchronize(st), "sync");
+      if (ctx->io) cudaFree(ctx->io);
+      ctx->io = nullptr;
+      ctx->io_bytes = 0;
+      ck(cudaMalloc(&ctx->io, off), "cudaMalloc(io)");
+      ctx->io_bytes = off;
     }
-    for (void* p : bufs) cudaFree(p);
-    if (r != OCWG_OK) fail(r, msg);
+    char* io = static_cast<char*>(ctx->io);
+    float* wd = reinterpret_cast<float*>(io + ow);
+    uint16_t* xd = reinterpret_cast<uint16_t*>(io + ox);
+    int16_t* cd = reinterpret_cast<int16_t*>(io + oc);
+    float* sd = reinterpret_cast<float*>(io + os);
+    int32_t* zd = reinterpret_cast<int32_t*>(io + oz);
+    float* whd = reinterpret_cast<float*>(io + owh);
+    uint8_t* pd = reinterpret_cast<uint8_t*>(io + opl);
+    float* hd = reinterpret_cast<float*>(io + oh);
+    // ---- workspace
+    Arena ar(ctx);
+    size_t o[10];
+    gptq_reserve(ar, ctx, n, m, o);
+    const size_t om = ar.reserve(4096 * 4);
+    const long long chunk = 32768;  // tokens per H2D chunk (a multiple of the 16384 split)
+    const size_t hws = hessian_tc_workspace_bytes(std::min<long long>(chunk, (long long)tokens),
+                                                  (long long)n);
+    const size_t ohw = ar.reserve(hws);
+    ar.commit();
+    // ---- pipeline: W and X chunks on the copy stream, H chunk by chunk on st
+    const long long nchunks = tokens ? ((long long)tokens + chunk - 1) / chunk : 0;
+    while ((long long)ctx->cev.size() < nchunks + 2) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      ctx->cev.push_back(e);
+    }
+    ck(cudaEventRecord(ctx->cev[0], st), "event");  // copies start after prior work on st
+    ck(cudaStreamWaitEvent(ctx->cpy, ctx->cev[0], 0), "event");
+    ck(cudaMemcpyAsync(wd, w, n * m * 4, cudaMemcpyHostToDevice, ctx->cpy), "H2D(W)");
+    ck(cudaEventRecord(ctx->cev[1], ctx->cpy), "event");
+    if (tokens == 0) ck(cudaMemsetAsync(hd, 0, n * n * 4, st), "memset");
+    for (long long k = 0; k < nchunks; ++k) {
+      const long long t0 = k * chunk, tc = std::min<long long>(chunk, (long long)tokens - t0);
+      ck(cudaMemcpyAsync(xd + t0 * n, x + t0 * n, size_t(tc) * n * 2, cudaMemcpyHostToDevice,
+                         ctx->cpy),
+         "H2D(X)");
+      ck(cudaEventRecord(ctx->cev[2 + k], ctx->cpy), "event");
+      ck(cudaStreamWaitEvent(st, ctx->cev[2 + k], 0), "event");
+      const int r = hessian_tc(xd + t0 * n, tc, (long long)n, hd, k > 0 ? 1 : 0, ar.at<void>(ohw),
+                               hws, st);
+      if (r == -1) hessian_simt(xd + t0 * n, tc, (long long)n, hd, k > 0 ? 1 : 0, st);
+      else if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
+    }
+    ck(cudaStreamWaitEvent(st, ctx->cev[1], 0), "event");  // W resident
+    run_gptq(ctx, wd, m, hd, n, m, cfg, opts, mode, cd, sd, zd, w_hat ? whd : nullptr,
+             gptq_bufs(ar, ctx, o, n, m), ar.at<float>(om));
+    if (payload) launch_pack(cd, (long long)(n * m), (long long)ng, qcfg(cfg, m), sd, zd, pd, st);
+    d2h(codes, cd, n * m * 2, ctx);
+    d2h(scales, sd, ng * 4, ctx);
+    d2h(zeros, zd, ng * 4, ctx);
+    if (w_hat) d2h(w_hat, whd, n * m * 4, ctx);
+    if (payload) d2h(payload, pd, pb, ctx);
+    if (h_out) d2h(h_out, hd, n * n * 4, ctx);
+    finish(ctx);
   });
 }
 

@@ -1,20 +1,31 @@
 // On-GPU factorisation for GPTQ (replaces layerwise.cpp:31-51):
 //   hd = fp64(H); damp = percdamp*mean(diag(hd)); hd += damp*I;
 //   hp = P hd P^T;  hinv = hp^-1;  U = upper Cholesky factor of hinv.
-// Computed as  A = J hp J = L L^T (lower, blocked right-looking),
-//              U = J L^-1 J.
-// Mathematically identical to the reference's LLT -> solve(I) -> LLT (by the
-// uniqueness of the Cholesky factor of hinv), with 2n^3/3 (Cholesky n^3/3 +
-// inverse) instead of 8n^3/3 flops.  Templated on the compute type T (float
-// default, double = the reference's arithmetic class).
 //
-// Cholesky: one fused launch per 64-column panel (every CTA factors + inverts
-// the 64x64 diagonal block in shared memory; CTA 0 stores L_kk and L_kk^-1,
-// CTA c >= 1 solves its 64-row slice of the panel), then one trailing SYRK
-// (tensor cores in fp32 mode).  Triangular inverse: log-depth recursive
-// doubling over the diagonal blocks,
-//   inv([A 0; B C]) = [A^-1 0; -C^-1 (B A^-1), C^-1],
-// each level two batched GEMMs (6 levels for n = 4096).
+// The reference forms hinv and factors it again (8n^3/3 flops).  Here
+//   A = J hp J = L L^T                 (one Cholesky, n^3/3 flops)
+// and the sweep consumes L directly.  U = (J L J)^-1 by uniqueness of the
+// Cholesky factor, so with D = diag(U) the reference's error propagation
+//   wp[k] -= U[i,k] * (wp[i] - w_hat[i]) / U[i,i]              (layerwise.cpp:76-90)
+// unrolls to the closed form (V = D^-1 U unit upper)
+//   w_cur[k] = w[k] + sum_{i<k} G[k,i] * (w[i] - w_hat[i]),    G = V^-T - I,
+//   G[k,i]  = L[n-1-i, n-1-k] / L[n-1-k, n-1-k]                 (i < k).
+// i.e. G is the unit-lower LDL^T factor of hp read in processing order.  No
+// triangular inverse is on the hot path; the inverse (for the H^-1 / U
+// parity artefacts of ocwg_gptq_factor) is computed only on request.
+//
+// Cholesky: one persistent, dataflow-scheduled kernel over 64x64 tiles.
+// Work items are the lower tiles (r, c) of a column range [c0, c1) in
+// column-major order, handed out by an atomic counter; item (r, c) computes
+//   S = A[r,c] - sum_{c0<=k<c} L[r,k] L[c,k]^T
+// waiting on per-tile ready flags (acquire/release) for each L[.,k], then
+//   r == c: factors S (64-step right-looking elimination, one barrier per step)
+//   r >  c: L[r,c] = S L[c,c]^-T by forward substitution (warp shuffles only)
+// and publishes L[r,c] (and the matching block of G) with a release flag.
+// Items only ever wait on items handed out earlier, so the schedule cannot
+// deadlock whatever the residency.  Large n runs macro panels: the dataflow
+// kernel over a column range, then one tcgen05 3xTF32 SYRK for the trailing
+// matrix (gemm.cu / tc_gemm.cu).
 #include <cmath>
 
 #include "kernels.h"
@@ -22,7 +33,8 @@
 namespace ocwg {
 namespace {
 
-constexpr int NB = 64;  // panel width / base block
+constexpr int TB = 64;    // tile
+constexpr int CT = 256;   // threads per CTA: 16 x 16, each a 4x4 register block
 
 // A[i][j] = T(double(H[o(i)][o(j)]) + (i==j)*damp), o(i) = order[n-1-i]; lower only
 template <typename T>
@@ -56,173 +68,393 @@ __global__ void damp_kernel(const float* __restrict__ h, long long n, double per
   }
 }
 
-// Fused panel step at column k0 (block width nb <= 64).
-// Every CTA factors and inverts the (already updated) 64x64 diagonal block
-// with a 16x16 grid of threads, each holding a 4x4 register tile (static
-// register indices, two barriers per elimination step: publish column/row j,
-// then rank-1 update).  Rows/cols >= nb are identity padding.  CTA 0 stores
-// L_kk (into A) and L_kk^-1 (dinv); CTA c >= 1 computes its 64-row panel slice
-// L_slice = A_slice * L_kk^-T and writes it back into A.
-template <typename T>
-__device__ __forceinline__ T pick4(const T (&v)[4], int i) {
-  return i == 0 ? v[0] : (i == 1 ? v[1] : (i == 2 ? v[2] : v[3]));
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag(const int* p) {
+  while (!ld_acquire(p)) __nanosleep(20);
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) panel_kernel(T* a, long long n, long long k0, T* dinv,
-                                                    unsigned* flag) {
-  extern __shared__ __align__(16) unsigned char dsm_raw[];
-  T(*lb)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(dsm_raw);                              // L
-  T(*xb)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(dsm_raw + sizeof(T) * NB * (NB + 1));  // L^-1
-  T(*ps)[NB + 1] = reinterpret_cast<T(*)[NB + 1]>(dsm_raw + 2 * sizeof(T) * NB * (NB + 1));
-  T* diag = reinterpret_cast<T*>(dsm_raw + 3 * sizeof(T) * NB * (NB + 1));
-  T* vec = diag + NB;  // column j of L / row j of L^-1 being published
-  const int nb = int(min((long long)NB, n - k0));
-  const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
-  const long long r0 = k0 + nb + (long long)(blockIdx.x - 1) * NB;  // panel slice rows
-  const int pr = blockIdx.x == 0 ? 0 : int(min((long long)NB, n - r0));
+__device__ __forceinline__ T ldcg(const T* p) {
+  return __ldcg(p);
+}
 
-  T t[4][4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int r = 4 * ti + u, c = 4 * tj + v;
-      T val = T(0);
-      if (r < nb && c < nb) {
-        if (c <= r) val = a[(k0 + r) * n + k0 + c];
-      } else if (r == c) {
-        val = T(1);
-      }
-      t[u][v] = val;
-      if (r == c) diag[r] = val;
-    }
-  if (blockIdx.x > 0)
-    for (int e = tid; e < NB * NB; e += 256) {
-      const int r = e / NB, c = e % NB;
-      ps[r][c] = (r < pr && c < nb) ? a[(r0 + r) * n + k0 + c] : T(0);
-    }
-  __syncthreads();
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t u = __float_as_uint(x);
+  u = (u + 0xFFFu + ((u >> 13) & 1u)) & ~0x1FFFu;  // RNE to 10 mantissa bits
+  return __uint_as_float(u);
+}
 
-  // ---- Cholesky of the block (right-looking, lower)
-  bool bad = false;
-  for (int j = 0; j < NB; ++j) {
-    const T piv = diag[j];
-    const T d = sqrt(piv);
-    const T rd = T(1) / d;
-    if (tid == 0 && j < nb) bad |= !(piv > T(0));  // Eigen: x <= 0 -> NumericalIssue
-    if (tj == (j >> 2) && ti >= tj) {
-      const int jj = j & 3;
+// A 64x64 tile (row-major, ld) <-> 16 elements per thread: rows tid/16 + 16*ii,
+// cols 4*(tid%16) + e.  Out-of-range elements read as 0.
+template <typename T>
+struct TileRegs {
+  T v[4][4];
+};
+
+template <typename T>
+__device__ __forceinline__ void load_tile(TileRegs<T>& R, const T* base, long long ld, int rows,
+                                          int cols, bool vec_ok) {
+  const int tid = threadIdx.x, c4 = (tid & 15) * 4;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = 4 * ti + u;
-        if (r > j) {
-          const T lv = pick4(t[u], jj) * rd;
-          vec[r] = lv;
-          lb[r][j] = lv;
-        } else if (r == j) {
-          lb[j][j] = d;
-        }
+  for (int ii = 0; ii < 4; ++ii) {
+    const int r = (tid >> 4) + 16 * ii;
+    const T* p = base + (long long)r * ld + c4;
+    if (vec_ok && r < rows && c4 + 4 <= cols) {
+      if constexpr (sizeof(T) == 4) {
+        const float4 f = __ldcg(reinterpret_cast<const float4*>(p));
+        R.v[ii][0] = f.x, R.v[ii][1] = f.y, R.v[ii][2] = f.z, R.v[ii][3] = f.w;
+      } else {
+        const double2 f0 = __ldcg(reinterpret_cast<const double2*>(p));
+        const double2 f1 = __ldcg(reinterpret_cast<const double2*>(p + 2));
+        R.v[ii][0] = f0.x, R.v[ii][1] = f0.y, R.v[ii][2] = f1.x, R.v[ii][3] = f1.y;
       }
-    }
-    __syncthreads();
-    if (ti >= tj && 4 * ti + 3 > j && 4 * tj + 3 > j) {
+    } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = 4 * ti + u;
-        if (r <= j) continue;
-        const T lr = vec[r];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int c = 4 * tj + v;
-          if (c > j && c <= r) t[u][v] -= lr * vec[c];
-        }
-        if (ti == tj) diag[r] = t[u][u];
-      }
+      for (int e = 0; e < 4; ++e) R.v[ii][e] = (r < rows && c4 + e < cols) ? ldcg(p + e) : T(0);
     }
-    __syncthreads();
   }
-  // ---- X = L^-1 (right-looking): publish row j of X scaled by 1/L_jj, update rows below
+}
+
+// Store the tile transposed into swizzled k-major smem: S[k][i] at
+// k*64 + ((i/4) ^ ((k/4)&15))*4 + i%4  (conflict-free stores and float4 reads).
+template <typename T>
+__device__ __forceinline__ void store_tile_t(const TileRegs<T>& R, T* S) {
+  const int tid = threadIdx.x, tx = tid & 15;
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int ii = 0; ii < 4; ++ii) {
+    const int i = (tid >> 4) + 16 * ii;
+    const int pg = (i >> 2) ^ tx;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) t[u][v] = T((4 * ti + u) == (4 * tj + v) ? 1 : 0);
-  for (int j = 0; j < NB; ++j) {
-    const T rl = T(1) / lb[j][j];
-    if (ti == (j >> 2) && 4 * tj <= j) {
-      const int jj = j & 3;
-#pragma unroll
-      for (int uu = 0; uu < 4; ++uu) {
-        if (uu != jj) continue;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int c = 4 * tj + v;
-          if (c <= j) {
-            t[uu][v] *= rl;
-            vec[c] = t[uu][v];
-          }
-        }
-      }
+    for (int e = 0; e < 4; ++e) {
+      const int k = 4 * tx + e;
+      S[k * TB + pg * 4 + (i & 3)] = R.v[ii][e];
     }
-    __syncthreads();
-    if (ti >= (j >> 2) && 4 * tj <= j) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = 4 * ti + u;
-        if (r <= j) continue;
-        const T lr = lb[r][j];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int c = 4 * tj + v;
-          if (c <= j) t[u][v] -= lr * vec[c];
-        }
-      }
-    }
-    __syncthreads();
   }
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int r = 4 * ti + u, c = 4 * tj + v;
-      xb[r][c] = (c <= r) ? t[u][v] : T(0);
-    }
-  __syncthreads();
-  if (blockIdx.x == 0) {
-    for (int e = tid; e < NB * NB; e += 256) {
-      const int r = e / NB, c = e % NB;
-      if (r < nb && c < nb) {
-        if (c <= r) a[(k0 + r) * n + k0 + c] = lb[r][c];
-        dinv[r * NB + c] = xb[r][c];
-      }
-    }
-    if (tid == 0 && bad) atomicOr(flag, kFlagNotPD);
-    return;
+}
+
+template <typename T>
+__device__ __forceinline__ void ld4(const T* p, T (&o)[4]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    o[0] = f.x, o[1] = f.y, o[2] = f.z, o[3] = f.w;
+  } else {
+    const double2 f0 = *reinterpret_cast<const double2*>(p);
+    const double2 f1 = *reinterpret_cast<const double2*>(p + 2);
+    o[0] = f0.x, o[1] = f0.y, o[2] = f1.x, o[3] = f1.y;
   }
-  // ---- panel slice: out[r][c] = sum_k P[r][k] * X[c][k]
-  T acc[4][4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) acc[u][v] = T(0);
-  for (int k = 0; k < NB; ++k) {
-    T pv[4], xv[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) pv[u] = ps[4 * ti + u][k];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) xv[v] = xb[4 * tj + v][k];
+}
+
+// acc[u][v] += sum_k P[4ty+u][k] * Q[4tx+v][k]
+template <typename T>
+__device__ __forceinline__ void tile_mma(T (&acc)[4][4], const T* Ps, const T* Qs) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+#pragma unroll 4
+  for (int k = 0; k < TB; ++k) {
+    const int sw = (k >> 2) & 15;
+    T p[4], q[4];
+    ld4(Ps + k * TB + ((ty ^ sw) << 2), p);
+    ld4(Qs + k * TB + ((tx ^ sw) << 2), q);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] += pv[u] * xv[v];
+      for (int v = 0; v < 4; ++v) acc[u][v] = fma(p[u], q[v], acc[u][v]);
   }
+}
+
+template <typename T>
+struct CholSmem {
+  T ps[TB * TB];
+  T qs[TB * TB];
+  T lt[TB][TB + 4];   // diag tile L_cc transposed (lt[j][c] = L[c][j]); also G staging
+  T col[2][TB];       // published column (diag elimination)
+  T rdiag[TB];
+  int item;
+  int ready;
+};
+
+// Publish the finalised tile (values in t, rows b = 64r + 4ty + u, cols
+// a = 64c + 4tx + v) into G: G[n-1-a][n-1-b] = L[b][a] / L[a][a] for b > a.
+// `diag` holds L[a][a] for the tile's column range.  Uses sm.lt as staging.
+template <typename T>
+__device__ void emit_g(const T (&t)[4][4], CholSmem<T>& sm, const T* diag, int r, int c, long long n,
+                       T* ghi, float* glo, float* gpl) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  __syncthreads();
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int r = 4 * ti + u, c = 4 * tj + v;
-      if (r < pr && c < nb) a[(r0 + r) * n + k0 + c] = acc[u][v];
+    for (int v = 0; v < 4; ++v) sm.lt[4 * ty + u][4 * tx + v] = t[u][v];
+  __syncthreads();
+  const long long b0 = (long long)r * TB, a0 = (long long)c * TB;
+  for (int e = tid; e < TB * TB; e += CT) {
+    const int al = e >> 6, q = e & 63;  // G row k = n-1-(a0+al); col i = n-1-(b0+63-q)
+    const int bl = 63 - q;
+    const long long a = a0 + al, b = b0 + bl;
+    if (a >= n || b >= n) continue;
+    T g = T(0);
+    if (b > a) g = sm.lt[bl][al] / diag[al];
+    const long long off = (n - 1 - a) * n + (n - 1 - b);
+    if (sizeof(T) == 4 && glo) {
+      const float hi = tf32_hi(float(g));
+      ghi[off] = T(hi);
+      glo[off] = float(g) - hi;
+      gpl[off] = float(g);
+    } else {
+      ghi[off] = g;
     }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
+    chol_tile_kernel(T* __restrict__ a, long long n, int nt, int c0, int c1, int* flags,
+                     int* counter, unsigned* status, T* ghi, float* glo, float* gpl) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  CholSmem<T>& sm = *reinterpret_cast<CholSmem<T>*>(smraw);
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15, lane = tid & 31;
+  const bool vec_ok = (sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0);
+  long long total = 0;
+  for (int c = c0; c < c1; ++c) total += nt - c;
+
+  while (true) {
+    if (tid == 0) sm.item = atomicAdd(counter, 1);
+    __syncthreads();
+    long long idx = sm.item;
+    __syncthreads();
+    if (idx >= total) break;
+    int c = c0;
+    while (idx >= nt - c) {
+      idx -= nt - c;
+      ++c;
+    }
+    const int r = c + int(idx);
+    const int rows = int(std::min<long long>(TB, n - (long long)r * TB));
+    const int cols = int(std::min<long long>(TB, n - (long long)c * TB));
+
+    // ---- S = A[r,c] - sum_k L[r,k] L[c,k]^T
+    T acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = T(0);
+    TileRegs<T> P, Q;
+    if (c0 < c) {
+      if (tid == 0) {
+        wait_flag(flags + r * nt + c0);
+        wait_flag(flags + c * nt + c0);
+      }
+      __syncthreads();
+      load_tile(P, a + (long long)r * TB * n + (long long)c0 * TB, n, rows, TB, vec_ok);
+      load_tile(Q, a + (long long)c * TB * n + (long long)c0 * TB, n, cols, TB, vec_ok);
+    }
+    for (int k = c0; k < c; ++k) {
+      store_tile_t(P, sm.ps);
+      store_tile_t(Q, sm.qs);
+      const bool more = k + 1 < c;
+      const int* fr = flags + r * nt + k + 1;
+      const int* fc = flags + c * nt + k + 1;
+      if (tid == 0) sm.ready = more && ld_acquire(fr) && ld_acquire(fc);
+      __syncthreads();
+      const bool ready = sm.ready;
+      // prefetch k+1 under the MMA when its tiles are already published
+      if (ready) {
+        load_tile(P, a + (long long)r * TB * n + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
+        load_tile(Q, a + (long long)c * TB * n + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+      }
+      tile_mma(acc, sm.ps, sm.qs);
+      if (more && !ready) {  // at the dependency frontier: wait, then load
+        if (tid == 0) {
+          wait_flag(fr);
+          wait_flag(fc);
+        }
+        __syncthreads();
+        load_tile(P, a + (long long)r * TB * n + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
+        load_tile(Q, a + (long long)c * TB * n + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+      }
+      __syncthreads();
+    }
+    // t = A[r,c] - acc (own 4x4 block: rows 4ty+u, cols 4tx+v)
+    T t[4][4];
+    {
+      const T* ab = a + (long long)r * TB * n + (long long)c * TB;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = 4 * ty + u;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int cc = 4 * tx + v;
+          T x = (rr < rows && cc < cols) ? ab[(long long)rr * n + cc] : T(0);
+          if (r == c && rr == cc && rr >= rows) x = T(1);  // identity padding
+          t[u][v] = x - acc[u][v];
+        }
+      }
+    }
+
+    if (r == c) {
+      // ---- diagonal tile: right-looking elimination, one barrier per step.
+      // Unscaled column u[.] = a[.][j] is published; a[r][c] -= u_r u_c / u_j.
+      bool bad = false;
+#pragma unroll 1
+      for (int j0 = 0; j0 < TB; j0 += 4) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = j0 + jj, buf = j & 1;
+          if (tx == (j >> 2)) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sm.col[buf][4 * ty + u] = t[u][jj];
+          }
+          __syncthreads();
+          const T p = sm.col[buf][j];
+          bad |= !(p > T(0));
+          const T rp = T(1) / p;
+          const T sq = sqrt(p);
+          const T rsq = sq * rp;  // 1/sqrt(p)
+          T cr[4], cc[4];
+          ld4(&sm.col[buf][4 * ty], cr);
+          ld4(&sm.col[buf][4 * tx], cc);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int rr = 4 * ty + u;
+            const T cru = cr[u] * rp;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int cl = 4 * tx + v;
+              if (cl > j && cl <= rr) t[u][v] = fma(-cru, cc[v], t[u][v]);
+            }
+          }
+          if (tx == (j >> 2)) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int rr = 4 * ty + u;
+              if (rr > j) t[u][jj] = cr[u] * rsq;
+              else if (rr == j) t[u][jj] = sq;
+            }
+          }
+        }
+      }
+      if (bad && tid == 0 && cols > 0) {
+        // only pivots of real (non-padding) columns count (padding is exactly 1)
+        atomicOr(status, kFlagNotPD);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (4 * tx + v > 4 * ty + u) t[u][v] = T(0);
+      // diag values for G scaling
+      if (tx == ty) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sm.rdiag[4 * ty + u] = t[u][u];
+      }
+    } else {
+      // ---- off-diagonal tile: X L_cc^T = t by forward substitution
+      if (tid == 0) wait_flag(flags + c * nt + c);
+      __syncthreads();
+      {
+        const T* lb = a + (long long)c * TB * n + (long long)c * TB;
+        T x[TB * TB / CT];
+#pragma unroll
+        for (int q = 0; q < TB * TB / CT; ++q) {
+          const int e = tid + q * CT, rr = e >> 6, cl = e & 63;
+          x[q] = (rr < cols && cl <= rr) ? ldcg(lb + (long long)rr * n + cl) : T(rr == cl ? 1 : 0);
+        }
+#pragma unroll
+        for (int q = 0; q < TB * TB / CT; ++q) {
+          const int e = tid + q * CT, rr = e >> 6, cl = e & 63;
+          sm.lt[cl][rr] = x[q];  // lt[j][c] = L[c][j]
+        }
+      }
+      __syncthreads();
+      if (tid < TB) sm.rdiag[tid] = T(1) / sm.lt[tid][tid];
+      __syncthreads();
+      const int src0 = lane & 16;
+#pragma unroll 1
+      for (int j0 = 0; j0 < TB; j0 += 4) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = j0 + jj;
+          const T rd = sm.rdiag[j];
+          T x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const T own = t[u][jj] * rd;
+            x[u] = __shfl_sync(0xffffffffu, own, src0 + (j >> 2));
+          }
+          if (tx == (j >> 2)) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) t[u][jj] = x[u];
+          }
+          T l[4];
+          ld4(&sm.lt[j][4 * tx], l);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            if (4 * tx + v > j) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) t[u][v] = fma(-x[u], l[v], t[u][v]);
+            }
+          }
+        }
+      }
+      // diag values of L_cc for G scaling: lt[j][j]
+      __syncthreads();
+      if (tid < TB) sm.rdiag[tid] = sm.lt[tid][tid];
+    }
+
+    // ---- store L[r,c], publish
+    {
+      T* ab = a + (long long)r * TB * n + (long long)c * TB;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = 4 * ty + u;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int cl = 4 * tx + v;
+          if (rr < rows && cl < cols && (r != c || cl <= rr)) ab[(long long)rr * n + cl] = t[u][v];
+        }
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(flags + r * nt + c, 1);
+    if (ghi) {
+      // rdiag holds L[a][a] of column tile c (written before the last barrier)
+      emit_g(t, sm, sm.rdiag, r, c, n, ghi, glo, gpl);
+    }
+    __syncthreads();
+  }
+}
+
+// Inverse of each 64x64 diagonal block of L (lower): dinv[b] = L_bb^-1.
+// Column-parallel forward substitution (off the hot path: parity artefacts).
+template <typename T>
+__global__ void diag_inverse_kernel(const T* __restrict__ l, long long n, T* dinv) {
+  __shared__ T ls[TB][TB + 1];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  T* xs = dinv + (long long)b * TB * TB;  // X[i][j] at xs[i*TB + j]
+  const long long k0 = (long long)b * TB;
+  const int w = int(std::min<long long>(TB, n - k0));
+  for (int e = tid; e < TB * TB; e += blockDim.x) {
+    const int r = e / TB, c = e % TB;
+    T v = (r < w && c < w) ? l[(k0 + r) * n + k0 + c] : T(r == c ? 1 : 0);
+    ls[r][c] = (c <= r) ? v : T(0);
+  }
+  __syncthreads();
+  if (tid < TB) {
+    const int j = tid;  // column j of the inverse: L x = e_j
+    for (int i = 0; i < TB; ++i) {
+      T s = (i == j) ? T(1) : T(0);
+      for (int k = j; k < i; ++k) s -= ls[i][k] * xs[k * TB + j];
+      xs[i * TB + j] = (i < j) ? T(0) : s / ls[i][i];
+    }
+  }
 }
 
 // X = blockdiag(dinv_k), zero elsewhere (lower block triangle is filled by the doubling)
@@ -231,8 +463,8 @@ __global__ void init_inverse_kernel(T* x, long long n, const T* __restrict__ din
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n * n;
        e += (long long)gridDim.x * blockDim.x) {
     const long long r = e / n, c = e % n;
-    const long long br = r / NB, bc = c / NB;
-    x[e] = (br == bc) ? dinv[br * NB * NB + (r % NB) * NB + (c % NB)] : T(0);
+    const long long br = r / TB, bc = c / TB;
+    x[e] = (br == bc) ? dinv[br * TB * TB + (r % TB) * TB + (c % TB)] : T(0);
   }
 }
 
@@ -251,12 +483,22 @@ inline int blocks_for(long long n) {
   return int(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
 }
 
-template <typename T>
-constexpr int panel_smem() {
-  return (3 * NB * (NB + 1) + 2 * NB) * int(sizeof(T));
+int num_sms_f() {
+  static int v = [] {
+    int dev = 0, s = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    return s;
+  }();
+  return v;
 }
 
 }  // namespace
+
+size_t cholesky_flag_ints(long long n) {
+  const long long nt = (n + TB - 1) / TB;
+  return size_t(nt * nt + 64);
+}
 
 template <typename T>
 void launch_build_factor_input(const float* h, long long n, const int32_t* order, double percdamp,
@@ -266,48 +508,62 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
   build_input_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(h, n, order, damp, a);
 }
 
-// ws layout: [nblk*NB*NB dinv blocks][n*n scratch]
 template <typename T>
-void factor_upper_inverse(T* a, long long n, T* u, T* ws, unsigned* flag, cudaStream_t st,
-                          cudaEvent_t mid) {
+void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, int* flags, unsigned* status,
+                long long macro_cols, cudaStream_t st) {
   static const bool attr = [] {
-    cudaFuncSetAttribute(panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         panel_smem<T>());
+    cudaFuncSetAttribute(chol_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(CholSmem<T>)));
     return true;
   }();
   (void)attr;
-  const long long nblk = (n + NB - 1) / NB;
-  T* dinv = ws;
-  T* tmp = ws + nblk * NB * NB;
-  // ---- Cholesky: fused panel kernel + trailing SYRK per 64 columns
-  for (long long kb = 0; kb < nblk; ++kb) {
-    const long long k0 = kb * NB, w = std::min<long long>(NB, n - k0), rest = n - k0 - w;
+  const int nt = int((n + TB - 1) / TB);
+  int* counters = flags + (long long)nt * nt;
+  cudaMemsetAsync(flags, 0, cholesky_flag_ints(n) * sizeof(int), st);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_tile_kernel<T>, CT,
+                                                sizeof(CholSmem<T>));
+  const int max_ctas = std::max(1, occ) * num_sms_f();
+  const int step = macro_cols <= 0 ? nt : int(std::max<long long>(1, macro_cols / TB));
+  int ci = 0;
+  for (int c0 = 0; c0 < nt; c0 += step, ++ci) {
+    const int c1 = std::min(nt, c0 + step);
+    long long items = 0;
+    for (int c = c0; c < c1; ++c) items += nt - c;
+    const int grid = int(std::min<long long>(items, max_ctas));
     count_launches(1);
-    panel_kernel<T><<<unsigned(1 + (rest + NB - 1) / NB), 256, panel_smem<T>(), st>>>(
-        a, n, k0, dinv + kb * NB * NB, flag);
-    if (rest > 0)
-      mm<T>(rest, rest, w, -1.0, a + (k0 + w) * n + k0, n, false, a + (k0 + w) * n + k0, n, true,
-            1.0, a + (k0 + w) * n + (k0 + w), n, true, st);
+    chol_tile_kernel<T><<<grid, CT, sizeof(CholSmem<T>), st>>>(a, n, nt, c0, c1, flags,
+                                                                counters + ci, status, ghi, glo, gpl);
+    const long long k0 = (long long)c0 * TB, k1 = std::min<long long>(n, (long long)c1 * TB);
+    const long long rest = n - k1;
+    if (rest > 0)  // trailing SYRK: A22 -= L21 L21^T (lower tiles)
+      mm<T>(rest, rest, k1 - k0, -1.0, a + k1 * n + k0, n, false, a + k1 * n + k0, n, true, 1.0,
+            a + k1 * n + k1, n, true, st);
   }
-  if (mid) cudaEventRecord(mid, st);
-  // ---- X = L^-1 by recursive doubling over the diagonal blocks (in u)
-  T* x = u;
+}
+
+// U = (J L J)^-1 from the Cholesky factor (a, lower): parity artefact path.
+// ws: nblk*64*64 + n*n elements; u receives U (n x n upper).
+template <typename T>
+void upper_from_cholesky(const T* a, long long n, T* u, T* ws, cudaStream_t st) {
+  const long long nblk = (n + TB - 1) / TB;
+  T* dinv = ws;
+  T* tmp = ws + nblk * TB * TB;
   count_launches(2);
+  diag_inverse_kernel<T><<<unsigned(nblk), 64, 0, st>>>(a, n, dinv);
+  // X = L^-1 by recursive doubling over the diagonal blocks (in u)
+  T* x = u;
   init_inverse_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(x, n, dinv);
-  for (long long s = 2 * NB; s < 2 * n; s *= 2) {
+  for (long long s = 2 * TB; s < 2 * n; s *= 2) {
     const long long h = s / 2;
-    const long long full = n / s;  // pairs with a full-size second half
-    // batched full pairs: base row/col p*s; A-block [p*s, p*s+h), C-block [p*s+h, p*s+s)
+    const long long full = n / s;
     if (full > 0) {
       const long long stride = s * (n + 1);
-      // tmp_p = L[C, A] * X[A, A]         (h x h x h)
       mm<T>(h, h, h, 1.0, a + h * n, n, false, x, n, false, 0.0, tmp, h, false, st, int(full),
             stride, stride, h * h);
-      // X[C, A] = -X[C, C] * tmp_p         (h x h x h)
       mm<T>(h, h, h, -1.0, x + h * n + h, n, false, tmp, h, false, 0.0, x + h * n, n, false, st,
             int(full), stride, h * h, stride);
     }
-    // a trailing partial pair: A-block [p0, p0+h), C-block [p0+h, n) with 0 < n-p0-h < h
     const long long p0 = full * s, c2 = n - p0 - h;
     if (c2 > 0) {
       mm<T>(c2, h, h, 1.0, a + (p0 + h) * n + p0, n, false, x + p0 * n + p0, n, false, 0.0, tmp, h,
@@ -316,6 +572,7 @@ void factor_upper_inverse(T* a, long long n, T* u, T* ws, unsigned* flag, cudaSt
             x + (p0 + h) * n + p0, n, false, st);
     }
   }
+  count_launches(1);
   reverse_to_upper_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(x, n, tmp);
   cudaMemcpyAsync(u, tmp, size_t(n * n) * sizeof(T), cudaMemcpyDeviceToDevice, st);
 }
@@ -329,10 +586,13 @@ template void launch_build_factor_input<float>(const float*, long long, const in
                                                float*, double*, cudaStream_t);
 template void launch_build_factor_input<double>(const float*, long long, const int32_t*, double,
                                                 double*, double*, cudaStream_t);
-template void factor_upper_inverse<float>(float*, long long, float*, float*, unsigned*,
-                                          cudaStream_t, cudaEvent_t);
-template void factor_upper_inverse<double>(double*, long long, double*, double*, unsigned*,
-                                           cudaStream_t, cudaEvent_t);
+template void cholesky_g<float>(float*, long long, float*, float*, float*, int*, unsigned*,
+                                long long, cudaStream_t);
+template void cholesky_g<double>(double*, long long, double*, float*, float*, int*, unsigned*,
+                                 long long, cudaStream_t);
+template void upper_from_cholesky<float>(const float*, long long, float*, float*, cudaStream_t);
+template void upper_from_cholesky<double>(const double*, long long, double*, double*,
+                                          cudaStream_t);
 template void launch_gram_upper<float>(const float*, long long, double*, cudaStream_t);
 template void launch_gram_upper<double>(const double*, long long, double*, cudaStream_t);
 

@@ -6,7 +6,7 @@
 //
 // Design (sm_100a):
 //   * Only output tiles touching the upper triangle are computed (SYRK:
-//     T*N*(N+1) flops instead of 2*T*N^2); a finalize pass mirrors them.
+//     T*N*(N+1) flops instead of 2*T*N^2); the last split mirrors them.
 //   * CTA tile 128 (i) x 256 (j) channels, one tcgen05.mma.cta_group::1
 //     kind::f16 M=128 N=256 K=16 per 16 tokens, FP32 accumulators in TMEM
 //     (2 x 256 columns: the epilogue drains one while the MMA fills the other).
@@ -16,12 +16,19 @@
 //   * Warp roles: w0 TMA producer, w1 MMA issuer (+TMEM owner), w2..w5 epilogue.
 //   * Persistent CTAs over (split-K, tile) units, split-major so all CTAs
 //     stream the same token window (X read from HBM ~once, reused via L2).
-//     Each split writes its own fp32 partial; finalize sums the splits in a
-//     fixed order (deterministic, no atomics) and mirrors to the full matrix.
+//     Splits cap each TMEM accumulation at 16384 tokens (fp32 accuracy).
+//   * The split partials are reduced inside the kernel, in split order: the
+//     epilogue of (tile, s) waits for the tile's flag to reach s (acquire),
+//     adds its accumulator into H's upper entries, and releases s+1; the last
+//     split also writes the mirrored lower entries.  Deterministic (fixed
+//     order, no data atomics) and overlapped with the MMAs of other units --
+//     no partial buffers and no separate finalize pass.
 #include <cuda.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "kernels.h"
 
@@ -63,6 +70,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "r"(bar), "r"(parity)
         : "memory");
   } while (!done);
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag_eq(const int* p, int v) {
+  while (ld_acquire(p) != v) __nanosleep(64);
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1) {
@@ -135,7 +153,8 @@ __device__ __forceinline__ void tile_coords(int tile, int nbi, int& bi, int& bj)
 
 __global__ void __launch_bounds__(THREADS, 1)
     hessian_tc_kernel(const __grid_constant__ CUtensorMap xmap, long long tokens, int dim,
-                      int nbi, int ntiles, int splits, long long kb_total, float* __restrict__ part) {
+                      int nbi, int ntiles, int splits, long long kb_total, float* __restrict__ h,
+                      int accumulate, int* __restrict__ tile_flag) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
@@ -242,10 +261,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       tile_coords(tile, nbi, bi, bj);
       const uint32_t acc = uint32_t(local & 1);
       const uint32_t use = uint32_t(local >> 1);
+      // partials of this tile are added in split order
+      if (warp == 2 && lane == 0) wait_flag_eq(tile_flag + tile, split);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
       mbar_wait(smem_u32(&tfull_bar[acc]), use & 1u);
       tc_fence_after();
       const long long row = (long long)bi * TM + q * 32 + lane;
-      float* prow = part + (long long)split * dim * dim + row * dim;
+      const bool first = split == 0 && !accumulate, last = split == splits - 1;
 #pragma unroll 1
       for (int c0 = 0; c0 < TN; c0 += 32) {
         uint32_t r[32];
@@ -262,21 +284,41 @@ __global__ void __launch_bounds__(THREADS, 1)
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const long long col0 = (long long)bj * TN + c0;
+        if (col0 + 31 < (long long)bi * TM) continue;  // chunk entirely below the diagonal
+        float v[32];
         if (row < dim) {
-          if (col0 + 32 <= dim) {
-            float4* dst = reinterpret_cast<float4*>(prow + col0);
+          float* hrow = h + row * dim + col0;
+          const bool full = col0 + 32 <= dim;
+          if (full && !first) {
 #pragma unroll
-            for (int v = 0; v < 8; ++v)
-              dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+            for (int e = 0; e < 8; ++e) {
+              const float4 o = __ldcg(reinterpret_cast<const float4*>(hrow) + e);
+              v[4 * e] = o.x, v[4 * e + 1] = o.y, v[4 * e + 2] = o.z, v[4 * e + 3] = o.w;
+            }
           } else {
 #pragma unroll
-            for (int v = 0; v < 32; ++v)
-              if (col0 + v < dim) prow[col0 + v] = __uint_as_float(r[v]);
+            for (int e = 0; e < 32; ++e) v[e] = (!first && col0 + e < dim) ? __ldcg(hrow + e) : 0.f;
+          }
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] += __uint_as_float(r[e]);
+          // upper entries (row <= col) accumulate; the lower half is the mirror
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (col0 + e < dim && col0 + e >= row) hrow[e] = v[e];
+        }
+        if (last) {
+          // mirror: H[col][row] = H[row][col] for col > row (coalesced along rows)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const long long col = col0 + e;
+            if (row < dim && col < dim && col > row) h[col * dim + row] = v[e];
           }
         }
       }
+      __threadfence();
       tc_fence_before();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 2 && lane == 0) st_release(tile_flag + tile, split + 1);
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[acc]));
     }
@@ -289,34 +331,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(TMEM_COLS)
                  : "memory");
-  }
-}
-
-// H[i][j] = (acc ? H : 0) + sum_s part[s][min(i,j)][max(i,j)], via 32x32 tiles
-__global__ void finalize_kernel(const float* __restrict__ part, int splits, int dim, float* h,
-                                int accumulate) {
-  __shared__ float t[32][33];
-  const int bi = blockIdx.y, bj = blockIdx.x;
-  if (bi > bj) return;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  const long long size = (long long)dim * dim;
-  for (int r = ty; r < 32; r += 8) {
-    const long long i = (long long)bi * 32 + r, j = (long long)bj * 32 + tx;
-    float v = 0.f;
-    if (i < dim && j < dim) {
-      const long long ui = min(i, j), uj = max(i, j);
-      double acc = accumulate ? double(h[i * dim + j]) : 0.0;
-      for (int s = 0; s < splits; ++s) acc += double(part[s * size + ui * dim + uj]);
-      v = float(acc);
-      h[i * dim + j] = v;
-    }
-    t[r][tx] = v;
-  }
-  if (bi == bj) return;
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {  // mirrored tile H[bj][bi] = tile^T
-    const long long i = (long long)bj * 32 + r, j = (long long)bi * 32 + tx;
-    if (i < dim && j < dim) h[i * dim + j] = t[tx][r];
   }
 }
 
@@ -353,7 +367,7 @@ Plan make_plan(long long tokens, long long dim, int sms) {
   // split-K factor.  Accuracy bound: the tensor core's fp32 accumulation over
   // one TMEM tile is capped at kMaxSplitTokens tokens (measured: 262144
   // tokens in one accumulator -> 1.6e-4 relative error, above the 1e-4
-  // tolerance; 16384 -> ~1e-5); partials are summed in fp64 by finalize.
+  // tolerance; 16384 -> ~1e-5); the split partials are chained in fp32 in split order.
   // Within that bound, pick the best wave efficiency.
   const long long min_splits = (p.kb_total * TK + kMaxSplitTokens - 1) / kMaxSplitTokens;
   int best = int(std::max<long long>(1, min_splits));
@@ -386,7 +400,7 @@ int num_sms() {
 
 size_t hessian_tc_workspace_bytes(long long tokens, long long dim) {
   const Plan p = make_plan(tokens, dim, num_sms());
-  return size_t(p.splits) * size_t(dim) * size_t(dim) * sizeof(float);
+  return size_t(p.ntiles) * sizeof(int) + 256;
 }
 
 // returns 0 ok, -1 unsupported shape (caller must use another kernel), >0 cuda error
@@ -398,7 +412,7 @@ int hessian_tc(const uint16_t* x, long long tokens, long long dim, float* h, int
   if (!enc) return -1;
   const int sms = num_sms();
   const Plan p = make_plan(tokens, dim, sms);
-  if (ws_bytes < size_t(p.splits) * size_t(dim) * size_t(dim) * sizeof(float)) return -2;
+  if (ws_bytes < size_t(p.ntiles) * sizeof(int)) return -2;
 
   CUtensorMap map;
   const cuuint64_t gdim[2] = {cuuint64_t(dim), cuuint64_t(tokens)};
@@ -417,14 +431,23 @@ int hessian_tc(const uint16_t* x, long long tokens, long long dim, float* h, int
                          SMEM_BYTES);
     attr_set = true;
   }
-  float* part = static_cast<float*>(ws);
+  int* tile_flag = static_cast<int*>(ws);
+  cudaMemsetAsync(tile_flag, 0, size_t(p.ntiles) * sizeof(int), st);
   const long long units = (long long)p.ntiles * p.splits;
   const int grid = int(std::min<long long>(units, sms));
+  count_launches(1);
   hessian_tc_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(map, tokens, int(dim), p.nbi, p.ntiles,
-                                                       p.splits, p.kb_total, part);
-  const int nb32 = int((dim + 31) / 32);
-  count_launches(2);
-  finalize_kernel<<<dim3(nb32, nb32), 256, 0, st>>>(part, p.splits, int(dim), h, accumulate);
+                                                       p.splits, p.kb_total, h, accumulate,
+                                                       tile_flag);
+  if (getenv("OCWG_DEBUG_HESSIAN")) {
+    cudaStreamSynchronize(st);
+    std::vector<int> f(p.ntiles);
+    cudaMemcpy(f.data(), tile_flag, f.size() * 4, cudaMemcpyDeviceToHost);
+    int mn = 1 << 30, mx = -1;
+    for (int v : f) mn = std::min(mn, v), mx = std::max(mx, v);
+    fprintf(stderr, "hessian_tc: dim %lld tok %lld grid %d ntiles %d splits %d flags [%d, %d] err %s ws %p h %p\n",
+            dim, tokens, grid, p.ntiles, p.splits, mn, mx, cudaGetErrorString(cudaGetLastError()), ws, (void*)h);
+  }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : int(e);
 }

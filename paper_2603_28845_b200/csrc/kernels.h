@@ -50,13 +50,21 @@ void launch_order(const float* h, long long n, int actorder, int32_t* order, cud
 template <typename T>
 void launch_build_factor_input(const float* h, long long n, const int32_t* order,
                                double percdamp, T* a, double* damp, cudaStream_t st);
-// In-place lower Cholesky of A (n x n, row-major, lower used), then
-// U = (J L J)^-1 written to u (n x n row-major upper, zero below).
-// Sets kFlagNotPD in *flag on breakdown.  ws: nblk*64*64 + n*n elements.
-// mid (optional): event recorded between the Cholesky and the inverse.
+// In-place lower Cholesky A = L L^T (n x n row-major, lower used) by the
+// persistent tile-dataflow kernel, over macro panels of `macro_cols` columns
+// (<= 0: one panel) with a trailing SYRK (mm<T>) between panels.  Emits
+// G[k][i] = L[n-1-i][n-1-k] / L[n-1-k][n-1-k] (i < k) for the sweep into ghi
+// (+ glo: tf32 hi/lo split when non-null, T = float, with the plain value in
+// gpl).  flags: ints from cholesky_flag_ints(n).  Sets kFlagNotPD in *status
+// on breakdown.
+size_t cholesky_flag_ints(long long n);
 template <typename T>
-void factor_upper_inverse(T* a, long long n, T* u, T* ws, unsigned* flag, cudaStream_t st,
-                          cudaEvent_t mid = nullptr);
+void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, int* flags, unsigned* status,
+                long long macro_cols, cudaStream_t st);
+// U = (J L J)^-1 (n x n upper, processing order) from the Cholesky factor:
+// parity artefacts only.  ws: ceil(n/64)*64*64 + n*n elements.
+template <typename T>
+void upper_from_cholesky(const T* a, long long n, T* u, T* ws, cudaStream_t st);
 // hinv = U^T U in fp64 (parity artefact: (H_p + damp I)^-1 in processing order)
 template <typename T>
 void launch_gram_upper(const T* u, long long n, double* hinv, cudaStream_t st);
@@ -81,6 +89,12 @@ bool tc_gemm_tf32x3(int batch, long long m, long long n, long long k, float alph
 // Workspace for the fp32 GEMMs of the factorisation / sweep (set by the C ABI
 // per call).  With a workspace set, fp32 GEMMs run on the tensor cores.
 void set_tc_workspace(float* ws, size_t floats);
+// Pre-split K-major operands: C = beta C + alpha (a_hi+a_lo)(b_hi+b_lo)^T, A m x k,
+// B n x k.  Returns false when the shape/alignment needs another path.
+bool tc_gemm_presplit(long long m, long long n, long long k, float alpha, const float* a_hi,
+                      const float* a_lo, long long lda, const float* b_hi, const float* b_lo,
+                      long long ldb, float beta, float* c, long long ldc, cudaStream_t st,
+                      int max_ctas = 0);
 // Dispatch: T = float -> tcgen05 3xTF32 (when a workspace is set and the
 // problem is big enough to fill tiles), else SIMT.
 template <typename T>
@@ -90,16 +104,20 @@ void mm(long long m, long long n, long long k, double alpha, const T* a, long lo
 
 // ---- GPTQ sweep (sweep.cu) ---------------------------------------------
 constexpr long long kMaxSweepBlock = 128;
-// w has row stride ldw; wp is contiguous n x m (rows in processing order)
+// D buffer elements per block parity (m x 128, K-major)
+size_t sweep_delta_elems(long long m);
+// Closed-form sweep over G (factor.cu).  w: original W (row stride ldw);
+// gpl: plain G (in-block staging), ghi/glo: the GEMM operand (glo null =
+// plain, SIMT GEMM); codes / w_hat written with row stride ldo in original row
+// order; acc: n x m scratch; dpl/dhi/dlo: two D buffers each (plain; tf32
+// hi/lo when glo != null); aux: second stream for the trailing GEMMs;
+// ev: 5 events (fork, in-block, trailing x2, join).
 template <typename T>
-void launch_permute_rows(const float* w, long long n, long long m, long long ldw,
-                         const int32_t* order, T* wp, cudaStream_t st);
-// codes / w_hat are written with row stride ldo (original row order);
-// err_ws: kMaxSweepBlock * m elements
-template <typename T>
-void gptq_sweep(T* wp, long long n, long long m, const T* u, const int32_t* order, const QCfg& c,
-                const float* scales, const int32_t* zeros, long long block, int16_t* codes,
-                float* w_hat, long long ldo, T* err_ws, cudaStream_t st);
+void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const T* gpl,
+                  const T* ghi, const float* glo, const int32_t* order, const QCfg& c,
+                  const float* scales, const int32_t* zeros, long long block, int16_t* codes,
+                  float* w_hat, long long ldo, T* acc, T* const dpl[2], float* const dhi[2],
+                  float* const dlo[2], cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev);
 
 // ---- statistics (stats.cu, hessian_tc.cu) -------------------------------
 // fp64 accumulate_stats for fp32 inputs (stats.cpp:10-19): gram += Xp^T Xp,

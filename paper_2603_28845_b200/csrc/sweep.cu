@@ -2,207 +2,314 @@
 // compute type T (float default, double = the reference's arithmetic class).
 //
 // Reference orientation: W is n x m, rows = input indices processed in
-// `order`, columns = output channels, mutually independent.  Per block of B
-// rows [ib, ie):
-//   in-block (this file): for i in block, for every column j:
-//       code = q(float(wp[i,j]), grid[orig_i, j]);  err = (wp[i,j] - w_hat)/U[i,i]
-//       wp[k,j] -= U[i,k]*err  for k in (i, ie)             (layerwise.cpp:68-83)
-//   trailing (gemm.cu): wp[ie:, :] -= U[ib:ie, ie:]^T * E   (layerwise.cpp:85-90)
+// `order`, columns = output channels, mutually independent.  The reference
+// updates the working copy row by row,
+//   err = (wp[i] - w_hat[i]) / U[i,i];  wp[k] -= U[i,k] * err   (k > i)
+// which is, in closed form (factor.cu),
+//   w_cur[k] = w[k] + sum_{i<k} G[k,i] * D[i],   D[i] = w[i] - w_hat[i],
+// with G the unit-lower factor emitted by the Cholesky and w the ORIGINAL
+// (permuted) row.  Per block of B rows [ib, ie):
+//   in-block (inblock_g_kernel): for i in block: w_cur = w + acc; quantize;
+//       D = w - w_hat; acc[k] += G[k,i] D  for the block's later rows k;
+//   trailing: acc[ie + B':, :] += G[ie + B':, blk] * D[blk, :]  (tcgen05 3xTF32).
+// Lookahead: the trailing update of block b skips block b+1's rows; block
+// b+1's in-block kernel applies that slice itself (G[blk b+1, blk b] D_b)
+// from shared memory.  In-block kernels run back to back on the calling
+// stream while the trailing GEMMs run on an auxiliary stream:
+//   inblock(b+1) needs inblock(b) (same stream) and trailing(b-1) (event);
+//   trailing(b)  needs inblock(b) (event).
+// acc needs no initialisation: trailing(0) writes it with beta = 0 and
+// blocks 0 and 1 never read it.
 //
 // In-block mapping: a CTA owns 32 columns (8 warps x 4); lane = cc + 4*rg
-// keeps rows rg, rg+8, ... of its column in registers.  The row loop is
-// fully unrolled (row li = 8t + o), so the owner lane's register index is a
-// compile-time constant; the error is broadcast with one warp shuffle.  The
-// U block, the processing->original row map and the block's grids are staged
-// in shared memory once per block, off the sequential critical path.
+// keeps rows rg, rg+8, ... of its column in registers (with the column's
+// original weights, scales and zero points for those rows).  The 8-row group
+// body is unrolled and the register arrays rotate by one slot per group, so
+// every register index is a compile-time constant; D is broadcast with one
+// warp shuffle.  The block's strictly-lower G is staged packed in shared
+// memory; D is staged for a coalesced K-major store (the GEMM's B operand).
 #include "kernels.h"
 
 namespace ocwg {
 namespace {
 
-constexpr int kCols = 32;  // columns per CTA
+constexpr int kCols = 32;      // columns per CTA
+constexpr int kB = 128;        // max rows per block (D stride)
+constexpr int kLaChunk = 64;   // lookahead staging chunk (columns of G)
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t u = __float_as_uint(x);
+  u = (u + 0xFFFu + ((u >> 13) & 1u)) & ~0x1FFFu;
+  return __uint_as_float(u);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// asynchronous 4/8-byte global -> shared copy (LDGSTS): staging loops keep
+// every load in flight instead of round-tripping through registers
+template <typename T>
+__device__ __forceinline__ void cp_async(T* dst, const T* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "n"(int(sizeof(T)))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
 
 template <typename T>
-__global__ void permute_rows_kernel(const float* __restrict__ w, long long n, long long m,
-                                    long long ldw, const int32_t* __restrict__ order, T* wp) {
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n * m;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long i = e / m, j = e % m;
-    wp[e] = T(w[(long long)order[i] * ldw + j]);
+__device__ __forceinline__ void ld4(const T* p, T (&o)[4]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    o[0] = f.x, o[1] = f.y, o[2] = f.z, o[3] = f.w;
+  } else {
+    const double2 f0 = *reinterpret_cast<const double2*>(p);
+    const double2 f1 = *reinterpret_cast<const double2*>(p + 2);
+    o[0] = f0.x, o[1] = f0.y, o[2] = f1.x, o[3] = f1.y;
   }
 }
 
-template <typename T>
-__device__ __forceinline__ T err_of(T wv, float wh, T d);
-template <>
-__device__ __forceinline__ float err_of<float>(float wv, float wh, float d) {
-  return __fdiv_rn(__fsub_rn(wv, wh), d);
-}
-template <>
-__device__ __forceinline__ double err_of<double>(double wv, float wh, double d) {
-  return __ddiv_rn(__dsub_rn(wv, double(wh)), d);  // (wp - double(w_hat)) / d  (:76-77)
-}
+__host__ __device__ constexpr int packed_off(int li) { return li * kB - li * (li + 1) / 2; }
 
 template <typename T>
-__device__ __forceinline__ T upd(T r, T u, T e);
-template <>
-__device__ __forceinline__ float upd<float>(float r, float u, float e) {
-  return fmaf(-u, e, r);
-}
-template <>
-__device__ __forceinline__ double upd<double>(double r, double u, double e) {
-  return __dsub_rn(r, __dmul_rn(u, e));  // two roundings, like the reference (:79-83)
-}
+struct InblockSmem {
+  union {
+    T gs[packed_off(kB)];  // strictly-lower G block, column-packed: (k, li) at off(li)+k-li-1
+    struct {
+      T gc[kB][kLaChunk + 4];     // lookahead: G[ib + li][kprev + q0 + q]
+      T dp[kCols][kLaChunk + 4];  // lookahead: D_prev[q0 + q] of column cj
+    } la;
+  } u;
+  T ds[kCols][kB + 1];  // D of this block, staged for the K-major store
+  int og[kB];           // processing -> original row of the block
+};
 
 template <typename T, int RPT>
-__global__ void __launch_bounds__(256) inblock_kernel(
-    T* __restrict__ wp, long long n, long long m, const T* __restrict__ u,
-    const int32_t* __restrict__ order, QCfg c, const float* __restrict__ scales,
-    const int32_t* __restrict__ zeros, long long ib, int bsz, int16_t* __restrict__ codes,
-    float* __restrict__ w_hat, long long ldo, T* __restrict__ err_out) {
-  constexpr int B = 8 * RPT;
-  extern __shared__ __align__(16) unsigned char smem[];
-  T* us = reinterpret_cast<T*>(smem);                                   // B x (B+1)
-  float* gs = reinterpret_cast<float*>(smem + sizeof(T) * B * (B + 1));  // B x kCols
-  int* gz = reinterpret_cast<int*>(gs + B * kCols);                     // B x kCols
-  int* og = gz + B * kCols;                                             // B
-
-  const int tid = threadIdx.x;
-  const long long j0 = (long long)blockIdx.x * kCols;
-  for (int e = tid; e < B; e += 256) og[e] = e < bsz ? order[ib + e] : 0;
-  for (int e = tid; e < B * B; e += 256) {
-    const int li = e / B, lk = e % B;
-    us[li * (B + 1) + lk] = (li < bsz && lk < bsz) ? u[(ib + li) * n + ib + lk] : T(0);
-  }
-  __syncthreads();
-  for (int e = tid; e < B * kCols; e += 256) {
-    const int li = e / kCols, cj = e % kCols;
-    const long long jj = j0 + cj;
-    float s = 1.0f;
-    int z = 0;
-    if (li < bsz && jj < m) {
-      const long long g = group_of(c, og[li], jj);
-      s = scales[g];
-      z = zeros[g];
-    }
-    gs[e] = s;
-    gz[e] = z;
-  }
-  __syncthreads();
-
-  const int lane = tid & 31, warp = tid >> 5;
+__global__ void __launch_bounds__(256) inblock_g_kernel(
+    const float* __restrict__ w, long long ldw, const int32_t* __restrict__ order,
+    const T* __restrict__ acc, int use_acc, const T* __restrict__ gpl,
+    const T* __restrict__ dprev, int bprev, T* __restrict__ dcur, float* __restrict__ dcur_hi,
+    float* __restrict__ dcur_lo, QCfg c, const float* __restrict__ scales,
+    const int32_t* __restrict__ zeros, long long n, long long m, long long ib, int bsz,
+    int16_t* __restrict__ codes, float* __restrict__ w_hat, long long ldo) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  InblockSmem<T>& sm = *reinterpret_cast<InblockSmem<T>*>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cc = lane & 3, rg = lane >> 2;
   const int cj = warp * 4 + cc;
+  const long long j0 = (long long)blockIdx.x * kCols;
   const long long j = j0 + cj;
   const bool col_ok = j < m;
+
+  for (int e = tid; e < kB; e += 256) sm.og[e] = e < bsz ? order[ib + e] : 0;
+  __syncthreads();
+  // ---- per-lane rows rg + 8t: current partial sums, original weights, grids
   T r[RPT];
+  float w0[RPT], s[RPT];
+  int z[RPT];
 #pragma unroll
   for (int t = 0; t < RPT; ++t) {
     const int li = rg + 8 * t;
-    r[t] = (col_ok && li < bsz) ? wp[(ib + li) * m + j] : T(0);
+    r[t] = T(0);
+    w0[t] = 0.f;
+    s[t] = 1.f;
+    z[t] = 0;
+    if (col_ok && li < bsz) {
+      const long long orig = sm.og[li];
+      w0[t] = w[orig * ldw + j];
+      const long long g = group_of(c, orig, j);
+      s[t] = scales[g];
+      z[t] = zeros[g];
+      if (use_acc) r[t] = acc[(ib + li) * m + j];
+    }
   }
-  // Rows li = 8t + o.  r[] is rotated down by one slot after every group of
-  // 8 rows, so the owner's value is always r[0] and every register index is
-  // a compile-time constant while only the 8-row group body is unrolled
-  // (keeps the kernel inside the instruction cache).
+
+  // ---- lookahead: r += G[blk, prev blk] * D_prev  (the slice trailing(b-1) skipped)
+  if (bprev > 0) {
+    const long long kprev = ib - bprev;
+    for (int q0 = 0; q0 < bprev; q0 += kLaChunk) {
+      for (int e = tid; e < kB * kLaChunk; e += 256) {
+        const int li = e / kLaChunk, q = e % kLaChunk;
+        if (li < bsz && q0 + q < bprev)
+          cp_async(&sm.u.la.gc[li][q], gpl + (ib + li) * n + kprev + q0 + q);
+        else
+          sm.u.la.gc[li][q] = T(0);
+      }
+      for (int e = tid; e < kCols * kLaChunk; e += 256) {
+        const int cl = e / kLaChunk, q = e % kLaChunk;
+        if (j0 + cl < m && q0 + q < bprev)
+          cp_async(&sm.u.la.dp[cl][q], dprev + (j0 + cl) * kB + q0 + q);
+        else
+          sm.u.la.dp[cl][q] = T(0);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+#pragma unroll 2
+      for (int q = 0; q < kLaChunk; q += 4) {
+        T dv[4];
+        ld4(&sm.u.la.dp[cj][q], dv);
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) {
+          T g[4];
+          ld4(&sm.u.la.gc[rg + 8 * t][q], g);
+          r[t] = fma(g[0], dv[0], r[t]);
+          r[t] = fma(g[1], dv[1], r[t]);
+          r[t] = fma(g[2], dv[2], r[t]);
+          r[t] = fma(g[3], dv[3], r[t]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- stage the block's strictly-lower G (packed by column)
+  for (int k = 1 + warp; k < bsz; k += 8)
+    for (int li = lane; li < k; li += 32)
+      cp_async(&sm.u.gs[packed_off(li) + k - li - 1], gpl + (ib + k) * n + ib + li);
+  cp_async_wait_all();
+  __syncthreads();
+
+  // ---- sequential rows li = 8t + o; owner lane rg == o holds the row in slot 0
 #pragma unroll 1
   for (int t = 0; t < RPT; ++t) {
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
       const int li = 8 * t + o;
       if (li >= bsz) break;
-      T e = T(0);
+      T d = T(0);
       if (rg == o) {
-        const float s = gs[li * kCols + cj];
-        const int z = gz[li * kCols + cj];
-        const int q = quantize_code(float(r[0]), s, z, c.qmin, c.qmax);  // row_f (:70)
-        const float wh = dequantize_code(q, s, z);
-        e = err_of<T>(r[0], wh, us[li * (B + 1) + li]);
+        const T cur = T(w0[0]) + r[0];  // w_cur = w + sum G D
+        const int q = quantize_code(float(cur), s[0], z[0], c.qmin, c.qmax);  // row_f (:70)
+        const float wh = dequantize_code(q, s[0], z[0]);
+        d = T(w0[0]) - T(wh);
         if (col_ok) {
-          const long long orig = og[li];
+          const long long orig = sm.og[li];
           codes[orig * ldo + j] = int16_t(q);  // original row order (:75)
           if (w_hat) w_hat[orig * ldo + j] = wh;
-          err_out[(long long)li * m + j] = e;
         }
+        sm.ds[cj][li] = d;
       }
-      e = __shfl_sync(0xffffffffu, e, cc + 4 * o);
-      const T* urow = us + li * (B + 1) + rg + 8 * t;
+      d = __shfl_sync(0xffffffffu, d, cc + 4 * o);
+      const T* gcol = sm.u.gs + packed_off(li) - li - 1;  // gcol[k] = G[k][li]
 #pragma unroll
-      for (int k = 0; k < RPT; ++k) {
-        if ((k > 0 || rg > o) && t + k < RPT) r[k] = upd<T>(r[k], urow[8 * k], e);
+      for (int kk = 0; kk < RPT; ++kk) {
+        const int row = rg + 8 * (t + kk);
+        if ((kk > 0 || rg > o) && t + kk < RPT && row < bsz) r[kk] = fma(gcol[row], d, r[kk]);
       }
     }
 #pragma unroll
-    for (int k = 0; k + 1 < RPT; ++k) r[k] = r[k + 1];
+    for (int k = 0; k + 1 < RPT; ++k) {
+      r[k] = r[k + 1];
+      w0[k] = w0[k + 1];
+      s[k] = s[k + 1];
+      z[k] = z[k + 1];
+    }
+  }
+  __syncthreads();
+  // ---- D (K-major: column j's kB values contiguous): plain, and the tf32
+  // hi/lo split the tensor-core GEMM consumes
+  for (int e = tid; e < kCols * kB; e += 256) {
+    const int cl = e / kB, li = e % kB;
+    if (j0 + cl >= m) continue;
+    const T v = li < bsz ? sm.ds[cl][li] : T(0);
+    const long long off = (j0 + cl) * kB + li;
+    dcur[off] = v;
+    if (dcur_hi) {
+      const float hi = tf32_hi(float(v));
+      dcur_hi[off] = hi;
+      dcur_lo[off] = float(v) - hi;
+    }
   }
 }
 
 template <typename T, int RPT>
-constexpr int inblock_smem() {
-  return int(sizeof(T)) * 8 * RPT * (8 * RPT + 1) + 8 * RPT * kCols * 8 + 8 * RPT * 4;
-}
-
-template <typename T, int RPT>
-void launch_inblock(T* wp, long long n, long long m, const T* u, const int32_t* order,
-                    const QCfg& c, const float* scales, const int32_t* zeros, long long ib, int bsz,
-                    int16_t* codes, float* w_hat, long long ldo, T* err, cudaStream_t st) {
+void launch_inblock(const float* w, long long ldw, const int32_t* order, const T* acc, int use_acc,
+                    const T* gpl, const T* dprev, int bprev, T* dcur, float* dch, float* dcl,
+                    const QCfg& c, const float* scales, const int32_t* zeros, long long n,
+                    long long m, long long ib, int bsz, int16_t* codes, float* w_hat, long long ldo,
+                    cudaStream_t st) {
   static const bool attr = [] {
-    cudaFuncSetAttribute(inblock_kernel<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         inblock_smem<T, RPT>());
+    cudaFuncSetAttribute(inblock_g_kernel<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(InblockSmem<T>)));
     return true;
   }();
   (void)attr;
   const unsigned ctas = unsigned((m + kCols - 1) / kCols);
   count_launches(1);
-  inblock_kernel<T, RPT><<<ctas, 256, inblock_smem<T, RPT>(), st>>>(
-      wp, n, m, u, order, c, scales, zeros, ib, bsz, codes, w_hat, ldo, err);
+  inblock_g_kernel<T, RPT><<<ctas, 256, sizeof(InblockSmem<T>), st>>>(
+      w, ldw, order, acc, use_acc, gpl, dprev, bprev, dcur, dch, dcl, c, scales, zeros, n, m, ib,
+      bsz, codes, w_hat, ldo);
 }
 
 }  // namespace
 
-template <typename T>
-void launch_permute_rows(const float* w, long long n, long long m, long long ldw,
-                         const int32_t* order, T* wp, cudaStream_t st) {
-  long long g = (n * m + 255) / 256;
-  if (g > 148 * 32) g = 148 * 32;
-  count_launches(1);
-  permute_rows_kernel<T><<<int(g < 1 ? 1 : g), 256, 0, st>>>(w, n, m, ldw, order, wp);
-}
+size_t sweep_delta_elems(long long m) { return size_t(m) * kB; }
 
 template <typename T>
-void gptq_sweep(T* wp, long long n, long long m, const T* u, const int32_t* order, const QCfg& c,
-                const float* scales, const int32_t* zeros, long long block, int16_t* codes,
-                float* w_hat, long long ldo, T* err_ws, cudaStream_t st) {
+void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const T* gpl,
+                  const T* ghi, const float* glo, const int32_t* order, const QCfg& c,
+                  const float* scales, const int32_t* zeros, long long block, int16_t* codes,
+                  float* w_hat, long long ldo, T* acc, T* const dpl[2], float* const dhi[2],
+                  float* const dlo[2], cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev) {
   // block size is a pure re-association of the trailing update (SURVEY §0
   // item 11); blocks above 128 rows run as 128-row blocks.
-  const long long B = block < 1 ? 1 : (block > kMaxSweepBlock ? kMaxSweepBlock : block);
-  for (long long ib = 0; ib < n; ib += B) {
-    const long long ie = std::min(n, ib + B);
+  const long long B = block < 1 ? 1 : (block > kB ? kB : block);
+  const long long nb = (n + B - 1) / B;
+  const bool split = glo != nullptr;
+  // ev: [0] fork, [1] in-block done, [2..3] trailing done (by block parity), [4] join
+  cudaEventRecord(ev[0], st);
+  cudaStreamWaitEvent(aux, ev[0], 0);
+  for (long long b = 0; b < nb; ++b) {
+    const long long ib = b * B, ie = std::min(n, ib + B);
     const int bsz = int(ie - ib);
+    const int p = int(b & 1);
+    if (b >= 2) cudaStreamWaitEvent(st, ev[2 + p], 0);  // trailing(b-2) done
+    const int bprev = b > 0 ? int(B) : 0;
+    const T* dprev = b > 0 ? dpl[p ^ 1] : nullptr;
+    float* dch = split ? dhi[p] : nullptr;
+    float* dcl = split ? dlo[p] : nullptr;
     if (B <= 32)
-      launch_inblock<T, 4>(wp, n, m, u, order, c, scales, zeros, ib, bsz, codes, w_hat, ldo, err_ws,
-                           st);
+      launch_inblock<T, 4>(w, ldw, order, acc, b >= 2, gpl, dprev, bprev, dpl[p], dch, dcl, c,
+                           scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, st);
     else if (B <= 64)
-      launch_inblock<T, 8>(wp, n, m, u, order, c, scales, zeros, ib, bsz, codes, w_hat, ldo, err_ws,
-                           st);
+      launch_inblock<T, 8>(w, ldw, order, acc, b >= 2, gpl, dprev, bprev, dpl[p], dch, dcl, c,
+                           scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, st);
     else
-      launch_inblock<T, 16>(wp, n, m, u, order, c, scales, zeros, ib, bsz, codes, w_hat, ldo,
-                            err_ws, st);
-    if (ie < n)
-      mm<T>(n - ie, m, bsz, -1.0, u + ib * n + ie, n, true, err_ws, m, false, 1.0,
-                    wp + ie * m, m, false, st);
+      launch_inblock<T, 16>(w, ldw, order, acc, b >= 2, gpl, dprev, bprev, dpl[p], dch, dcl, c,
+                            scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, st);
+    // trailing(b): rows [ie + next, n) -- block b+1 takes its slice by lookahead
+    const long long r0 = std::min(n, ie + B);
+    if (r0 < n) {
+      cudaEventRecord(ev[1], st);
+      cudaStreamWaitEvent(aux, ev[1], 0);
+      const double beta = b == 0 ? 0.0 : 1.0;
+      bool done = false;
+      if constexpr (sizeof(T) == 4) {
+        if (split)
+          done = tc_gemm_presplit(n - r0, m, bsz, 1.0f, reinterpret_cast<const float*>(ghi) + r0 * n + ib,
+                                  glo + r0 * n + ib, n, dhi[p], dlo[p], kB, float(beta),
+                                  reinterpret_cast<float*>(acc) + r0 * m, m, aux);
+      }
+      if (!done)
+        gemm<T, T, T>(n - r0, m, bsz, 1.0, gpl + r0 * n + ib, n, false, dpl[p], kB, true, beta,
+                      acc + r0 * m, m, false, aux);
+      cudaEventRecord(ev[2 + p], aux);
+    }
   }
+  cudaEventRecord(ev[4], aux);
+  cudaStreamWaitEvent(st, ev[4], 0);
 }
 
-template void launch_permute_rows<float>(const float*, long long, long long, long long,
-                                         const int32_t*, float*, cudaStream_t);
-template void launch_permute_rows<double>(const float*, long long, long long, long long,
-                                          const int32_t*, double*, cudaStream_t);
-template void gptq_sweep<float>(float*, long long, long long, const float*, const int32_t*,
-                                const QCfg&, const float*, const int32_t*, long long, int16_t*,
-                                float*, long long, float*, cudaStream_t);
-template void gptq_sweep<double>(double*, long long, long long, const double*, const int32_t*,
-                                 const QCfg&, const float*, const int32_t*, long long, int16_t*,
-                                 float*, long long, double*, cudaStream_t);
+template void gptq_sweep_g<float>(const float*, long long, long long, long long, const float*,
+                                  const float*, const float*, const int32_t*, const QCfg&,
+                                  const float*, const int32_t*, long long, int16_t*, float*,
+                                  long long, float*, float* const[2], float* const[2],
+                                  float* const[2], cudaStream_t, cudaStream_t, cudaEvent_t*);
+template void gptq_sweep_g<double>(const float*, long long, long long, long long, const double*,
+                                   const double*, const float*, const int32_t*, const QCfg&,
+                                   const float*, const int32_t*, long long, int16_t*, float*,
+                                   long long, double*, double* const[2], float* const[2],
+                                   float* const[2], cudaStream_t, cudaStream_t, cudaEvent_t*);
 
 }  // namespace ocwg

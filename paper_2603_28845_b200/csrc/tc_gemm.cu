@@ -375,6 +375,14 @@ int num_sms_tc() {
 
 inline long long pad4(long long x) { return (x + 3) & ~3LL; }
 
+void ensure_attr() {
+  static const bool attr = [] {
+    cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    return true;
+  }();
+  (void)attr;
+}
+
 }  // namespace
 
 size_t tc_gemm_workspace_floats(long long m, long long n, long long k, int batch) {
@@ -392,11 +400,7 @@ bool tc_gemm_tf32x3(int batch, long long m, long long n, long long k, float alph
   if (!encoder() || k <= 0) return false;
   if (ws_floats < tc_gemm_workspace_floats(m, n, k, batch)) return false;
   if ((long long)batch * std::max(m, n) >= (1LL << 31)) return false;
-  static const bool attr = [] {
-    cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    return true;
-  }();
-  (void)attr;
+  ensure_attr();
   const long long ldk = pad4(k);
   float* a_hi = ws;
   float* a_lo = a_hi + batch * m * ldk;
@@ -417,6 +421,34 @@ bool tc_gemm_tf32x3(int batch, long long m, long long n, long long k, float alph
   tc_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(mah, mal, mbh, mbl, 0, 0, m, n, k, alpha, beta,
                                                     c, ldc, sc, lower_only ? 1 : 0, tiles_m,
                                                     tiles_n, ntiles);
+  return cudaGetLastError() == cudaSuccess;
+}
+
+// Operands already split and K-major: A = (a_hi + a_lo) is m x k (row stride
+// lda), B = (b_hi + b_lo) is n x k (row stride ldb); C = beta C + alpha A B^T.
+// Used by the GPTQ sweep, whose G and D are emitted pre-split by the Cholesky
+// and in-block kernels (no split launches on the sweep's critical path).
+bool tc_gemm_presplit(long long m, long long n, long long k, float alpha, const float* a_hi,
+                      const float* a_lo, long long lda, const float* b_hi, const float* b_lo,
+                      long long ldb, float beta, float* c, long long ldc, cudaStream_t st,
+                      int max_ctas) {
+  if (m <= 0 || n <= 0) return true;
+  if (!encoder() || k <= 0 || m >= (1LL << 31) || n >= (1LL << 31)) return false;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if ((lda & 3) || (ldb & 3) || !al16(a_hi) || !al16(a_lo) || !al16(b_hi) || !al16(b_lo))
+    return false;
+  ensure_attr();
+  CUtensorMap mah, mal, mbh, mbl;
+  if (!make_map(&mah, a_hi, m, k, lda, TM) || !make_map(&mal, a_lo, m, k, lda, TM) ||
+      !make_map(&mbh, b_hi, n, k, ldb, TN) || !make_map(&mbl, b_lo, n, k, ldb, TN))
+    return false;
+  const int tiles_m = int((m + TM - 1) / TM), tiles_n = int((n + TN - 1) / TN);
+  const int ntiles = tiles_m * tiles_n;
+  const int cap = max_ctas > 0 ? std::min(max_ctas, num_sms_tc()) : num_sms_tc();
+  const int grid = std::min(ntiles, cap);
+  count_launches(1);
+  tc_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(mah, mal, mbh, mbl, 0, 0, m, n, k, alpha, beta,
+                                                    c, ldc, 0, 0, tiles_m, tiles_n, ntiles);
   return cudaGetLastError() == cudaSuccess;
 }
 

@@ -13,9 +13,20 @@ from . import (GptqOptions, QuantConfig, ScaleMode, _check, context, lib, quant_
 
 
 def _bind_stream(device: int):
+    """Run on torch's current stream (handle 0 = the legacy default stream)."""
     ctx = context(device)
     _check(lib().ocwg_set_stream(ctx.handle, C.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
     return ctx
+
+
+def set_async(on: bool, device: int = 0) -> None:
+    """Device calls return once enqueued; errors surface at synchronize()."""
+    _check(lib().ocwg_set_async(context(device).handle, int(on)))
+
+
+def synchronize(device: int = 0) -> None:
+    """Drain the context's stream and raise any latched device-side error."""
+    _check(lib().ocwg_synchronize(context(device).handle))
 
 
 class LayerBuffers:
