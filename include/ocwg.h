@@ -151,8 +151,14 @@ int ocwg_gptq_quantize(ocwg_ctx* ctx, const float* w, const float* h, uint64_t n
  * output may be NULL; hinv/u are N x N fp64 row-major, processing order). */
 int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, double percdamp,
                      int64_t* order, double* hinv, double* u, double* damp);
+/* qep_target (layerwise.cpp:95-112): out = W + alpha (gram + lambda I)^-1 (cross W),
+ * lambda = eta * mean(diag(gram)); fp64 like the reference.  gram / cross:
+ * N x N fp64 (CalibStats), W / out: N x M fp32 (out may alias W). */
+int ocwg_qep_target(ocwg_ctx* ctx, const float* w, const double* gram, const double* cross,
+                    uint64_t n, uint64_t m, double alpha, double eta, float* out);
 /* quantize_layer (layerwise.cpp:120-126) over fp64 stats (gram N x N);
- * method: 0 rtn, 1 gptq.  QEP (qep != 0) is reserved: OCWG_UNSUPPORTED. */
+ * method: 0 rtn, 1 gptq.  qep must be 0 here: the QEP-corrected target comes
+ * from ocwg_qep_target first (as quantize_layer does, layerwise.cpp:121). */
 int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, uint64_t n, uint64_t m,
                         int method, const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
                         int scale_mode, int qep, int16_t* codes, float* scales, int32_t* zeros,

@@ -174,6 +174,16 @@ def accumulate_stats(gram, cross, x_fp, x_pert, token_count=0, timing=False):
     return (int(tc.value), sec.value) if timing else int(tc.value)
 
 
+def qep_target(w, gram, cross, alpha=1.0, eta=0.01):
+    """layerwise.cpp:95-112 (the reference's own qep_target)."""
+    w = _f32(w)
+    out = np.empty_like(w)
+    _ck(lib().ocwref_qep_target(_p(w), _p(np.ascontiguousarray(gram, np.float64)),
+                                _p(np.ascontiguousarray(cross, np.float64)), w.shape[0], w.shape[1],
+                                float(alpha), float(eta), _p(out)))
+    return out
+
+
 def quantize_layer(w, gram, cross, method_gptq, bits, scheme, gran, group, mse=False,
                    actorder=False, percdamp=0.01, block=32, qep=None):
     w = _f32(w)

@@ -33,7 +33,7 @@ import numpy as np
 
 __all__ = [
     "Scheme", "Granularity", "ScaleMode", "QuantConfig", "GptqOptions", "QuantizedMatrix",
-    "CalibStats", "LayerQuantOptions", "InvalidInput", "NumericError", "IoError", "CudaError",
+    "CalibStats", "LayerQuantOptions", "QepOptions", "qep_target", "base_method_from_name", "InvalidInput", "NumericError", "IoError", "CudaError",
     "calibrate_grids", "quantize_matrix", "dequantize", "activation_objective",
     "accumulate_stats", "hessian_bf16", "gptq_order", "gptq_quantize", "gptq_factor",
     "quantize_layer", "quantize_layer_x", "pack_uniform", "unpack_uniform",
@@ -151,8 +151,15 @@ class CalibStats:
 
 
 @dataclass
+class QepOptions:
+    """layerwise.hpp:28-31: propagation strength alpha in [0,1]; lambda = eta * mean(diag(gram))."""
+    alpha: float = 1.0
+    eta: float = 0.01
+
+
+@dataclass
 class LayerQuantOptions:
-    """layerwise.hpp:41-47 (QEP: next row, not built)."""
+    """layerwise.hpp:41-47; qep: QepOptions or None (enabled when set)."""
     method: str = "gptq"
     config: QuantConfig = field(default_factory=QuantConfig)
     scale_mode: ScaleMode = ScaleMode.minmax
@@ -182,6 +189,7 @@ _SIGS = {
     "ocwg_set_precision": (C.c_int, [_P, C.c_int]),
     "ocwg_synchronize": (C.c_int, [_P]),
     "ocwg_set_async": (C.c_int, [_P, C.c_int]),
+    "ocwg_qep_target": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.c_double, C.c_double, _P]),
     "ocwg_validate_config": (C.c_int, [C.POINTER(_QCfg)]),
     "ocwg_group_count": (_U64, [C.POINTER(_QCfg), _U64, _U64]),
     "ocwg_storage_bytes": (_U64, [C.POINTER(_QCfg), _U64, _U64]),
@@ -453,15 +461,34 @@ def gptq_factor(h, actorder: bool, percdamp: float, device: int = 0):
     return order, hinv, u, float(damp.value)
 
 
+def qep_target(w, stats: CalibStats, opts: QepOptions, device: int = 0) -> np.ndarray:
+    """layerwise.cpp:95-112: W + alpha (gram + lambda I)^-1 (cross W), fp64 on the GPU."""
+    w = _f32(w)
+    if stats.dim() != w.shape[0]:
+        raise InvalidInput("qep_target: stats dimension does not match W rows")
+    gram = np.ascontiguousarray(stats.gram, np.float64)
+    cross = np.ascontiguousarray(stats.cross, np.float64)
+    out = np.empty_like(w)
+    _check(lib().ocwg_qep_target(context(device).handle, _ptr(w), _ptr(gram), _ptr(cross),
+                                 w.shape[0], w.shape[1], float(opts.alpha), float(opts.eta),
+                                 _ptr(out)))
+    return out
+
+
+def base_method_from_name(name: str) -> str:
+    """layerwise.cpp:114-118."""
+    if name in ("rtn", "gptq"):
+        return name
+    raise InvalidInput(f"unknown quantization method: {name}")
+
+
 def quantize_layer(w, stats: CalibStats, opts: LayerQuantOptions, device: int = 0) -> QuantizedMatrix:
-    """layerwise.cpp:120-126."""
-    if opts.qep is not None:
-        raise Unsupported("quantize_layer: QEP target correction not built yet")
-    if opts.method == "rtn":
-        return quantize_matrix(w, opts.config, opts.scale_mode, device)
-    if opts.method != "gptq":
-        raise InvalidInput(f"unknown quantization method: {opts.method}")
-    return gptq_quantize(w, stats.gram_matrix(), opts.config, opts.gptq, opts.scale_mode,
+    """layerwise.cpp:120-126: [qep_target] -> RTN or GPTQ on stats.gram_matrix()."""
+    target = qep_target(w, stats, opts.qep, device) if opts.qep is not None else _f32(w)
+    method = base_method_from_name(opts.method)
+    if method == "rtn":
+        return quantize_matrix(target, opts.config, opts.scale_mode, device)
+    return gptq_quantize(target, stats.gram_matrix(), opts.config, opts.gptq, opts.scale_mode,
                          device=device)
 
 

@@ -192,6 +192,7 @@ struct GptqBufs {
   void* ghi;   // n x n  T: G (tf32 hi part when split)
   float* glo;  // n x n  fp32 lo part (null: plain G in ghi)
   void* gpl;   // n x n  T: plain G (== ghi when not split)
+  float* gtt;  // n x 128 fp32: diagonal blocks of G^T in in-block lane order
   int* flags;  // Cholesky tile flags
   void* acc;   // n x m  T: sweep partial sums
   void* dpl[2];   // D (m x 128 T), by block parity
@@ -233,6 +234,7 @@ void gptq_reserve(Arena& ar, const ocwg_ctx* ctx, uint64_t n, uint64_t m, size_t
   o[7] = ar.reserve(2 * de * es);
   o[8] = ar.reserve(split ? 4 * de * 4 : 0);
   o[9] = ar.reserve(tc_ws_floats(n) * sizeof(float));
+  o[10] = ar.reserve(split ? n * 128 * 4 + 1024 : 0);
 }
 GptqBufs gptq_bufs(const Arena& ar, const ocwg_ctx* ctx, const size_t* o, uint64_t n, uint64_t m) {
   const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
@@ -255,6 +257,7 @@ GptqBufs gptq_bufs(const Arena& ar, const ocwg_ctx* ctx, const size_t* o, uint64
   }
   b.tcws = ar.at<float>(o[9]);
   b.tcws_floats = tc_ws_floats(n);
+  b.gtt = split ? ar.at<float>(o[10]) : nullptr;
   return b;
 }
 
@@ -268,7 +271,7 @@ void run_factor_t(ocwg_ctx* ctx, const float* h_dev, uint64_t n, int actorder, d
                                st);
   if (ctx->profile) cudaEventRecord(ctx->ev[1], st);
   cholesky_g<T>(static_cast<T*>(b.a), (long long)n, static_cast<T*>(b.ghi), b.glo,
-                b.glo ? static_cast<float*>(b.gpl) : nullptr, b.flags, ctx->flag,
+                b.glo ? static_cast<float*>(b.gpl) : nullptr, b.gtt, b.flags, ctx->flag,
                 chol_macro_cols(n), st);
   if (ctx->profile) {
     cudaEventRecord(ctx->ev[2], st);
@@ -293,7 +296,7 @@ void run_sweep_t(ocwg_ctx* ctx, const float* w, uint64_t ldw, uint64_t n, uint64
   float* const dh[2] = {b.dhi[0], b.dhi[1]};
   float* const dl[2] = {b.dlo[0], b.dlo[1]};
   gptq_sweep_g<T>(w, (long long)ldw, (long long)n, (long long)m, static_cast<const T*>(b.gpl),
-                  static_cast<const T*>(b.ghi), b.glo, b.order, c, scales, zeros,
+                  b.gtt, static_cast<const T*>(b.ghi), b.glo, b.order, c, scales, zeros,
                   (long long)opts->block_cols, codes, w_hat, (long long)ldw, static_cast<T*>(b.acc),
                   dp, dh, dl, ctx->stream, ctx->aux, ctx->sev);
 }
@@ -773,7 +776,7 @@ int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, do
     const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
     const uint64_t nblk = (n + 63) / 64;
     Arena ar(ctx);
-    size_t o[10];
+    size_t o[11];
     gptq_reserve(ar, ctx, n, 1, o);
     const size_t oh = ar.reserve(n * n * 4), ohi = ar.reserve(n * n * 8),
                  ou64 = ar.reserve(n * n * 8), ou = ar.reserve(n * n * es),
@@ -816,7 +819,7 @@ int ocwg_gptq_quantize_dev(ocwg_ctx* ctx, const float* w, uint64_t ldw, const fl
     std::lock_guard<std::mutex> lk(ctx->mu);
     begin(ctx, true);
     Arena ar(ctx);
-    size_t o[10];
+    size_t o[11];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     ar.commit();
@@ -898,6 +901,43 @@ int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, uint6
   });
 }
 
+int ocwg_qep_target(ocwg_ctx* ctx, const float* w, const double* gram, const double* cross,
+                    uint64_t n, uint64_t m, double alpha, double eta, float* out) {
+  return guard([&] {
+    // validation order of layerwise.cpp:96-101
+    if (!(alpha >= 0.0 && alpha <= 1.0)) fail(OCWG_INVALID_INPUT, "qep_target: alpha must be in [0,1]");
+    if (!(eta > 0.0)) fail(OCWG_INVALID_INPUT, "qep_target: eta must be positive");
+    if (alpha == 0.0) {
+      if (out != w) std::memmove(out, w, n * m * sizeof(float));
+      return;
+    }
+    if (n == 0) return;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    Arena ar(ctx);
+    const size_t ow = ar.reserve(n * m * 4), og = ar.reserve(n * n * 8), oc = ar.reserve(n * n * 8),
+                 oo = ar.reserve(n * m * 4),
+                 of = ar.reserve(cholesky_flag_ints((long long)n) * sizeof(int)),
+                 ows = ar.reserve(qep_workspace_doubles((long long)n, (long long)m) * 8);
+    ar.commit();
+    h2d(ar.at<float>(ow), w, n * m * 4, ctx);
+    h2d(ar.at<double>(og), gram, n * n * 8, ctx);
+    h2d(ar.at<double>(oc), cross, n * n * 8, ctx);
+    set_tc_workspace(nullptr, 0);
+    qep_target_f64(ar.at<float>(ow), ar.at<double>(og), ar.at<double>(oc), (long long)n,
+                   (long long)m, alpha, eta, ar.at<float>(oo), ar.at<double>(ows), ar.at<int>(of),
+                   ctx->flag, ctx->stream);
+    d2h(out, ar.at<float>(oo), n * m * 4, ctx);
+    try {
+      finish(ctx);
+    } catch (const Error& e) {
+      if (e.code == OCWG_NUMERIC_ERROR)
+        fail(OCWG_NUMERIC_ERROR, "qep_target: regularized Gram matrix is singular");
+      throw;
+    }
+  });
+}
+
 // ------------------------------------------------------------------ end to end
 int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint64_t tokens,
                               uint64_t n, uint64_t m, const ocwg_quant_config* cfg,
@@ -911,7 +951,7 @@ int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, 
     begin(ctx, true);
     const uint64_t ng = group_count(cfg, n, m);
     Arena ar(ctx);
-    size_t o[10];
+    size_t o[11];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const size_t oh = ar.reserve(n * n * 4);
@@ -986,7 +1026,7 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
     float* hd = reinterpret_cast<float*>(io + oh);
     // ---- workspace
     Arena ar(ctx);
-    size_t o[10];
+    size_t o[11];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const long long chunk = 32768;  // tokens per H2D chunk (a multiple of the 16384 split)

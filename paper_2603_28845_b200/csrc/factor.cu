@@ -27,6 +27,9 @@
 // kernel over a column range, then one tcgen05 3xTF32 SYRK for the trailing
 // matrix (gemm.cu / tc_gemm.cu).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "kernels.h"
 
@@ -90,6 +93,36 @@ __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t u = __float_as_uint(x);
   u = (u + 0xFFFu + ((u >> 13) & 1u)) & ~0x1FFFu;  // RNE to 10 mantissa bits
   return __uint_as_float(u);
+}
+
+// 1/x and 1/sqrt(x) to fp32 accuracy without the IEEE slow-path checks
+// (pivots are positive normal numbers, or the factorisation has failed)
+__device__ __forceinline__ float rcp_nr(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return fmaf(y, fmaf(-x, y, 1.0f), y);
+}
+__device__ __forceinline__ double rcp_nr(double x) { return 1.0 / x; }
+__device__ __forceinline__ float rsqrt_nr(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y * fmaf(-0.5f * x * y, y, 1.5f);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) { return rsqrt(x); }
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(a, b);
+  reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
+}
+
+// Position of block-local column kk (0..127) of a sweep block row in the
+// in-block kernel's order: lane group rg = kk % 4 owns slots s = kk / 4,
+// stored in 16-byte chunks c = s / 4, XOR-swizzled by 2 rg (sweep.cu).
+__host__ __device__ inline int gp_pos(int kk) {
+  const int rg = kk & 3, s = kk >> 2;
+  return rg * 32 + 4 * ((s >> 2) ^ (2 * rg)) + (s & 3);
 }
 
 // A 64x64 tile (row-major, ld) <-> 16 elements per thread: rows tid/16 + 16*ii,
@@ -216,9 +249,18 @@ __device__ void emit_g(const T (&t)[4][4], CholSmem<T>& sm, const T* diag, int r
 template <typename T>
 __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
     chol_tile_kernel(T* __restrict__ a, long long n, int nt, int c0, int c1, int* flags,
-                     int* counter, unsigned* status, T* ghi, float* glo, float* gpl) {
+                     int* counter, unsigned* status, T* ghi, float* glo, float* gpl, float* gtt,
+                     unsigned long long* trace) {
   extern __shared__ __align__(16) unsigned char smraw[];
   CholSmem<T>& sm = *reinterpret_cast<CholSmem<T>*>(smraw);
+  // optional timeline (debug): per item {r, c, start, k-loop done, solve done, published}
+  auto stamp = [&](long long item, int slot) {
+    if (trace && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[item * 6 + slot] = t;
+    }
+  };
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15, lane = tid & 31;
   const bool vec_ok = (sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0);
   long long total = 0;
@@ -230,12 +272,18 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
     long long idx = sm.item;
     __syncthreads();
     if (idx >= total) break;
+    const long long item_id = idx;
     int c = c0;
     while (idx >= nt - c) {
       idx -= nt - c;
       ++c;
     }
     const int r = c + int(idx);
+    if (trace && tid == 0) {
+      trace[item_id * 6 + 0] = (unsigned long long)r;
+      trace[item_id * 6 + 1] = (unsigned long long)c;
+    }
+    stamp(item_id, 2);
     const int rows = int(std::min<long long>(TB, n - (long long)r * TB));
     const int cols = int(std::min<long long>(TB, n - (long long)c * TB));
 
@@ -298,44 +346,42 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       }
     }
 
+    stamp(item_id, 3);
     if (r == c) {
       // ---- diagonal tile: right-looking elimination, one barrier per step.
       // Unscaled column u[.] = a[.][j] is published; a[r][c] -= u_r u_c / u_j.
+      // Lanes whose 4 columns all lie right of pivot group j0 update all 16
+      // entries, the pivot-owning lanes the columns right of j (upper-triangle
+      // entries take garbage and are zeroed afterwards).
       bool bad = false;
 #pragma unroll 1
       for (int j0 = 0; j0 < TB; j0 += 4) {
+        const bool own = tx == (j0 >> 2), later = tx > (j0 >> 2);
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
           const int j = j0 + jj, buf = j & 1;
-          if (tx == (j >> 2)) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) sm.col[buf][4 * ty + u] = t[u][jj];
-          }
+          if (own) st4(&sm.col[buf][4 * ty], t[0][jj], t[1][jj], t[2][jj], t[3][jj]);
           __syncthreads();
           const T p = sm.col[buf][j];
           bad |= !(p > T(0));
-          const T rp = T(1) / p;
-          const T sq = sqrt(p);
-          const T rsq = sq * rp;  // 1/sqrt(p)
+          const T rp = rcp_nr(p);
+          const T rsq = rsqrt_nr(p);
           T cr[4], cc[4];
           ld4(&sm.col[buf][4 * ty], cr);
           ld4(&sm.col[buf][4 * tx], cc);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int rr = 4 * ty + u;
             const T cru = cr[u] * rp;
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const int cl = 4 * tx + v;
-              if (cl > j && cl <= rr) t[u][v] = fma(-cru, cc[v], t[u][v]);
-            }
+            for (int v = 0; v < 4; ++v)
+              if (later || (own && v > jj)) t[u][v] = fma(-cru, cc[v], t[u][v]);
           }
-          if (tx == (j >> 2)) {
+          if (own) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int rr = 4 * ty + u;
               if (rr > j) t[u][jj] = cr[u] * rsq;
-              else if (rr == j) t[u][jj] = sq;
+              else if (rr == j) t[u][jj] = p * rsq;
             }
           }
         }
@@ -378,29 +424,26 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       const int src0 = lane & 16;
 #pragma unroll 1
       for (int j0 = 0; j0 < TB; j0 += 4) {
+        const bool own = tx == (j0 >> 2), later = tx > (j0 >> 2);
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
           const int j = j0 + jj;
           const T rd = sm.rdiag[j];
           T x[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const T own = t[u][jj] * rd;
-            x[u] = __shfl_sync(0xffffffffu, own, src0 + (j >> 2));
-          }
-          if (tx == (j >> 2)) {
+          for (int u = 0; u < 4; ++u) x[u] = __shfl_sync(0xffffffffu, t[u][jj] * rd, src0 + (j >> 2));
+          if (own) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) t[u][jj] = x[u];
           }
           T l[4];
           ld4(&sm.lt[j][4 * tx], l);
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            if (4 * tx + v > j) {
+          for (int v = 0; v < 4; ++v)
+            if (later || (own && v > jj)) {
 #pragma unroll
               for (int u = 0; u < 4; ++u) t[u][v] = fma(-x[u], l[v], t[u][v]);
             }
-          }
         }
       }
       // diag values of L_cc for G scaling: lt[j][j]
@@ -408,6 +451,7 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       if (tid < TB) sm.rdiag[tid] = sm.lt[tid][tid];
     }
 
+    stamp(item_id, 4);
     // ---- store L[r,c], publish
     {
       T* ab = a + (long long)r * TB * n + (long long)c * TB;
@@ -424,6 +468,25 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
     __threadfence();
     __syncthreads();
     if (tid == 0) st_release(flags + r * nt + c, 1);
+    stamp(item_id, 5);
+    if (gtt) {
+      // diagonal 128 x 128 blocks of G^T in the sweep's lane order (sweep.cu
+      // gp_pos): row i = n-1-b, column k = n-1-a, only when i, k share a block
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long b = (long long)r * TB + 4 * ty + u;
+        if (b >= n) continue;
+        const long long i = n - 1 - b;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const long long av = (long long)c * TB + 4 * tx + v;
+          if (av >= n || b <= av) continue;
+          const long long k = n - 1 - av;
+          if ((i >> 7) != (k >> 7)) continue;
+          gtt[i * 128 + gp_pos(int(k & 127))] = float(t[u][v] / sm.rdiag[4 * tx + v]);
+        }
+      }
+    }
     if (ghi) {
       // rdiag holds L[a][a] of column tile c (written before the last barrier)
       emit_g(t, sm, sm.rdiag, r, c, n, ghi, glo, gpl);
@@ -509,8 +572,8 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
 }
 
 template <typename T>
-void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, int* flags, unsigned* status,
-                long long macro_cols, cudaStream_t st) {
+void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, float* gtt, int* flags,
+                unsigned* status, long long macro_cols, cudaStream_t st) {
   static const bool attr = [] {
     cudaFuncSetAttribute(chol_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(CholSmem<T>)));
@@ -520,6 +583,7 @@ void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, int* flags, u
   const int nt = int((n + TB - 1) / TB);
   int* counters = flags + (long long)nt * nt;
   cudaMemsetAsync(flags, 0, cholesky_flag_ints(n) * sizeof(int), st);
+  if (gtt) cudaMemsetAsync(gtt, 0, size_t(n) * 128 * sizeof(float), st);  // non-emitted = 0
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_tile_kernel<T>, CT,
                                                 sizeof(CholSmem<T>));
@@ -532,8 +596,22 @@ void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, int* flags, u
     for (int c = c0; c < c1; ++c) items += nt - c;
     const int grid = int(std::min<long long>(items, max_ctas));
     count_launches(1);
+    unsigned long long* trace = nullptr;
+    const char* tp = getenv("OCWG_CHOL_TRACE");
+    if (tp) cudaMallocAsync(&trace, size_t(items) * 6 * 8, st);
     chol_tile_kernel<T><<<grid, CT, sizeof(CholSmem<T>), st>>>(a, n, nt, c0, c1, flags,
-                                                                counters + ci, status, ghi, glo, gpl);
+                                                                counters + ci, status, ghi, glo, gpl,
+                                                                gtt, trace);
+    if (tp) {
+      std::vector<unsigned long long> h(size_t(items) * 6);
+      cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      cudaFreeAsync(trace, st);
+      if (FILE* f = fopen(tp, "ab")) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+      }
+    }
     const long long k0 = (long long)c0 * TB, k1 = std::min<long long>(n, (long long)c1 * TB);
     const long long rest = n - k1;
     if (rest > 0)  // trailing SYRK: A22 -= L21 L21^T (lower tiles)
@@ -542,17 +620,15 @@ void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, int* flags, u
   }
 }
 
-// U = (J L J)^-1 from the Cholesky factor (a, lower): parity artefact path.
-// ws: nblk*64*64 + n*n elements; u receives U (n x n upper).
+// X = L^-1 (n x n lower) from the Cholesky factor (a, lower) by recursive
+// doubling over the 64x64 diagonal blocks.  ws: nblk*64*64 + n*n elements.
 template <typename T>
-void upper_from_cholesky(const T* a, long long n, T* u, T* ws, cudaStream_t st) {
+void lower_inverse(const T* a, long long n, T* x, T* ws, cudaStream_t st) {
   const long long nblk = (n + TB - 1) / TB;
   T* dinv = ws;
   T* tmp = ws + nblk * TB * TB;
   count_launches(2);
   diag_inverse_kernel<T><<<unsigned(nblk), 64, 0, st>>>(a, n, dinv);
-  // X = L^-1 by recursive doubling over the diagonal blocks (in u)
-  T* x = u;
   init_inverse_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(x, n, dinv);
   for (long long s = 2 * TB; s < 2 * n; s *= 2) {
     const long long h = s / 2;
@@ -572,8 +648,17 @@ void upper_from_cholesky(const T* a, long long n, T* u, T* ws, cudaStream_t st) 
             x + (p0 + h) * n + p0, n, false, st);
     }
   }
+}
+
+// U = (J L J)^-1 from the Cholesky factor (a, lower): parity artefact path.
+// ws: ceil(n/64)*64*64 + n*n elements; u receives U (n x n upper).
+template <typename T>
+void upper_from_cholesky(const T* a, long long n, T* u, T* ws, cudaStream_t st) {
+  const long long nblk = (n + TB - 1) / TB;
+  lower_inverse<T>(a, n, u, ws, st);
+  T* tmp = ws + nblk * TB * TB;
   count_launches(1);
-  reverse_to_upper_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(x, n, tmp);
+  reverse_to_upper_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(u, n, tmp);
   cudaMemcpyAsync(u, tmp, size_t(n * n) * sizeof(T), cudaMemcpyDeviceToDevice, st);
 }
 
@@ -586,10 +671,12 @@ template void launch_build_factor_input<float>(const float*, long long, const in
                                                float*, double*, cudaStream_t);
 template void launch_build_factor_input<double>(const float*, long long, const int32_t*, double,
                                                 double*, double*, cudaStream_t);
-template void cholesky_g<float>(float*, long long, float*, float*, float*, int*, unsigned*,
-                                long long, cudaStream_t);
-template void cholesky_g<double>(double*, long long, double*, float*, float*, int*, unsigned*,
-                                 long long, cudaStream_t);
+template void cholesky_g<float>(float*, long long, float*, float*, float*, float*, int*,
+                                unsigned*, long long, cudaStream_t);
+template void cholesky_g<double>(double*, long long, double*, float*, float*, float*, int*,
+                                 unsigned*, long long, cudaStream_t);
+template void lower_inverse<float>(const float*, long long, float*, float*, cudaStream_t);
+template void lower_inverse<double>(const double*, long long, double*, double*, cudaStream_t);
 template void upper_from_cholesky<float>(const float*, long long, float*, float*, cudaStream_t);
 template void upper_from_cholesky<double>(const double*, long long, double*, double*,
                                           cudaStream_t);

@@ -193,6 +193,7 @@ void mm<double>(long long m, long long n, long long k, double alpha, const doubl
 OCWG_GEMM_INST(double, double, double)
 OCWG_GEMM_INST(double, float, float)
 OCWG_GEMM_INST(double, float, double)
+OCWG_GEMM_INST(double, double, float)
 OCWG_GEMM_INST(float, float, float)
 
 }  // namespace ocwg

@@ -55,12 +55,16 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
 // (<= 0: one panel) with a trailing SYRK (mm<T>) between panels.  Emits
 // G[k][i] = L[n-1-i][n-1-k] / L[n-1-k][n-1-k] (i < k) for the sweep into ghi
 // (+ glo: tf32 hi/lo split when non-null, T = float, with the plain value in
-// gpl).  flags: ints from cholesky_flag_ints(n).  Sets kFlagNotPD in *status
-// on breakdown.
+// gpl; gtt (optional): the diagonal 128 x 128 blocks of G^T, n x 128 fp32, in
+// the in-block kernel's lane order (gp_pos in factor.cu)).  flags: ints
+// from cholesky_flag_ints(n).  Sets kFlagNotPD in *status on breakdown.
 size_t cholesky_flag_ints(long long n);
 template <typename T>
-void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, int* flags, unsigned* status,
-                long long macro_cols, cudaStream_t st);
+void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, float* gtt, int* flags,
+                unsigned* status, long long macro_cols, cudaStream_t st);
+// X = L^-1 (n x n lower) from the Cholesky factor; ws as upper_from_cholesky.
+template <typename T>
+void lower_inverse(const T* a, long long n, T* x, T* ws, cudaStream_t st);
 // U = (J L J)^-1 (n x n upper, processing order) from the Cholesky factor:
 // parity artefacts only.  ws: ceil(n/64)*64*64 + n*n elements.
 template <typename T>
@@ -114,7 +118,7 @@ size_t sweep_delta_elems(long long m);
 // ev: 5 events (fork, in-block, trailing x2, join).
 template <typename T>
 void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const T* gpl,
-                  const T* ghi, const float* glo, const int32_t* order, const QCfg& c,
+                  const float* gtt, const T* ghi, const float* glo, const int32_t* order, const QCfg& c,
                   const float* scales, const int32_t* zeros, long long block, int16_t* codes,
                   float* w_hat, long long ldo, T* acc, T* const dpl[2], float* const dhi[2],
                   float* const dlo[2], cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev);
@@ -135,6 +139,13 @@ void hessian_simt(const uint16_t* x, long long tokens, long long dim, float* h, 
 // fp32 -> bf16 (RNE) conversion, and "all values bf16-exact" check
 void launch_f32_to_bf16(const float* x, long long n, uint16_t* out, unsigned* inexact,
                         cudaStream_t st);
+
+// ---- QEP target correction (qep.cu), fp64 -----------------------------------
+size_t qep_workspace_doubles(long long n, long long m);
+// out = W + alpha (gram + eta*mean(diag gram) I)^-1 (cross W); flags: Cholesky flags
+void qep_target_f64(const float* w, const double* gram, const double* cross, long long n,
+                    long long m, double alpha, double eta, float* out, double* ws, int* flags,
+                    unsigned* status, cudaStream_t st);
 
 // ---- misc ----------------------------------------------------------------
 void launch_f64_to_f32(const double* in, long long n, float* out, cudaStream_t st);

@@ -54,6 +54,10 @@ __device__ __forceinline__ void cp_async(T* dst, const T* src) {
                "n"(int(sizeof(T)))
                : "memory");
 }
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -70,12 +74,18 @@ __device__ __forceinline__ void ld4(const T* p, T (&o)[4]) {
   }
 }
 
-__host__ __device__ constexpr int packed_off(int li) { return li * kB - li * (li + 1) / 2; }
+// Rotated G block: for row li = 8t + o the coefficients a lane (rg) needs are
+// G[rg + 8(t + kk)][li], kk = 0..RPT-1 -- its register slot kk after t
+// rotations -- stored contiguously at gt[li][rg * kRg + kk] (zero where the row
+// is outside the block or not strictly below li), so a row step is RPT/4
+// LDS.128 and RPT unconditional FMAs.  kRg = 20 (not 16) spreads the 8
+// row groups of a warp over all 32 banks.
+constexpr int kRg = 20;
 
 template <typename T>
 struct InblockSmem {
   union {
-    T gs[packed_off(kB)];  // strictly-lower G block, column-packed: (k, li) at off(li)+k-li-1
+    T gt[kB][8 * kRg];
     struct {
       T gc[kB][kLaChunk + 4];     // lookahead: G[ib + li][kprev + q0 + q]
       T dp[kCols][kLaChunk + 4];  // lookahead: D_prev[q0 + q] of column cj
@@ -83,6 +93,7 @@ struct InblockSmem {
   } u;
   T ds[kCols][kB + 1];  // D of this block, staged for the K-major store
   int og[kB];           // processing -> original row of the block
+  long long orow[kB];   // og * ldo: output row offsets
 };
 
 template <typename T, int RPT>
@@ -93,6 +104,7 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
     float* __restrict__ dcur_lo, QCfg c, const float* __restrict__ scales,
     const int32_t* __restrict__ zeros, long long n, long long m, long long ib, int bsz,
     int16_t* __restrict__ codes, float* __restrict__ w_hat, long long ldo) {
+  static_assert(RPT % 4 == 0 && RPT <= kRg, "row slots");
   extern __shared__ __align__(16) unsigned char smraw[];
   InblockSmem<T>& sm = *reinterpret_cast<InblockSmem<T>*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -102,28 +114,32 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
   const long long j = j0 + cj;
   const bool col_ok = j < m;
 
-  for (int e = tid; e < kB; e += 256) sm.og[e] = e < bsz ? order[ib + e] : 0;
+  for (int e = tid; e < kB; e += 256) {
+    sm.og[e] = e < bsz ? order[ib + e] : 0;
+    sm.orow[e] = (long long)sm.og[e] * ldo;
+  }
   __syncthreads();
-  // ---- per-lane rows rg + 8t: current partial sums, original weights, grids
+  // ---- per-lane rows rg + 8t: partial sums, original weights, grids (+ 1/s)
   T r[RPT];
-  float w0[RPT], s[RPT];
-  int z[RPT];
+  float w0[RPT], s[RPT], y[RPT], zf[RPT];
 #pragma unroll
   for (int t = 0; t < RPT; ++t) {
     const int li = rg + 8 * t;
     r[t] = T(0);
     w0[t] = 0.f;
     s[t] = 1.f;
-    z[t] = 0;
+    zf[t] = 0.f;
     if (col_ok && li < bsz) {
       const long long orig = sm.og[li];
       w0[t] = w[orig * ldw + j];
       const long long g = group_of(c, orig, j);
       s[t] = scales[g];
-      z[t] = zeros[g];
+      zf[t] = float(zeros[g]);
       if (use_acc) r[t] = acc[(ib + li) * m + j];
     }
+    y[t] = rcp_refined(s[t]);
   }
+  const float qminf = float(c.qmin), qmaxf = float(c.qmax);
 
   // ---- lookahead: r += G[blk, prev blk] * D_prev  (the slice trailing(b-1) skipped)
   if (bprev > 0) {
@@ -163,47 +179,63 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
     }
   }
 
-  // ---- stage the block's strictly-lower G (packed by column)
-  for (int k = 1 + warp; k < bsz; k += 8)
-    for (int li = lane; li < k; li += 32)
-      cp_async(&sm.u.gs[packed_off(li) + k - li - 1], gpl + (ib + k) * n + ib + li);
+  // ---- stage the block's G in the rotated layout (coalesced along li)
+  for (int e = tid; e < kB * 8 * RPT; e += 256) {
+    const int li = e % kB, slot = e / kB;  // slot = rg * RPT + kk
+    const int rgs = slot / RPT, kk = slot % RPT;
+    const int k = rgs + 8 * ((li >> 3) + kk);  // row of G this slot multiplies
+    T* dst = &sm.u.gt[li][rgs * kRg + kk];
+    if (li < bsz && k < bsz && k > li)
+      cp_async(dst, gpl + (ib + k) * n + ib + li);
+    else
+      *dst = T(0);
+  }
   cp_async_wait_all();
   __syncthreads();
 
-  // ---- sequential rows li = 8t + o; owner lane rg == o holds the row in slot 0
+  // ---- sequential rows li = 8t + o; owner lane rg == o holds the row in slot 0.
+  // Every lane quantises its own slot 0 (branch-free); the owner's D is broadcast.
+  int16_t* code_col = codes + j;
+  float* wh_col = w_hat ? w_hat + j : nullptr;
 #pragma unroll 1
   for (int t = 0; t < RPT; ++t) {
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
       const int li = 8 * t + o;
       if (li >= bsz) break;
-      T d = T(0);
+      // coefficients of this row first: their smem latency overlaps the chain
+      T g[RPT];
+      const T* gp = &sm.u.gt[li][rg * kRg];
+#pragma unroll
+      for (int k4 = 0; k4 < RPT; k4 += 4) {
+        T g4[4];
+        ld4(gp + k4, g4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) g[k4 + e] = g4[e];
+      }
+      const T cur = T(w0[0]) + r[0];  // w_cur = w + sum G D
+      const float cf = quantize_code_f(div_rn_fast(float(cur), s[0], y[0]), zf[0], qminf, qmaxf);
+      const float wh = __fmul_rn(s[0], __fsub_rn(cf, zf[0]));  // quant.cpp:33-35
+      T d = T(w0[0]) - T(wh);
       if (rg == o) {
-        const T cur = T(w0[0]) + r[0];  // w_cur = w + sum G D
-        const int q = quantize_code(float(cur), s[0], z[0], c.qmin, c.qmax);  // row_f (:70)
-        const float wh = dequantize_code(q, s[0], z[0]);
-        d = T(w0[0]) - T(wh);
         if (col_ok) {
-          const long long orig = sm.og[li];
-          codes[orig * ldo + j] = int16_t(q);  // original row order (:75)
-          if (w_hat) w_hat[orig * ldo + j] = wh;
+          const long long orow = sm.orow[li];  // original row order (:75)
+          code_col[orow] = int16_t(int(cf));
+          if (wh_col) wh_col[orow] = wh;
         }
         sm.ds[cj][li] = d;
       }
       d = __shfl_sync(0xffffffffu, d, cc + 4 * o);
-      const T* gcol = sm.u.gs + packed_off(li) - li - 1;  // gcol[k] = G[k][li]
 #pragma unroll
-      for (int kk = 0; kk < RPT; ++kk) {
-        const int row = rg + 8 * (t + kk);
-        if ((kk > 0 || rg > o) && t + kk < RPT && row < bsz) r[kk] = fma(gcol[row], d, r[kk]);
-      }
+      for (int k = 0; k < RPT; ++k) r[k] = fma(g[k], d, r[k]);
     }
 #pragma unroll
     for (int k = 0; k + 1 < RPT; ++k) {
       r[k] = r[k + 1];
       w0[k] = w0[k + 1];
       s[k] = s[k + 1];
-      z[k] = z[k + 1];
+      y[k] = y[k + 1];
+      zf[k] = zf[k + 1];
     }
   }
   __syncthreads();
@@ -221,6 +253,218 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
       dcur_lo[off] = float(v) - hi;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// fp32, 128-row blocks: 4 lanes per column (lane = cc + 8 rg), 8 columns per
+// warp, 2 warps (16 columns) per CTA.  Lane group rg owns rows rg + 4s,
+// s = 0..31, in registers r[k] <-> s = k + 4T, where T counts 16-row steps: the
+// 16-row body is unrolled (the owner of row 4t + o is rg = o, slot k = t % 4,
+// static) and the registers rotate by 4 slots after it -- compact code (the
+// body fits the instruction cache) with static register indices.  The
+// coefficients G[rg + 4s][li] of a row are a contiguous, 16-byte aligned run
+// of the diagonal block of G^T that the Cholesky emits in exactly this order
+// (factor.cu gp_pos; chunks XOR-swizzled by 2 rg so the 4 lane groups hit
+// distinct banks): 8 LDS.128 per row.  The owner's (w, s, 1/s, z) come from a
+// per-row table gathered once with cp.async.
+namespace l4 {
+constexpr int kLpc = 4, kRpt = 32, kCpw = 8, kWarps = 2, kCols4 = kCpw * kWarps;
+
+struct Smem {
+  union {
+    float gt[kB * kB + 32];  // block rows of G^T in lane order (+ pad for dead slots)
+    struct {
+      float gc[kB][kLaChunk + 4];
+      float dp[kCols4][kLaChunk + 4];
+    } la;
+  } u;
+  float4 tab[kB][kCols4];  // {w, s, 1/s, z} of (row li, column cj)
+  float ds[kCols4][kB + 1];
+  long long orow[kB];
+  int og[kB];
+};
+
+__global__ void __launch_bounds__(64) inblock4_kernel(
+    const float* __restrict__ w, long long ldw, const int32_t* __restrict__ order,
+    const float* __restrict__ acc, int use_acc, const float* __restrict__ gpl,
+    const float* __restrict__ gpb, const float* __restrict__ dprev, int bprev,
+    float* __restrict__ dcur, float* __restrict__ dcur_hi, float* __restrict__ dcur_lo, QCfg c,
+    const float* __restrict__ scales, const int32_t* __restrict__ zeros, long long n, long long m,
+    long long ib, int bsz, int16_t* __restrict__ codes, float* __restrict__ w_hat, long long ldo) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cc = lane & 7, rg = lane >> 3;
+  const int cj = warp * kCpw + cc;
+  const long long j0 = (long long)blockIdx.x * kCols4;
+  const long long j = j0 + cj;
+  const bool col_ok = j < m;
+
+  // ---- per-row table: original row, output offset, (w, s, 1/s, z) per column;
+  // gathered with 4-byte cp.async (every load in flight at once)
+  for (int e = tid; e < kB; e += 64) {
+    const int o = e < bsz ? order[ib + e] : 0;
+    sm.og[e] = o;
+    sm.orow[e] = (long long)o * ldo;
+  }
+  __syncthreads();
+  for (int e = tid; e < kB * kCols4; e += 64) {
+    const int li = e / kCols4, cl = e % kCols4;
+    const long long jj = j0 + cl;
+    float4* v = &sm.tab[li][cl];
+    if (li < bsz && jj < m) {
+      const long long orig = sm.og[li];
+      const long long g = group_of(c, orig, jj);
+      cp_async(&v->x, w + orig * ldw + jj);
+      cp_async(&v->y, scales + g);
+      cp_async(reinterpret_cast<int*>(&v->w), zeros + g);
+    } else {
+      *v = make_float4(0.f, 1.f, 1.f, 0.f);
+      reinterpret_cast<int*>(&v->w)[0] = 0;
+    }
+  }
+  float r[kRpt];
+#pragma unroll
+  for (int k = 0; k < kRpt; ++k) {
+    const int li = rg + 4 * k;
+    r[k] = (use_acc && col_ok && li < bsz) ? acc[(ib + li) * m + j] : 0.f;
+  }
+  // ---- lookahead: r += G[blk, prev blk] D_prev (16-byte staging)
+  if (bprev > 0) {
+    const long long kprev = ib - bprev;
+    for (int q0 = 0; q0 < bprev; q0 += kLaChunk) {
+      for (int e = tid; e < kB * kLaChunk / 4; e += 64) {
+        const int li = e / (kLaChunk / 4), q = (e % (kLaChunk / 4)) * 4;
+        float* dst = &sm.u.la.gc[li][q];
+        if (li < bsz && q0 + q < bprev)
+          cp_async16(dst, gpl + (ib + li) * n + kprev + q0 + q);
+        else
+          *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int e = tid; e < kCols4 * kLaChunk / 4; e += 64) {
+        const int cl = e / (kLaChunk / 4), q = (e % (kLaChunk / 4)) * 4;
+        float* dst = &sm.u.la.dp[cl][q];
+        if (j0 + cl < m && q0 + q < bprev)
+          cp_async16(dst, dprev + (j0 + cl) * kB + q0 + q);
+        else
+          *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+#pragma unroll 1
+      for (int q = 0; q < kLaChunk; q += 4) {
+        float dv[4];
+        ld4(&sm.u.la.dp[cj][q], dv);
+#pragma unroll
+        for (int k = 0; k < kRpt; ++k) {
+          float g[4];
+          ld4(&sm.u.la.gc[rg + 4 * k][q], g);
+          r[k] = fmaf(g[0], dv[0], r[k]);
+          r[k] = fmaf(g[1], dv[1], r[k]);
+          r[k] = fmaf(g[2], dv[2], r[k]);
+          r[k] = fmaf(g[3], dv[3], r[k]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- the block's rows of G^T (already in lane order): 16-byte copies
+  for (int e = tid; e < kB * kB / 4; e += 64) {
+    const int li = e / (kB / 4), q = (e % (kB / 4)) * 4;
+    float* dst = &sm.u.gt[li * kB + q];
+    if (li < bsz)
+      cp_async16(dst, gpb + (ib + li) * kB + q);
+    else
+      *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (tid < 8) reinterpret_cast<float4*>(&sm.u.gt[kB * kB])[tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+  cp_async_wait_all();
+  __syncthreads();
+  for (int e = tid; e < kB * kCols4; e += 64) {  // 1/s and float(z) for the table
+    float4& v = sm.tab[e / kCols4][e % kCols4];
+    v.z = rcp_refined(v.y);
+    v.w = float(__float_as_int(v.w));
+  }
+  __syncthreads();
+
+  const float qminf = float(c.qmin), qmaxf = float(c.qmax);
+  int16_t* code_col = codes + j;
+  float* wh_col = w_hat ? w_hat + j : nullptr;
+#pragma unroll 1
+  for (int T = 0; T < kRpt / 4; ++T) {
+    if (16 * T >= bsz) break;
+    int off[8];  // chunk offsets of this lane's slots k = 4m .. 4m+3 (logical chunk T + m)
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) off[mm] = rg * 32 + 4 * ((T + mm) ^ (2 * rg));
+#pragma unroll
+    for (int tt = 0; tt < 4; ++tt) {
+#pragma unroll
+      for (int o = 0; o < kLpc; ++o) {
+        const int li = 16 * T + 4 * tt + o;
+        if (li < bsz) {
+          float g[kRpt];
+          const float* gp = &sm.u.gt[li * kB];
+#pragma unroll
+          for (int mm = 0; mm < 8; ++mm) {
+            float g4[4];
+            ld4(gp + off[mm], g4);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) g[4 * mm + e] = g4[e];
+          }
+          const float4 tv = sm.tab[li][cj];  // (w, s, 1/s, z) of row li
+          const float x = __fadd_rn(tv.x, r[tt]);  // w_cur = w + sum G D (owner lanes)
+          const float cf = quantize_code_f(div_rn_fast(x, tv.y, tv.z), tv.w, qminf, qmaxf);
+          const float wh = __fmul_rn(tv.y, __fsub_rn(cf, tv.w));  // quant.cpp:33-35
+          float d = __fsub_rn(tv.x, wh);
+          if (rg == o) {
+            if (col_ok) {
+              const long long orow = sm.orow[li];  // original row order (:75)
+              code_col[orow] = int16_t(int(cf));
+              if (wh_col) wh_col[orow] = wh;
+            }
+            sm.ds[cj][li] = d;
+          }
+          d = __shfl_sync(0xffffffffu, d, cc + kCpw * o);
+#pragma unroll
+          for (int k = 0; k < kRpt; ++k) r[k] = fmaf(g[k], d, r[k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRpt; ++k) r[k] = k + 4 < kRpt ? r[k + 4] : 0.f;
+  }
+  __syncthreads();
+  for (int e = tid; e < kCols4 * kB; e += 64) {
+    const int cl = e / kB, li = e % kB;
+    if (j0 + cl >= m) continue;
+    const float v = li < bsz ? sm.ds[cl][li] : 0.f;
+    const long long off = (j0 + cl) * kB + li;
+    dcur[off] = v;
+    if (dcur_hi) {
+      const float hi = tf32_hi(v);
+      dcur_hi[off] = hi;
+      dcur_lo[off] = v - hi;
+    }
+  }
+}
+}  // namespace l4
+
+void launch_inblock4(const float* w, long long ldw, const int32_t* order, const float* acc,
+                     int use_acc, const float* gpl, const float* gtt, const float* dprev, int bprev,
+                     float* dcur, float* dch, float* dcl, const QCfg& c, const float* scales,
+                     const int32_t* zeros, long long n, long long m, long long ib, int bsz,
+                     int16_t* codes, float* w_hat, long long ldo, cudaStream_t st) {
+  static const bool attr = [] {
+    cudaFuncSetAttribute(l4::inblock4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(l4::Smem)));
+    return true;
+  }();
+  (void)attr;
+  const unsigned ctas = unsigned((m + l4::kCols4 - 1) / l4::kCols4);
+  count_launches(1);
+  l4::inblock4_kernel<<<ctas, 64, sizeof(l4::Smem), st>>>(w, ldw, order, acc, use_acc, gpl, gtt,
+                                                          dprev, bprev, dcur, dch, dcl, c, scales,
+                                                          zeros, n, m, ib, bsz, codes, w_hat, ldo);
 }
 
 template <typename T, int RPT>
@@ -248,7 +492,7 @@ size_t sweep_delta_elems(long long m) { return size_t(m) * kB; }
 
 template <typename T>
 void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const T* gpl,
-                  const T* ghi, const float* glo, const int32_t* order, const QCfg& c,
+                  const float* gtt, const T* ghi, const float* glo, const int32_t* order, const QCfg& c,
                   const float* scales, const int32_t* zeros, long long block, int16_t* codes,
                   float* w_hat, long long ldo, T* acc, T* const dpl[2], float* const dhi[2],
                   float* const dlo[2], cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev) {
@@ -275,6 +519,12 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
     else if (B <= 64)
       launch_inblock<T, 8>(w, ldw, order, acc, b >= 2, gpl, dprev, bprev, dpl[p], dch, dcl, c,
                            scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, st);
+    else if (sizeof(T) == 4 && gtt)
+      launch_inblock4(w, ldw, order, reinterpret_cast<const float*>(acc), b >= 2,
+                      reinterpret_cast<const float*>(gpl), gtt,
+                      reinterpret_cast<const float*>(dprev), bprev,
+                      reinterpret_cast<float*>(dpl[p]), dch, dcl, c, scales, zeros, n, m, ib, bsz,
+                      codes, w_hat, ldo, st);
     else
       launch_inblock<T, 16>(w, ldw, order, acc, b >= 2, gpl, dprev, bprev, dpl[p], dch, dcl, c,
                             scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, st);
@@ -302,12 +552,12 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
 }
 
 template void gptq_sweep_g<float>(const float*, long long, long long, long long, const float*,
-                                  const float*, const float*, const int32_t*, const QCfg&,
+                                  const float*, const float*, const float*, const int32_t*, const QCfg&,
                                   const float*, const int32_t*, long long, int16_t*, float*,
                                   long long, float*, float* const[2], float* const[2],
                                   float* const[2], cudaStream_t, cudaStream_t, cudaEvent_t*);
 template void gptq_sweep_g<double>(const float*, long long, long long, long long, const double*,
-                                   const double*, const float*, const int32_t*, const QCfg&,
+                                   const float*, const double*, const float*, const int32_t*, const QCfg&,
                                    const float*, const int32_t*, long long, int16_t*, float*,
                                    long long, double*, double* const[2], float* const[2],
                                    float* const[2], cudaStream_t, cudaStream_t, cudaEvent_t*);
