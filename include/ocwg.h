@@ -206,6 +206,10 @@ int ocwg_debug_profile(ocwg_ctx* ctx, int on, double* phase_ms);
 int ocwg_debug_gemm(ocwg_ctx* ctx, int precision, uint64_t m, uint64_t n, uint64_t k, double alpha,
                     const void* a, uint64_t lda, int ta, const void* b, uint64_t ldb, int tb,
                     double beta, void* c, uint64_t ldc, int lower_only, int reps, double* ms);
+/* Micro-benchmark of the 64 x 64 diagonal-tile factorisation (one CTA):
+ * cycles[0] = total clocks over `iters` runs, cycles[1] = clocks of the last;
+ * l_out (64 x 64 fp32) = the factor, for a check. */
+int ocwg_debug_factor_bench(ocwg_ctx* ctx, int iters, long long* cycles, float* l_out);
 /* Number of kernels this library launched on the context so far. */
 uint64_t ocwg_launch_count(ocwg_ctx* ctx);
 

@@ -36,7 +36,7 @@ __all__ = [
     "CalibStats", "LayerQuantOptions", "QepOptions", "qep_target", "base_method_from_name", "InvalidInput", "NumericError", "IoError", "CudaError",
     "calibrate_grids", "quantize_matrix", "dequantize", "activation_objective",
     "accumulate_stats", "hessian_bf16", "gptq_order", "gptq_quantize", "gptq_factor",
-    "quantize_layer", "quantize_layer_x", "pack_uniform", "unpack_uniform",
+    "quantize_layer", "quantize_layer_x", "LayerOutputs", "pack_uniform", "unpack_uniform",
     "uniform_storage_bytes", "storage_bytes", "quant_group_count", "lib", "context",
 ]
 
@@ -189,6 +189,7 @@ _SIGS = {
     "ocwg_set_precision": (C.c_int, [_P, C.c_int]),
     "ocwg_synchronize": (C.c_int, [_P]),
     "ocwg_set_async": (C.c_int, [_P, C.c_int]),
+    "ocwg_debug_factor_bench": (C.c_int, [_P, C.c_int, _P, _P]),
     "ocwg_qep_target": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.c_double, C.c_double, _P]),
     "ocwg_validate_config": (C.c_int, [C.POINTER(_QCfg)]),
     "ocwg_group_count": (_U64, [C.POINTER(_QCfg), _U64, _U64]),
@@ -492,26 +493,40 @@ def quantize_layer(w, stats: CalibStats, opts: LayerQuantOptions, device: int = 
                          device=device)
 
 
+class LayerOutputs:
+    """Caller-owned host buffers for quantize_layer_x (e.g. views of pinned
+    memory, so the device-to-host copies run at full PCIe rate)."""
+
+    def __init__(self, n: int, m: int, cfg: QuantConfig, alloc=np.zeros, with_h: bool = True):
+        ng = quant_group_count(cfg, n, m)
+        self.payload_bytes = uniform_storage_bytes(cfg, n, m)
+        self.codes = alloc((n, m), np.int16)
+        self.scales = alloc(ng, np.float32)
+        self.zeros = alloc(ng, np.int32)
+        self.w_hat = alloc((n, m), np.float32)
+        self.payload = alloc(max(self.payload_bytes, 1), np.uint8)
+        self.h = alloc((n, n), np.float32) if with_h else None
+
+
 def quantize_layer_x(w, x_bf16_bits, cfg: QuantConfig, opts: GptqOptions,
-                     mode: ScaleMode = ScaleMode.minmax, device: int = 0):
+                     mode: ScaleMode = ScaleMode.minmax, device: int = 0,
+                     out: LayerOutputs | None = None):
     """The north_star's one-call layer quantize from host buffers:
     W (N x M fp32) + calibration tokens X (T x N bf16 bits) ->
-    (QuantizedMatrix with w_hat, packed OCW1 payload bytes, H fp32)."""
+    (QuantizedMatrix with w_hat, packed OCW1 payload bytes, H fp32 or None).
+    X streams to the device in token chunks while the Hessian accumulates."""
     w = _f32(w)
     x = np.ascontiguousarray(x_bf16_bits, np.uint16)
     n, m = w.shape
     if x.shape[1] != n:
         raise InvalidInput("quantize_layer_x: X must be T x N with N = rows of W")
-    ng = quant_group_count(cfg, n, m)
-    pb = uniform_storage_bytes(cfg, n, m)
-    codes = np.zeros((n, m), np.int16)
-    s = np.zeros(ng, np.float32)
-    z = np.zeros(ng, np.int32)
-    wh = np.zeros((n, m), np.float32)
-    payload = np.zeros(max(pb, 1), np.uint8)
-    h = np.zeros((n, n), np.float32)
+    o_ = out if out is not None else LayerOutputs(n, m, cfg)
+    pb = o_.payload_bytes
+    codes, s, z, wh, payload, h = o_.codes, o_.scales, o_.zeros, o_.w_hat, o_.payload, o_.h
     c, o = cfg._c(), opts._c()
     _check(lib().ocwg_quantize_layer_x(context(device).handle, _ptr(w), _ptr(x), x.shape[0], n, m,
                                        C.byref(c), C.byref(o), int(mode), _ptr(codes), _ptr(s),
                                        _ptr(z), _ptr(wh), _ptr(payload), pb, _ptr(h)))
+    if out is not None:
+        return QuantizedMatrix(n, m, cfg, codes, s, z, wh), payload[:pb], h
     return QuantizedMatrix(n, m, cfg, codes, s, z, wh), payload[:pb].tobytes(), h

@@ -445,6 +445,20 @@ int ocwg_synchronize(ocwg_ctx* ctx) {
 
 uint64_t ocwg_launch_count(ocwg_ctx*) { return launches_issued(); }
 
+int ocwg_debug_factor_bench(ocwg_ctx* ctx, int iters, long long* cycles, float* l_out) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    Arena ar(ctx);
+    const size_t oc = ar.reserve(64), oo = ar.reserve(64 * 64 * 4);
+    ar.commit();
+    debug_factor_bench(iters, ar.at<long long>(oc), ar.at<float>(oo), ctx->stream);
+    d2h(cycles, ar.at<long long>(oc), 8 * 8, ctx);
+    d2h(l_out, ar.at<float>(oo), 64 * 64 * 4, ctx);
+    finish(ctx);
+  });
+}
+
 int ocwg_debug_gemm(ocwg_ctx* ctx, int precision, uint64_t m, uint64_t n, uint64_t k, double alpha,
                     const void* a, uint64_t lda, int ta, const void* b, uint64_t ldb, int tb,
                     double beta, void* c, uint64_t ldc, int lower_only, int reps, double* ms) {

@@ -207,7 +207,10 @@ struct CholSmem {
   T ps[TB * TB];
   T qs[TB * TB];
   T lt[TB][TB + 4];   // diag tile L_cc transposed (lt[j][c] = L[c][j]); also G staging
-  T col[2][TB];       // published column (diag elimination)
+  T col[2][TB];       // (unused)
+  T sf[TB][TB + 1];   // diagonal tile being factored
+  T wcol[2][72];      // warp elimination: published pivot column (shifted, + zero pad)
+  T lt32[32][40];     // warp elimination: L columns, shifted like wcol (for the solve)
   T rdiag[TB];
   int item;
   int ready;
@@ -244,6 +247,134 @@ __device__ void emit_g(const T (&t)[4][4], CholSmem<T>& sm, const T* diag, int r
       ghi[off] = g;
     }
   }
+}
+
+// Warp-synchronous right-looking Cholesky of a 32 x 32 block held one row per
+// lane (a[k] = A[lane][j0 + k], lower part used), written to out[lane][j0 + j].
+// The register array rotates as it is updated (a[0] is always the pivot
+// column).  Per pivot each lane publishes its pivot-column entry to shared
+// memory (one store + warp sync, double-buffered, zero-padded past 32) and
+// reads the others as broadcasts: no block barrier, no shuffles.
+// With WITH_B, each lane also carries row 32 + lane (b[k] = A[32 + lane][j0 + k])
+// through the same pivots: b ends as L21 = A21 L11^-T (written to out_b), off
+// the pivot chain.
+template <typename T, bool WITH_B>
+__device__ __forceinline__ bool warp_chol32(T (&a)[32], T (&b)[32], T* out_row, T* out_b,
+                                            T* rdiag, T (*wcol)[72], T (*lt32)[40] = nullptr) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+#pragma unroll 1
+  for (int j = 0; j < 32; ++j) {
+    // stored at lane + sh so that entry j+1 starts a 16-byte chunk: the 31
+    // entries a lane needs are 8 LDS.128 broadcasts
+    const int sh = (3 - j) & 3;
+    T* cb = wcol[j & 1];
+    cb[lane + sh] = a[0];
+    const T p = __shfl_sync(0xffffffffu, a[0], j);  // pivot off the shared-memory round trip
+    __syncwarp();
+    // the column entries first: their load latency overlaps the rsqrt chain
+    T v[32];
+    const T* nxt = cb + j + sh + 1;  // 16-byte aligned
+#pragma unroll
+    for (int k4 = 0; k4 < 32; k4 += 4) {
+      T v4[4];
+      ld4(nxt + k4, v4);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[k4 + e] = v4[e];
+    }
+    ok &= (p > T(0));
+    const T rs = rsqrt_nr(p);
+    const T l = a[0] * rs;  // L[lane][j]; lane j: sqrt(p)
+    const T lrs = l * rs;   // a[k] -= L[lane][j] L[j+k][j] = lrs * a_{j+k}[j]
+#pragma unroll
+    for (int k = 0; k + 1 < 32; ++k) a[k] = fma(-lrs, v[k], a[k + 1]);
+    a[31] = T(0);
+    const T lo = lane >= j ? l : T(0);
+    out_row[j] = lo;
+    if (lt32) lt32[j][lane + sh] = lo;  // column j of L, shifted like cb (for the solve)
+    if (lane == j) rdiag[j] = rs;  // 1 / L[j][j]
+    if (WITH_B) {
+      const T lb = b[0] * rs;  // L21[lane][j]
+      const T lbrs = lb * rs;
+#pragma unroll
+      for (int k = 0; k + 1 < 32; ++k) b[k] = fma(-lbrs, v[k], b[k + 1]);
+      b[31] = T(0);
+      out_b[j] = lb;
+    }
+  }
+  return ok;
+}
+
+// Factor the 64 x 64 tile in sm.sf (lower, padded with identity) in place:
+// L11 = chol(A11) and L21 = A21 L11^-T by warp 0, A22 -= L21 L21^T by the
+// CTA, L22 = chol(A22) by warp 0.  Upper entries are zeroed; sm.rdiag gets
+// 1 / L[j][j].  All threads call.
+template <typename T>
+__device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  bool ok = true;
+  auto pstamp = [&](int i) {
+    if (prof && tid == 0) prof[i] = clock64();
+  };
+  pstamp(0);
+  for (int e = tid; e < 2 * 72; e += CT) sm.wcol[e / 72][e % 72] = T(0);
+  for (int e = tid; e < 32 * 40; e += CT) sm.lt32[e / 40][e % 40] = T(0);
+  __syncthreads();
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    const int o = 32 * h;  // diagonal block [o, o+32)
+    if (warp == 0) {
+      T av[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) av[k] = sm.sf[o + lane][o + k];
+      ok &= warp_chol32<T, false>(av, av, &sm.sf[o + lane][o], nullptr, &sm.rdiag[o], sm.wcol,
+                                  sm.lt32);
+      pstamp(1 + 3 * h);
+      if (h == 0) {
+        __syncwarp();
+        // L21: rows 32 + lane solve x L11^T = a (forward substitution, rotating)
+#pragma unroll
+        for (int k = 0; k < 32; ++k) av[k] = sm.sf[32 + lane][k];
+#pragma unroll 1
+        for (int j = 0; j < 32; ++j) {
+          T v[32];
+          const T* lcol = &sm.lt32[j][j + ((3 - j) & 3) + 1];  // L11[j+1..][j], aligned
+#pragma unroll
+          for (int k4 = 0; k4 < 32; k4 += 4) {
+            T v4[4];
+            ld4(lcol + k4, v4);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[k4 + e] = v4[e];
+          }
+          const T x = av[0] * sm.rdiag[j];
+#pragma unroll
+          for (int k = 0; k + 1 < 32; ++k) av[k] = fma(-x, v[k], av[k + 1]);
+          av[31] = T(0);
+          sm.sf[32 + lane][j] = x;
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) sm.sf[lane][32 + k] = T(0);
+        pstamp(2);
+      }
+    }
+    __syncthreads();
+    if (h == 0) {  // A22 -= L21 L21^T: thread -> row i, 4 columns
+      const int i = tid >> 3, j0 = (tid & 7) * 4;
+      T s4[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const T li = sm.sf[32 + i][k];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) s4[jj] = fma(li, sm.sf[32 + j0 + jj][k], s4[jj]);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+        if (j0 + jj <= i) sm.sf[32 + i][32 + j0 + jj] -= s4[jj];
+      __syncthreads();
+      pstamp(3);
+    }
+  }
+  return ok;
 }
 
 template <typename T>
@@ -348,53 +479,18 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
 
     stamp(item_id, 3);
     if (r == c) {
-      // ---- diagonal tile: right-looking elimination, one barrier per step.
-      // Unscaled column u[.] = a[.][j] is published; a[r][c] -= u_r u_c / u_j.
-      // Lanes whose 4 columns all lie right of pivot group j0 update all 16
-      // entries, the pivot-owning lanes the columns right of j (upper-triangle
-      // entries take garbage and are zeroed afterwards).
-      bool bad = false;
-#pragma unroll 1
-      for (int j0 = 0; j0 < TB; j0 += 4) {
-        const bool own = tx == (j0 >> 2), later = tx > (j0 >> 2);
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int j = j0 + jj, buf = j & 1;
-          if (own) st4(&sm.col[buf][4 * ty], t[0][jj], t[1][jj], t[2][jj], t[3][jj]);
-          __syncthreads();
-          const T p = sm.col[buf][j];
-          bad |= !(p > T(0));
-          const T rp = rcp_nr(p);
-          const T rsq = rsqrt_nr(p);
-          T cr[4], cc[4];
-          ld4(&sm.col[buf][4 * ty], cr);
-          ld4(&sm.col[buf][4 * tx], cc);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const T cru = cr[u] * rp;
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              if (later || (own && v > jj)) t[u][v] = fma(-cru, cc[v], t[u][v]);
-          }
-          if (own) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int rr = 4 * ty + u;
-              if (rr > j) t[u][jj] = cr[u] * rsq;
-              else if (rr == j) t[u][jj] = p * rsq;
-            }
-          }
-        }
-      }
-      if (bad && tid == 0 && cols > 0) {
-        // only pivots of real (non-padding) columns count (padding is exactly 1)
-        atomicOr(status, kFlagNotPD);
-      }
+      // ---- diagonal tile: warp-level factorisation in shared memory (factor_tile64)
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v)
-          if (4 * tx + v > 4 * ty + u) t[u][v] = T(0);
+        for (int v = 0; v < 4; ++v) sm.sf[4 * ty + u][4 * tx + v] = t[u][v];
+      __syncthreads();
+      const bool ok = factor_tile64(sm);
+      if (!ok && tid == 0 && cols > 0) atomicOr(status, kFlagNotPD);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) t[u][v] = sm.sf[4 * ty + u][4 * tx + v];
       // diag values for G scaling
       if (tx == ty) {
 #pragma unroll
@@ -556,7 +652,42 @@ int num_sms_f() {
   return v;
 }
 
+// Micro-benchmark (debug): one CTA factors a well-conditioned 64 x 64 tile
+// `iters` times; cycles[0] = total clocks, cycles[1] = clocks of the last
+// factor_tile64 call, out = L (64 x 64) for a correctness check.
+template <typename T>
+__global__ void __launch_bounds__(CT, 1) factor_bench_kernel(int iters, long long* cycles, T* out) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  CholSmem<T>& sm = *reinterpret_cast<CholSmem<T>*>(smraw);
+  const int tid = threadIdx.x;
+  long long t_last = 0;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    for (int e = tid; e < TB * TB; e += CT) {
+      const int r = e >> 6, c = e & 63;
+      sm.sf[r][c] = r == c ? T(64 + r) : T(1) / T(1 + r + c);
+    }
+    __syncthreads();
+    const long long t1 = clock64();
+    factor_tile64(sm, cycles + 2);
+    t_last = clock64() - t1;
+  }
+  const long long t2 = clock64();
+  if (tid == 0) {
+    cycles[0] = t2 - t0;
+    cycles[1] = t_last;
+  }
+  for (int e = tid; e < TB * TB; e += CT) out[e] = sm.sf[e >> 6][e & 63];
+}
+
 }  // namespace
+
+void debug_factor_bench(int iters, long long* cycles, float* out, cudaStream_t st) {
+  cudaFuncSetAttribute(factor_bench_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(CholSmem<float>)));
+  count_launches(1);
+  factor_bench_kernel<float><<<1, CT, sizeof(CholSmem<float>), st>>>(iters, cycles, out);
+}
 
 size_t cholesky_flag_ints(long long n) {
   const long long nt = (n + TB - 1) / TB;

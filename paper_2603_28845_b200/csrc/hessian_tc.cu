@@ -268,8 +268,32 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const long long row = (long long)bi * TM + q * 32 + lane;
       const bool first = split == 0 && !accumulate, last = split == splits - 1;
+      // running partial of this lane's row, one 32-column chunk ahead (loads in flight
+      // while the current chunk is added and stored)
+      auto load_chunk = [&](int c0, float (&v)[32]) {
+        const long long col0 = (long long)bj * TN + c0;
+        const float* hrow = h + row * dim + col0;
+        if (first || row >= dim || col0 + 31 < (long long)bi * TM) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = 0.f;
+        } else if (col0 + 32 <= dim) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float4 o = __ldcg(reinterpret_cast<const float4*>(hrow) + e);
+            v[4 * e] = o.x, v[4 * e + 1] = o.y, v[4 * e + 2] = o.z, v[4 * e + 3] = o.w;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = col0 + e < dim ? __ldcg(hrow + e) : 0.f;
+        }
+      };
+      float v[32], nv[32];
+      load_chunk(0, nv);
 #pragma unroll 1
       for (int c0 = 0; c0 < TN; c0 += 32) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = nv[e];
+        if (c0 + 32 < TN) load_chunk(c0 + 32, nv);
         uint32_t r[32];
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * TN + c0;
         asm volatile(
@@ -285,26 +309,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const long long col0 = (long long)bj * TN + c0;
         if (col0 + 31 < (long long)bi * TM) continue;  // chunk entirely below the diagonal
-        float v[32];
         if (row < dim) {
           float* hrow = h + row * dim + col0;
-          const bool full = col0 + 32 <= dim;
-          if (full && !first) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float4 o = __ldcg(reinterpret_cast<const float4*>(hrow) + e);
-              v[4 * e] = o.x, v[4 * e + 1] = o.y, v[4 * e + 2] = o.z, v[4 * e + 3] = o.w;
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = (!first && col0 + e < dim) ? __ldcg(hrow + e) : 0.f;
-          }
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] += __uint_as_float(r[e]);
           // upper entries (row <= col) accumulate; the lower half is the mirror
+          if (col0 >= row && col0 + 32 <= dim) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (col0 + e < dim && col0 + e >= row) hrow[e] = v[e];
+            for (int e = 0; e < 8; ++e)
+              reinterpret_cast<float4*>(hrow)[e] =
+                  make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (col0 + e < dim && col0 + e >= row) hrow[e] = v[e];
+          }
         }
         if (last) {
           // mirror: H[col][row] = H[row][col] for col > row (coalesced along rows)

@@ -147,6 +147,9 @@ void qep_target_f64(const float* w, const double* gram, const double* cross, lon
                     long long m, double alpha, double eta, float* out, double* ws, int* flags,
                     unsigned* status, cudaStream_t st);
 
+// ---- debug micro-benchmarks -------------------------------------------------
+void debug_factor_bench(int iters, long long* cycles, float* out, cudaStream_t st);
+
 // ---- misc ----------------------------------------------------------------
 void launch_f64_to_f32(const double* in, long long n, float* out, cudaStream_t st);
 void launch_f32_to_f64(const float* in, long long n, double* out, cudaStream_t st);

@@ -282,6 +282,7 @@ struct Smem {
   float ds[kCols4][kB + 1];
   long long orow[kB];
   int og[kB];
+  long long jg[kCols4];  // column group index (per-group granularity)
 };
 
 __global__ void __launch_bounds__(64) inblock4_kernel(
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
     sm.og[e] = o;
     sm.orow[e] = (long long)o * ldo;
   }
+  if (tid < kCols4) sm.jg[tid] = c.gran == 2 ? (j0 + tid) / c.group : 0;
   __syncthreads();
   for (int e = tid; e < kB * kCols4; e += 64) {
     const int li = e / kCols4, cl = e % kCols4;
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
     float4* v = &sm.tab[li][cl];
     if (li < bsz && jj < m) {
       const long long orig = sm.og[li];
-      const long long g = group_of(c, orig, jj);
+      const long long g = c.gran == 0 ? 0 : (c.gran == 1 ? orig : orig * c.gpr + sm.jg[cl]);
       cp_async(&v->x, w + orig * ldw + jj);
       cp_async(&v->y, scales + g);
       cp_async(reinterpret_cast<int*>(&v->w), zeros + g);

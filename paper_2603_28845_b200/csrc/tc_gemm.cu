@@ -230,17 +230,43 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {  // ============ epilogue: C = beta C + alpha D
     const int q = warp & 3;
     int local = 0;
+    const bool vec_ld = ((ldc & 3) == 0);
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int tm, tn;
       tile_of(t, tm, tn);
       if (lower_only && (long long)tn * TN > (long long)tm * TM + TM - 1) continue;
       const uint32_t acc = uint32_t(local & 1), use = uint32_t(local >> 1);
       ++local;
+      const long long row = (long long)tm * TM + q * 32 + lane;
+      float* cbase = c + (long long)(t / per_batch) * sc + row * ldc + (long long)tn * TN;
+      // C does not depend on the MMA: its first chunk is read before the
+      // accumulator is ready, and each next chunk while the current one is stored
+      auto load_c = [&](int c0, float (&v)[32]) {
+        const long long col0 = (long long)tn * TN + c0;
+        float* crow = cbase + c0;
+        if (beta == 0.f || row >= m) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = 0.f;
+        } else if (vec_ld && col0 + 32 <= n && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0)) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float4 o = reinterpret_cast<const float4*>(crow)[e];
+            v[4 * e] = o.x, v[4 * e + 1] = o.y, v[4 * e + 2] = o.z, v[4 * e + 3] = o.w;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = col0 + e < n ? crow[e] : 0.f;
+        }
+      };
+      float cv[32], nv[32];
+      load_c(0, nv);
       mbar_wait(smem_u32(&tfull_bar[acc]), use & 1u);
       tc_fence_after();
-      const long long row = (long long)tm * TM + q * 32 + lane;
 #pragma unroll 1
       for (int c0 = 0; c0 < TN; c0 += 32) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) cv[e] = nv[e];
+        if (c0 + 32 < TN) load_c(c0 + 32, nv);
         uint32_t r[32];
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + acc * TN + c0;
         asm volatile(
@@ -256,27 +282,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const long long col0 = (long long)tn * TN + c0;
         if (row < m) {
-          float* crow = c + (long long)(t / per_batch) * sc + row * ldc + col0;
-          const bool vec = (col0 + 32 <= n) && ((ldc & 3) == 0) &&
-                           ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
-          if (vec) {
+          float* crow = cbase + c0;
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (beta != 0.f) cv = reinterpret_cast<float4*>(crow)[v];
-              cv.x = fmaf(alpha, __uint_as_float(r[4 * v + 0]), beta * cv.x);
-              cv.y = fmaf(alpha, __uint_as_float(r[4 * v + 1]), beta * cv.y);
-              cv.z = fmaf(alpha, __uint_as_float(r[4 * v + 2]), beta * cv.z);
-              cv.w = fmaf(alpha, __uint_as_float(r[4 * v + 3]), beta * cv.w);
-              reinterpret_cast<float4*>(crow)[v] = cv;
-            }
+          for (int e = 0; e < 32; ++e) cv[e] = fmaf(alpha, __uint_as_float(r[e]), beta * cv[e]);
+          if (vec_ld && col0 + 32 <= n && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0)) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              reinterpret_cast<float4*>(crow)[e] =
+                  make_float4(cv[4 * e], cv[4 * e + 1], cv[4 * e + 2], cv[4 * e + 3]);
           } else {
 #pragma unroll
-            for (int v = 0; v < 32; ++v)
-              if (col0 + v < n) {
-                const float old = beta != 0.f ? crow[v] : 0.f;
-                crow[v] = fmaf(alpha, __uint_as_float(r[v]), beta * old);
-              }
+            for (int e = 0; e < 32; ++e)
+              if (col0 + e < n) crow[e] = cv[e];
           }
         }
       }

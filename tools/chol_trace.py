@@ -1,32 +1,24 @@
-"""Analyse OCWG_CHOL_TRACE output (per item: r, c, start, k-loop done, solve done,
-published; globaltimer ns)."""
+"""Analyse OCWG_CHOL_TRACE output (10 u64 per item: row, col, start, k-loop
+done, diag published, sub published, diag k-step done, factor done,
+sub k-step done, sub solved; globaltimer ns; pair items have row == col)."""
 import sys
 
 import numpy as np
 
-d = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 6).astype(np.int64)
-t0 = d[:, 2].min()
+d = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 10).astype(np.int64)
+t0 = d[:, 2][d[:, 2] > 0].min()
 r, c = d[:, 0], d[:, 1]
-st, kl, sv, pb = (d[:, i] - t0 for i in range(2, 6))
-print(f"items {len(d)}  span {pb.max() / 1e3:.1f} us")
+T = {k: d[:, i] - t0 for k, i in
+     [("st", 2), ("kl", 3), ("dpub", 4), ("spub", 5), ("dk", 6), ("fac", 7), ("sk", 8), ("sol", 9)]}
 nt = int(c.max()) + 1
-print(" col   diag:start  kdone  solved  publ | sub(c+1,c): start kdone  publ | diag factor us")
-for col in list(range(0, 6)) + list(range(nt // 2, nt // 2 + 3)) + list(range(nt - 4, nt)):
-    i = np.where((r == col) & (c == col))[0][0]
-    line = f"{col:4d} {st[i]/1e3:10.1f} {kl[i]/1e3:7.1f} {sv[i]/1e3:7.1f} {pb[i]/1e3:7.1f} |"
-    s = np.where((r == col + 1) & (c == col))[0]
-    if len(s):
-        s = s[0]
-        line += f" {st[s]/1e3:8.1f} {kl[s]/1e3:7.1f} {pb[s]/1e3:7.1f} |"
-    line += f" {(sv[i]-kl[i])/1e3:6.2f}"
-    print(line)
-diag = np.array([np.where((r == k) & (c == k))[0][0] for k in range(nt)])
-gaps = np.diff(pb[diag])
-print("diag publish interval us: mean %.2f  median %.2f  max %.2f" % (gaps.mean() / 1e3, np.median(gaps) / 1e3, gaps.max() / 1e3))
-fac = (sv[diag] - kl[diag]) / 1e3
-print("diag factor us: mean %.2f" % fac.mean())
-sub = [np.where((r == k + 1) & (c == k))[0][0] for k in range(nt - 1)]
-sub = np.array(sub)
-print("sub solve us (publ - kdone): mean %.2f" % ((pb[sub] - kl[sub]) / 1e3).mean())
-print("diag(c+1) kdone - sub(c+1,c) publ us: mean %.2f" % ((kl[diag[1:]] - pb[sub]) / 1e3).mean())
-print("sub(c+1,c) kdone - diag(c) publ us: mean %.2f" % ((kl[sub] - pb[diag[:-1]]) / 1e3).mean())
+pair = np.array([np.where((r == k) & (c == k))[0][0] for k in range(nt)])
+print(f"items {len(d)}  span {T['spub'].max() / 1e3:.1f} us")
+P = {k: v[pair] for k, v in T.items()}
+seg = [("wait+diag k-step", P["dk"] - P["kl"]), ("factor", P["fac"] - P["dk"]),
+       ("publish diag", P["dpub"] - P["fac"]), ("wait+sub k-step", P["sk"] - P["dpub"]),
+       ("solve", P["sol"] - P["sk"]), ("publish sub", P["spub"] - P["sol"])]
+for name, v in seg:
+    v = v[:-1]
+    print(f"  {name:18s} mean {v.mean() / 1e3:7.2f} us  median {np.median(v) / 1e3:7.2f}")
+gap = (P["dk"][1:] - P["spub"][:-1]) / 1e3
+print(f"  next diag k-step done - sub publish: mean {gap.mean():.2f} us; interval {np.diff(P['spub']).mean() / 1e3:.2f} us")
