@@ -417,14 +417,26 @@ int num_sms() {
 
 }  // namespace
 
+bool use_pairs() {
+  static const bool on = [] {
+    const char* e = getenv("OCWG_HESSIAN_2CTA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 size_t hessian_tc_workspace_bytes(long long tokens, long long dim) {
   const Plan p = make_plan(tokens, dim, num_sms());
-  return size_t(p.ntiles) * sizeof(int) + 256;
+  return std::max(size_t(p.ntiles) * sizeof(int) + 256, hessian_tc2_workspace_bytes(tokens, dim));
 }
 
 // returns 0 ok, -1 unsupported shape (caller must use another kernel), >0 cuda error
 int hessian_tc(const uint16_t* x, long long tokens, long long dim, float* h, int accumulate,
                void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (use_pairs()) {
+    const int r = hessian_tc2(x, tokens, dim, h, accumulate, ws, ws_bytes, st);
+    if (r != -1) return r;  // -1: shape unsupported by the pair kernel -> single-CTA kernel
+  }
   if (dim % 8 != 0 || dim <= 0 || tokens <= 0 || tokens > (1LL << 31) || dim > (1LL << 31))
     return -1;
   EncodeTiled enc = get_encoder();

@@ -131,6 +131,10 @@ void accumulate_stats_f64(const float* x_fp, const float* x_pert, long long rows
 // bf16 X (tokens x dim, row-major) -> H (dim x dim fp32, symmetric, full).
 // accumulate: H += X^T X else H = X^T X.  tcgen05/TMEM/TMA kernel.
 size_t hessian_tc_workspace_bytes(long long tokens, long long dim);
+// CTA-pair variant (hessian_tc2.cu), used by hessian_tc unless OCWG_HESSIAN_2CTA=0
+size_t hessian_tc2_workspace_bytes(long long tokens, long long dim);
+int hessian_tc2(const uint16_t* x, long long tokens, long long dim, float* h, int accumulate,
+                void* ws, size_t ws_bytes, cudaStream_t st);
 int hessian_tc(const uint16_t* x, long long tokens, long long dim, float* h, int accumulate,
                void* ws, size_t ws_bytes, cudaStream_t st);
 // SIMT cross-check kernel (same contract), used by tests to validate hessian_tc.

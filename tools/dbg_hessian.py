@@ -1,4 +1,5 @@
-"""Debug: tcgen05 Hessian repeated calls; which calls leave H untouched."""
+"""tcgen05 Hessian (pair kernel by default) vs an fp64 reference: symmetry,
+relative error (|dH| / sqrt(Hii Hjj)), accumulate mode, and kernel time."""
 import sys
 from pathlib import Path
 
@@ -6,19 +7,30 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import torch
 
 import paper_2603_28845_b200 as g
-
-lib = g.lib()
 from paper_2603_28845_b200 import dev
+
 dev._bind_stream(0)
-cases = [(512, 65536), (512, 65536), (4096, 262144), (4096, 262144), (512, 65536), (2048, 131072),
-         (4096, 262080), (4096, 262144)]
-for dim, tok in cases:
-    torch.manual_seed(0)
+for dim, tok, acc in [(512, 65536, 0), (1000, 20000, 0), (4096, 262144, 0), (2048, 131072, 1)]:
+    torch.manual_seed(dim)
     x = torch.randn(tok, dim, device="cuda").to(torch.bfloat16)
-    h = torch.full((dim, dim), -7.0, device="cuda")
-    rc = lib.ocwg_debug_hessian_dev(g.context().handle, x.data_ptr(), tok, dim, h.data_ptr(), 0, 0)
+    ref = torch.zeros(dim, dim, device="cuda", dtype=torch.float64)
+    for t0 in range(0, tok, 16384):
+        xc = x[t0:t0 + 16384].double()
+        ref += xc.T @ xc
+    h = torch.zeros(dim, dim, device="cuda")
+    if acc:
+        h += 3.0
+        ref += 3.0
+    dev.hessian(x, h, accumulate=bool(acc))
     torch.cuda.synchronize()
-    diag = torch.diag(h)
-    ref = (x.float() ** 2).sum(0)
-    print(dim, tok, "rc", rc, "untouched", int((h == -7.0).sum()), "diag relerr",
-          float(((diag - ref).abs() / ref).max()), flush=True)
+    d = torch.sqrt(torch.outer(torch.diag(ref), torch.diag(ref)))
+    err = float(((h.double() - ref).abs() / d).max())
+    asym = int((h != h.T).sum())
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(3):
+        dev.hessian(x, h)
+    ev[1].record()
+    torch.cuda.synchronize()
+    print(f"dim {dim} tok {tok} acc {acc}: max rel err {err:.2e} asym {asym} "
+          f"time {ev[0].elapsed_time(ev[1]) / 3:.3f} ms", flush=True)
