@@ -210,6 +210,9 @@ int ocwg_debug_gemm(ocwg_ctx* ctx, int precision, uint64_t m, uint64_t n, uint64
  * cycles[0] = total clocks over `iters` runs, cycles[1] = clocks of the last;
  * l_out (64 x 64 fp32) = the factor, for a check. */
 int ocwg_debug_factor_bench(ocwg_ctx* ctx, int iters, long long* cycles, float* l_out);
+/* Phase timestamps (globaltimer ns, 8 per CTA) of the in-block sweep launch
+ * whose first row equals $OCWG_SWEEP_TRACE_IB; returns the count copied. */
+int ocwg_debug_sweep_trace(ocwg_ctx* ctx, unsigned long long* out, int cap);
 /* Number of kernels this library launched on the context so far. */
 uint64_t ocwg_launch_count(ocwg_ctx* ctx);
 

@@ -190,6 +190,7 @@ _SIGS = {
     "ocwg_synchronize": (C.c_int, [_P]),
     "ocwg_set_async": (C.c_int, [_P, C.c_int]),
     "ocwg_debug_factor_bench": (C.c_int, [_P, C.c_int, _P, _P]),
+    "ocwg_debug_sweep_trace": (C.c_int, [_P, _P, C.c_int]),
     "ocwg_qep_target": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.c_double, C.c_double, _P]),
     "ocwg_validate_config": (C.c_int, [C.POINTER(_QCfg)]),
     "ocwg_group_count": (_U64, [C.POINTER(_QCfg), _U64, _U64]),

@@ -459,6 +459,12 @@ int ocwg_debug_factor_bench(ocwg_ctx* ctx, int iters, long long* cycles, float* 
   });
 }
 
+int ocwg_debug_sweep_trace(ocwg_ctx* ctx, unsigned long long* out, int cap) {
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  cudaDeviceSynchronize();
+  return debug_sweep_trace(out, cap);
+}
+
 int ocwg_debug_gemm(ocwg_ctx* ctx, int precision, uint64_t m, uint64_t n, uint64_t k, double alpha,
                     const void* a, uint64_t lda, int ta, const void* b, uint64_t ldb, int tb,
                     double beta, void* c, uint64_t ldc, int lower_only, int reps, double* ms) {

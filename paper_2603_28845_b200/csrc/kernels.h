@@ -153,6 +153,7 @@ void qep_target_f64(const float* w, const double* gram, const double* cross, lon
 
 // ---- debug micro-benchmarks -------------------------------------------------
 void debug_factor_bench(int iters, long long* cycles, float* out, cudaStream_t st);
+int debug_sweep_trace(unsigned long long* out, int cap);
 
 // ---- misc ----------------------------------------------------------------
 void launch_f64_to_f32(const double* in, long long n, float* out, cudaStream_t st);

@@ -28,6 +28,8 @@
 // every register index is a compile-time constant; D is broadcast with one
 // warp shuffle.  The block's strictly-lower G is staged packed in shared
 // memory; D is staged for a coalesced K-major store (the GEMM's B operand).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace ocwg {
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
     const T* __restrict__ dprev, int bprev, T* __restrict__ dcur, float* __restrict__ dcur_hi,
     float* __restrict__ dcur_lo, QCfg c, const float* __restrict__ scales,
     const int32_t* __restrict__ zeros, long long n, long long m, long long ib, int bsz,
-    int16_t* __restrict__ codes, float* __restrict__ w_hat, long long ldo) {
+    int16_t* __restrict__ codes, float* __restrict__ w_hat, long long ldo, long long ldd) {
   static_assert(RPT % 4 == 0 && RPT <= kRg, "row slots");
   extern __shared__ __align__(16) unsigned char smraw[];
   InblockSmem<T>& sm = *reinterpret_cast<InblockSmem<T>*>(smraw);
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
       for (int e = tid; e < kCols * kLaChunk; e += 256) {
         const int cl = e / kLaChunk, q = e % kLaChunk;
         if (j0 + cl < m && q0 + q < bprev)
-          cp_async(&sm.u.la.dp[cl][q], dprev + (j0 + cl) * kB + q0 + q);
+          cp_async(&sm.u.la.dp[cl][q], dprev + (j0 + cl) * ldd + q0 + q);
         else
           sm.u.la.dp[cl][q] = T(0);
       }
@@ -243,9 +245,9 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
   // hi/lo split the tensor-core GEMM consumes
   for (int e = tid; e < kCols * kB; e += 256) {
     const int cl = e / kB, li = e % kB;
-    if (j0 + cl >= m) continue;
-    const T v = li < bsz ? sm.ds[cl][li] : T(0);
-    const long long off = (j0 + cl) * kB + li;
+    if (j0 + cl >= m || li >= bsz) continue;
+    const T v = sm.ds[cl][li];
+    const long long off = (j0 + cl) * ldd + li;
     dcur[off] = v;
     if (dcur_hi) {
       const float hi = tf32_hi(float(v));
@@ -279,21 +281,34 @@ struct Smem {
     } la;
   } u;
   float4 tab[kB][kCols4];  // {w, s, 1/s, z} of (row li, column cj)
-  float ds[kCols4][kB + 1];
+  float ds[kCols4][kB + 1];  // D = w - w_hat of (column, row)
+  int16_t cs[kCols4][kB + 2];  // codes of (column, row)
   long long orow[kB];
   int og[kB];
   long long jg[kCols4];  // column group index (per-group granularity)
 };
 
-__global__ void __launch_bounds__(64) inblock4_kernel(
+// phase timestamps (globaltimer ns) of one traced launch, per CTA
+__device__ unsigned long long g_trace[1024 * 8];
+__device__ __forceinline__ void stamp(int trace, int i) {
+  if (trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_trace[blockIdx.x * 8 + i] = t;
+  }
+}
+
+__global__ void __launch_bounds__(64, 1) inblock4_kernel(
     const float* __restrict__ w, long long ldw, const int32_t* __restrict__ order,
     const float* __restrict__ acc, int use_acc, const float* __restrict__ gpl,
     const float* __restrict__ gpb, const float* __restrict__ dprev, int bprev,
     float* __restrict__ dcur, float* __restrict__ dcur_hi, float* __restrict__ dcur_lo, QCfg c,
     const float* __restrict__ scales, const int32_t* __restrict__ zeros, long long n, long long m,
-    long long ib, int bsz, int16_t* __restrict__ codes, float* __restrict__ w_hat, long long ldo) {
+    long long ib, int bsz, int16_t* __restrict__ codes, float* __restrict__ w_hat, long long ldo,
+    long long ldd, int trace) {
   extern __shared__ __align__(16) unsigned char smraw[];
   Smem& sm = *reinterpret_cast<Smem*>(smraw);
+  stamp(trace, 0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cc = lane & 7, rg = lane >> 3;
   const int cj = warp * kCpw + cc;
@@ -331,6 +346,7 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
     const int li = rg + 4 * k;
     r[k] = (use_acc && col_ok && li < bsz) ? acc[(ib + li) * m + j] : 0.f;
   }
+  stamp(trace, 1);
   // ---- lookahead: r += G[blk, prev blk] D_prev (16-byte staging)
   if (bprev > 0) {
     const long long kprev = ib - bprev;
@@ -347,7 +363,7 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
         const int cl = e / (kLaChunk / 4), q = (e % (kLaChunk / 4)) * 4;
         float* dst = &sm.u.la.dp[cl][q];
         if (j0 + cl < m && q0 + q < bprev)
-          cp_async16(dst, dprev + (j0 + cl) * kB + q0 + q);
+          cp_async16(dst, dprev + (j0 + cl) * ldd + q0 + q);
         else
           *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -370,6 +386,7 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
       __syncthreads();
     }
   }
+  stamp(trace, 2);
   // ---- the block's rows of G^T (already in lane order): 16-byte copies
   for (int e = tid; e < kB * kB / 4; e += 64) {
     const int li = e / (kB / 4), q = (e % (kB / 4)) * 4;
@@ -388,10 +405,12 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
     v.w = float(__float_as_int(v.w));
   }
   __syncthreads();
+  stamp(trace, 3);
 
   const float qminf = float(c.qmin), qmaxf = float(c.qmax);
-  int16_t* code_col = codes + j;
-  float* wh_col = w_hat ? w_hat + j : nullptr;
+  // Rows li >= bsz of a short last block run as padding (w = 0, s = 1, z = 0,
+  // zero G rows): finite d that no real row picks up, never stored -- so the
+  // step loop has no per-row branch and the next row's loads hoist freely.
 #pragma unroll 1
   for (int T = 0; T < kRpt / 4; ++T) {
     if (16 * T >= bsz) break;
@@ -403,7 +422,7 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
 #pragma unroll
       for (int o = 0; o < kLpc; ++o) {
         const int li = 16 * T + 4 * tt + o;
-        if (li < bsz) {
+        {
           float g[kRpt];
           const float* gp = &sm.u.gt[li * kB];
 #pragma unroll
@@ -418,13 +437,9 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
           const float cf = quantize_code_f(div_rn_fast(x, tv.y, tv.z), tv.w, qminf, qmaxf);
           const float wh = __fmul_rn(tv.y, __fsub_rn(cf, tv.w));  // quant.cpp:33-35
           float d = __fsub_rn(tv.x, wh);
-          if (rg == o) {
-            if (col_ok) {
-              const long long orow = sm.orow[li];  // original row order (:75)
-              code_col[orow] = int16_t(int(cf));
-              if (wh_col) wh_col[orow] = wh;
-            }
+          if (rg == o) {  // stores leave with the epilogue
             sm.ds[cj][li] = d;
+            sm.cs[cj][li] = int16_t(int(cf));
           }
           d = __shfl_sync(0xffffffffu, d, cc + kCpw * o);
 #pragma unroll
@@ -436,11 +451,12 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
     for (int k = 0; k < kRpt; ++k) r[k] = k + 4 < kRpt ? r[k + 4] : 0.f;
   }
   __syncthreads();
+  stamp(trace, 4);
   for (int e = tid; e < kCols4 * kB; e += 64) {
     const int cl = e / kB, li = e % kB;
-    if (j0 + cl >= m) continue;
-    const float v = li < bsz ? sm.ds[cl][li] : 0.f;
-    const long long off = (j0 + cl) * kB + li;
+    if (j0 + cl >= m || li >= bsz) continue;
+    const float v = sm.ds[cl][li];
+    const long long off = (j0 + cl) * ldd + li;
     dcur[off] = v;
     if (dcur_hi) {
       const float hi = tf32_hi(v);
@@ -448,6 +464,20 @@ __global__ void __launch_bounds__(64) inblock4_kernel(
       dcur_lo[off] = v - hi;
     }
   }
+  // codes / W_hat in original row order (layerwise.cpp:75), row-contiguous
+  for (int e = tid; e < kB * kCols4; e += 64) {
+    const int li = e / kCols4, cl = e % kCols4;
+    if (li >= bsz || j0 + cl >= m) continue;
+    const int16_t q = sm.cs[cl][li];
+    const long long o = sm.orow[li] + j0 + cl;
+    codes[o] = q;
+    if (w_hat) {
+      const float4 tv = sm.tab[li][cl];
+      w_hat[o] = __fmul_rn(tv.y, __fsub_rn(float(q), tv.w));  // quant.cpp:33-35
+    }
+  }
+  __syncthreads();
+  stamp(trace, 5);
 }
 }  // namespace l4
 
@@ -455,7 +485,8 @@ void launch_inblock4(const float* w, long long ldw, const int32_t* order, const 
                      int use_acc, const float* gpl, const float* gtt, const float* dprev, int bprev,
                      float* dcur, float* dch, float* dcl, const QCfg& c, const float* scales,
                      const int32_t* zeros, long long n, long long m, long long ib, int bsz,
-                     int16_t* codes, float* w_hat, long long ldo, cudaStream_t st) {
+                     int16_t* codes, float* w_hat, long long ldo, long long ldd, int trace,
+                     cudaStream_t st) {
   static const bool attr = [] {
     cudaFuncSetAttribute(l4::inblock4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(l4::Smem)));
@@ -466,7 +497,8 @@ void launch_inblock4(const float* w, long long ldw, const int32_t* order, const 
   count_launches(1);
   l4::inblock4_kernel<<<ctas, 64, sizeof(l4::Smem), st>>>(w, ldw, order, acc, use_acc, gpl, gtt,
                                                           dprev, bprev, dcur, dch, dcl, c, scales,
-                                                          zeros, n, m, ib, bsz, codes, w_hat, ldo);
+                                                          zeros, n, m, ib, bsz, codes, w_hat, ldo,
+                                                          ldd, trace);
 }
 
 template <typename T, int RPT>
@@ -474,7 +506,7 @@ void launch_inblock(const float* w, long long ldw, const int32_t* order, const T
                     const T* gpl, const T* dprev, int bprev, T* dcur, float* dch, float* dcl,
                     const QCfg& c, const float* scales, const int32_t* zeros, long long n,
                     long long m, long long ib, int bsz, int16_t* codes, float* w_hat, long long ldo,
-                    cudaStream_t st) {
+                    long long ldd, cudaStream_t st) {
   static const bool attr = [] {
     cudaFuncSetAttribute(inblock_g_kernel<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(InblockSmem<T>)));
@@ -485,72 +517,97 @@ void launch_inblock(const float* w, long long ldw, const int32_t* order, const T
   count_launches(1);
   inblock_g_kernel<T, RPT><<<ctas, 256, sizeof(InblockSmem<T>), st>>>(
       w, ldw, order, acc, use_acc, gpl, dprev, bprev, dcur, dch, dcl, c, scales, zeros, n, m, ib,
-      bsz, codes, w_hat, ldo);
+      bsz, codes, w_hat, ldo, ldd);
 }
 
 }  // namespace
 
-size_t sweep_delta_elems(long long m) { return size_t(m) * kB; }
+constexpr long long kSuperRows = 512;  // rows of G D applied per trailing GEMM (K)
 
+size_t sweep_delta_elems(long long m) { return size_t(m) * kSuperRows; }
+
+// Two-level blocking: super-blocks of kSuperRows rows (4 blocks of 128).
+// In-block kernel b applies, by lookahead, every earlier block of its own
+// super-block (G[blk b, sb0:ib] D[sb0:ib]); one trailing GEMM per super-block
+// (K = kSuperRows) applies it to all later rows.  Accumulator traffic and
+// GEMM launches drop 4x against per-block trailing updates (which could not
+// overlap the in-block kernels anyway: they cannot share an SM).
 template <typename T>
 void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const T* gpl,
-                  const float* gtt, const T* ghi, const float* glo, const int32_t* order, const QCfg& c,
-                  const float* scales, const int32_t* zeros, long long block, int16_t* codes,
-                  float* w_hat, long long ldo, T* acc, T* const dpl[2], float* const dhi[2],
-                  float* const dlo[2], cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev) {
+                  const float* gtt, const T* ghi, const float* glo, const int32_t* order,
+                  const QCfg& c, const float* scales, const int32_t* zeros, long long block,
+                  int16_t* codes, float* w_hat, long long ldo, T* acc, T* const dpl[2],
+                  float* const dhi[2], float* const dlo[2], cudaStream_t st, cudaStream_t aux,
+                  cudaEvent_t* ev) {
+  (void)aux;
+  (void)ev;
   // block size is a pure re-association of the trailing update (SURVEY §0
   // item 11); blocks above 128 rows run as 128-row blocks.
   const long long B = block < 1 ? 1 : (block > kB ? kB : block);
-  const long long nb = (n + B - 1) / B;
+  const long long SB = std::max<long long>(1, kSuperRows / B);  // blocks per super-block
+  const long long SBK = SB * B;
   const bool split = glo != nullptr;
-  // ev: [0] fork, [1] in-block done, [2..3] trailing done (by block parity), [4] join
-  cudaEventRecord(ev[0], st);
-  cudaStreamWaitEvent(aux, ev[0], 0);
-  for (long long b = 0; b < nb; ++b) {
-    const long long ib = b * B, ie = std::min(n, ib + B);
-    const int bsz = int(ie - ib);
-    const int p = int(b & 1);
-    if (b >= 2) cudaStreamWaitEvent(st, ev[2 + p], 0);  // trailing(b-2) done
-    const int bprev = b > 0 ? int(B) : 0;
-    const T* dprev = b > 0 ? dpl[p ^ 1] : nullptr;
-    float* dch = split ? dhi[p] : nullptr;
-    float* dcl = split ? dlo[p] : nullptr;
-    if (B <= 32)
-      launch_inblock<T, 4>(w, ldw, order, acc, b >= 2, gpl, dprev, bprev, dpl[p], dch, dcl, c,
-                           scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, st);
-    else if (B <= 64)
-      launch_inblock<T, 8>(w, ldw, order, acc, b >= 2, gpl, dprev, bprev, dpl[p], dch, dcl, c,
-                           scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, st);
-    else if (sizeof(T) == 4 && gtt)
-      launch_inblock4(w, ldw, order, reinterpret_cast<const float*>(acc), b >= 2,
-                      reinterpret_cast<const float*>(gpl), gtt,
-                      reinterpret_cast<const float*>(dprev), bprev,
-                      reinterpret_cast<float*>(dpl[p]), dch, dcl, c, scales, zeros, n, m, ib, bsz,
-                      codes, w_hat, ldo, st);
-    else
-      launch_inblock<T, 16>(w, ldw, order, acc, b >= 2, gpl, dprev, bprev, dpl[p], dch, dcl, c,
-                            scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, st);
-    // trailing(b): rows [ie + next, n) -- block b+1 takes its slice by lookahead
-    const long long r0 = std::min(n, ie + B);
-    if (r0 < n) {
-      cudaEventRecord(ev[1], st);
-      cudaStreamWaitEvent(aux, ev[1], 0);
-      const double beta = b == 0 ? 0.0 : 1.0;
+  // debug timing switch (results invalid): OCWG_SWEEP_SKIP=inblock|gemm
+  static const long long trace_ib = [] {
+    const char* e = getenv("OCWG_SWEEP_TRACE_IB");
+    return e ? atoll(e) : -1LL;
+  }();
+  static const int skip = [] {
+    const char* e = getenv("OCWG_SWEEP_SKIP");
+    return !e ? 0 : (e[0] == 'i' ? 1 : (e[0] == 'g' ? 2 : 0));
+  }();
+  for (long long s0 = 0, si = 0; s0 < n; s0 += SBK, ++si) {
+    const long long se = std::min(n, s0 + SBK);
+    const int p = int(si & 1);
+    for (long long ib = s0; ib < se; ib += B) {
+      const int bsz = int(std::min(se, ib + B) - ib);
+      const int bprev = int(ib - s0);  // lookahead rows: this super-block's earlier blocks
+      const int use_acc = si >= 1;
+      T* dcur = dpl[p] + bprev;
+      float* dch = split ? dhi[p] + bprev : nullptr;
+      float* dcl = split ? dlo[p] + bprev : nullptr;
+      if (skip == 1)
+        ;
+      else if (B <= 32)
+        launch_inblock<T, 4>(w, ldw, order, acc, use_acc, gpl, dpl[p], bprev, dcur, dch, dcl, c,
+                             scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, kSuperRows, st);
+      else if (B <= 64)
+        launch_inblock<T, 8>(w, ldw, order, acc, use_acc, gpl, dpl[p], bprev, dcur, dch, dcl, c,
+                             scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, kSuperRows, st);
+      else if (sizeof(T) == 4 && gtt && B == kB)
+        launch_inblock4(w, ldw, order, reinterpret_cast<const float*>(acc), use_acc,
+                        reinterpret_cast<const float*>(gpl), gtt,
+                        reinterpret_cast<const float*>(dpl[p]), bprev,
+                        reinterpret_cast<float*>(dcur), dch, dcl, c, scales, zeros, n, m, ib, bsz,
+                        codes, w_hat, ldo, kSuperRows, ib == trace_ib, st);
+      else
+        launch_inblock<T, 16>(w, ldw, order, acc, use_acc, gpl, dpl[p], bprev, dcur, dch, dcl, c,
+                              scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, kSuperRows, st);
+    }
+    // trailing update of this super-block: acc[se:, :] (+)= G[se:, s0:se] D[s0:se, :]
+    if (se < n && skip != 2) {
+      const double beta = si == 0 ? 0.0 : 1.0;
+      const long long kk = se - s0;
       bool done = false;
       if constexpr (sizeof(T) == 4) {
         if (split)
-          done = tc_gemm_presplit(n - r0, m, bsz, 1.0f, reinterpret_cast<const float*>(ghi) + r0 * n + ib,
-                                  glo + r0 * n + ib, n, dhi[p], dlo[p], kB, float(beta),
-                                  reinterpret_cast<float*>(acc) + r0 * m, m, aux);
+          done = tc_gemm_presplit(n - se, m, kk, 1.0f,
+                                  reinterpret_cast<const float*>(ghi) + se * n + s0,
+                                  glo + se * n + s0, n, dhi[p], dlo[p], kSuperRows, float(beta),
+                                  reinterpret_cast<float*>(acc) + se * m, m, st);
       }
       if (!done)
-        gemm<T, T, T>(n - r0, m, bsz, 1.0, gpl + r0 * n + ib, n, false, dpl[p], kB, true, beta,
-                      acc + r0 * m, m, false, aux);
-      cudaEventRecord(ev[2 + p], aux);
+        gemm<T, T, T>(n - se, m, kk, 1.0, gpl + se * n + s0, n, false, dpl[p], kSuperRows, true,
+                      beta, acc + se * m, m, false, st);
     }
   }
-  cudaEventRecord(ev[4], aux);
-  cudaStreamWaitEvent(st, ev[4], 0);
+}
+
+int debug_sweep_trace(unsigned long long* out, int cap) {
+  const int k = std::min(cap, 1024 * 8);
+  return cudaMemcpyFromSymbol(out, l4::g_trace, sizeof(unsigned long long) * k) == cudaSuccess
+             ? k
+             : -1;
 }
 
 template void gptq_sweep_g<float>(const float*, long long, long long, long long, const float*,
