@@ -270,23 +270,30 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
 // distinct banks): 8 LDS.128 per row.  The owner's (w, s, 1/s, z) come from a
 // per-row table gathered once with cp.async.
 namespace l4 {
-constexpr int kLpc = 4, kRpt = 32, kCpw = 8, kWarps = 2, kCols4 = kCpw * kWarps;
+// 4 warps: warps 0-1 run the row chain of 16 columns (4 lanes per column,
+// lane (cc, rg) holds rows rg + 4k); warps 2-3 help with the prologue
+// (gather, acc, lookahead rows 64..127) and the epilogue, and idle at a
+// barrier during the chain.
+constexpr int kLpc = 4, kRpt = 32, kCpw = 8, kCols4 = 16, kThreads = 128;
+constexpr int kLa4 = 32;      // lookahead K chunk (double-buffered)
+constexpr int kGtEarly = 88;  // G rows >= this are staged before the lookahead
 
 struct Smem {
   union {
     float gt[kB * kB + 32];  // block rows of G^T in lane order (+ pad for dead slots)
     struct {
-      float gc[kB][kLaChunk + 4];
-      float dp[kCols4][kLaChunk + 4];
+      float gc[2][kB][kLa4 + 4];
+      float dp[2][kCols4][kLa4 + 4];
     } la;
   } u;
   float4 tab[kB][kCols4];  // {w, s, 1/s, z} of (row li, column cj)
-  float ds[kCols4][kB + 1];  // D = w - w_hat of (column, row)
+  float ds[kCols4][kB + 1];  // D = w - w_hat of (column, row); lookahead hand-off first
   int16_t cs[kCols4][kB + 2];  // codes of (column, row)
   long long orow[kB];
   int og[kB];
-  long long jg[kCols4];  // column group index (per-group granularity)
+  int role[4];
 };
+static_assert(sizeof(((Smem*)0)->u.la) <= kGtEarly * kB * sizeof(float), "early G rows overlap");
 
 // phase timestamps (globaltimer ns) of one traced launch, per CTA
 __device__ unsigned long long g_trace[1024 * 8];
@@ -297,8 +304,64 @@ __device__ __forceinline__ void stamp(int trace, int i) {
     if (blockIdx.x < 1024) g_trace[blockIdx.x * 8 + i] = t;
   }
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
-__global__ void __launch_bounds__(64, 1) inblock4_kernel(
+// 3xTF32 on the legacy warp-level tensor-core path (m16n8k8): the lookahead
+// is a 128 x 16 x K product per CTA, too small for a tcgen05 pipeline.
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = h;
+  lo = __float_as_uint(x - __uint_as_float(h));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// G^T rows [r0, r1) of the block (zero rows past bsz)
+__device__ __forceinline__ void stage_gt(Smem& sm, const float* gpb, long long ib, int bsz, int r0,
+                                         int r1, int tid) {
+  for (int e = r0 * (kB / 4) + tid; e < r1 * (kB / 4); e += kThreads) {
+    const int li = e / (kB / 4), q = (e % (kB / 4)) * 4;
+    float* dst = &sm.u.gt[li * kB + q];
+    if (li < bsz)
+      cp_async16(dst, gpb + (ib + li) * kB + q);
+    else
+      *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+// lookahead chunk: G[blk, kprev + q0 : +kLa4] and D_prev[q0 : +kLa4] of the CTA's columns
+__device__ __forceinline__ void stage_la(Smem& sm, int buf, const float* gpl, const float* dprev,
+                                         long long n, long long m, long long ib, int bsz,
+                                         long long kprev, int bprev, int q0, long long j0,
+                                         long long ldd, int tid) {
+  for (int e = tid; e < kB * kLa4 / 4; e += kThreads) {
+    const int li = e / (kLa4 / 4), q = (e % (kLa4 / 4)) * 4;
+    float* dst = &sm.u.la.gc[buf][li][q];
+    if (li < bsz && q0 + q < bprev)
+      cp_async16(dst, gpl + (ib + li) * n + kprev + q0 + q);
+    else
+      *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int e = tid; e < kCols4 * kLa4 / 4; e += kThreads) {
+    const int cl = e / (kLa4 / 4), q = (e % (kLa4 / 4)) * 4;
+    float* dst = &sm.u.la.dp[buf][cl][q];
+    if (j0 + cl < m && q0 + q < bprev)
+      cp_async16(dst, dprev + (j0 + cl) * ldd + q0 + q);
+    else
+      *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
     const float* __restrict__ w, long long ldw, const int32_t* __restrict__ order,
     const float* __restrict__ acc, int use_acc, const float* __restrict__ gpl,
     const float* __restrict__ gpb, const float* __restrict__ dprev, int bprev,
@@ -311,118 +374,185 @@ __global__ void __launch_bounds__(64, 1) inblock4_kernel(
   stamp(trace, 0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cc = lane & 7, rg = lane >> 3;
-  const int cj = warp * kCpw + cc;
+  // Roles: the two chain warps should sit on different SM sub-partitions
+  // from the co-resident CTA's chain warps.  Warp slots are handed out in
+  // CTA-sized runs, so take SMSPs {0,1} in even runs and {2,3} in odd runs
+  // (fall back to warps 0-1 if the slot layout is not as assumed).
+  unsigned wid;
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+  const int cand = ((wid & 3) >> 1) == ((wid >> 2) & 1);
+  if (lane == 0) sm.role[warp] = cand;
+  const int og = tid < bsz ? order[ib + tid] : 0;
+  __syncthreads();
+  int h, rank;  // h: 0 = chain warp; rank: column half of a chain warp
+  {
+    const int nm = sm.role[0] + sm.role[1] + sm.role[2] + sm.role[3];
+    if (nm == 2) {
+      h = cand ? 0 : 1;
+      rank = 0;
+      for (int q = 0; q < warp; ++q) rank += sm.role[q];
+    } else {
+      h = warp >> 1;
+      rank = warp & 1;
+    }
+  }
+  const int cj = rank * kCpw + cc;
   const long long j0 = (long long)blockIdx.x * kCols4;
   const long long j = j0 + cj;
   const bool col_ok = j < m;
 
-  // ---- per-row table: original row, output offset, (w, s, 1/s, z) per column;
-  // gathered with 4-byte cp.async (every load in flight at once)
-  for (int e = tid; e < kB; e += 64) {
-    const int o = e < bsz ? order[ib + e] : 0;
-    sm.og[e] = o;
-    sm.orow[e] = (long long)o * ldo;
-  }
-  if (tid < kCols4) sm.jg[tid] = c.gran == 2 ? (j0 + tid) / c.group : 0;
-  __syncthreads();
-  for (int e = tid; e < kB * kCols4; e += 64) {
-    const int li = e / kCols4, cl = e % kCols4;
-    const long long jj = j0 + cl;
-    float4* v = &sm.tab[li][cl];
-    if (li < bsz && jj < m) {
-      const long long orig = sm.og[li];
-      const long long g = c.gran == 0 ? 0 : (c.gran == 1 ? orig : orig * c.gpr + sm.jg[cl]);
-      cp_async(&v->x, w + orig * ldw + jj);
-      cp_async(&v->y, scales + g);
-      cp_async(reinterpret_cast<int*>(&v->w), zeros + g);
-    } else {
-      *v = make_float4(0.f, 1.f, 1.f, 0.f);
-      reinterpret_cast<int*>(&v->w)[0] = 0;
-    }
-  }
-  float r[kRpt];
+  // ---- row order (one row per thread) and this thread's acc rows, in flight together
+  float r[kRpt];  // main warps: slots k = rows rg + 4k (acc = earlier super-blocks)
 #pragma unroll
   for (int k = 0; k < kRpt; ++k) {
     const int li = rg + 4 * k;
-    r[k] = (use_acc && col_ok && li < bsz) ? acc[(ib + li) * m + j] : 0.f;
+    r[k] = (h == 0 && use_acc && col_ok && li < bsz) ? acc[(ib + li) * m + j] : 0.f;
   }
-  stamp(trace, 1);
-  // ---- lookahead: r += G[blk, prev blk] D_prev (16-byte staging)
-  if (bprev > 0) {
-    const long long kprev = ib - bprev;
-    for (int q0 = 0; q0 < bprev; q0 += kLaChunk) {
-      for (int e = tid; e < kB * kLaChunk / 4; e += 64) {
-        const int li = e / (kLaChunk / 4), q = (e % (kLaChunk / 4)) * 4;
-        float* dst = &sm.u.la.gc[li][q];
-        if (li < bsz && q0 + q < bprev)
-          cp_async16(dst, gpl + (ib + li) * n + kprev + q0 + q);
-        else
-          *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      for (int e = tid; e < kCols4 * kLaChunk / 4; e += 64) {
-        const int cl = e / (kLaChunk / 4), q = (e % (kLaChunk / 4)) * 4;
-        float* dst = &sm.u.la.dp[cl][q];
-        if (j0 + cl < m && q0 + q < bprev)
-          cp_async16(dst, dprev + (j0 + cl) * ldd + q0 + q);
-        else
-          *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      cp_async_wait_all();
-      __syncthreads();
-#pragma unroll 1
-      for (int q = 0; q < kLaChunk; q += 4) {
-        float dv[4];
-        ld4(&sm.u.la.dp[cj][q], dv);
+  // ---- async: late G rows (never overlapped by the lookahead buffers), lookahead chunk 0
+  const long long kprev = ib - bprev;
+  stage_gt(sm, gpb, ib, bsz, bprev > 0 ? kGtEarly : 0, kB, tid);
+  if (tid < 8) reinterpret_cast<float4*>(&sm.u.gt[kB * kB])[tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+  cp_async_commit();
+  if (bprev > 0) stage_la(sm, 0, gpl, dprev, n, m, ib, bsz, kprev, bprev, 0, j0, ldd, tid);
+  cp_async_commit();
+  sm.og[tid] = og;
+  sm.orow[tid] = (long long)og * ldo;
+  __syncthreads();
+  stamp(trace, 6);
+
+  // ---- per-(row, column) table {w, s, 1/s, z}: task = (row, 4 columns)
+  const bool wvec = (ldw & 3) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
 #pragma unroll
-        for (int k = 0; k < kRpt; ++k) {
-          float g[4];
-          ld4(&sm.u.la.gc[rg + 4 * k][q], g);
-          r[k] = fmaf(g[0], dv[0], r[k]);
-          r[k] = fmaf(g[1], dv[1], r[k]);
-          r[k] = fmaf(g[2], dv[2], r[k]);
-          r[k] = fmaf(g[3], dv[3], r[k]);
+  for (int i = 0; i < kB * kCols4 / 4 / kThreads; ++i) {
+    const int e = tid + i * kThreads;
+    const int li = e >> 2, q = (e & 3) * 4;
+    const long long jj = j0 + q;
+    float4* dst = &sm.tab[li][q];
+    if (li >= bsz) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dst[u] = make_float4(0.f, 1.f, 1.f, 0.f);
+      continue;
+    }
+    const long long orig = sm.og[li];
+    const float* wr = w + orig * ldw + jj;
+    float wv[4];
+    if (wvec && jj + 3 < m) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(wr));
+      wv[0] = f.x, wv[1] = f.y, wv[2] = f.z, wv[3] = f.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) wv[u] = jj + u < m ? __ldg(wr + u) : 0.f;
+    }
+    const long long g0 = group_of(c, orig, jj), g3 = group_of(c, orig, std::min(jj + 3, m - 1));
+    if (g0 == g3) {
+      const float sv = __ldg(scales + g0);
+      const float y = rcp_refined(sv), zf = float(__ldg(zeros + g0));
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        dst[u] = jj + u < m ? make_float4(wv[u], sv, y, zf) : make_float4(0.f, 1.f, 1.f, 0.f);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (jj + u < m) {
+          const long long g = group_of(c, orig, jj + u);
+          const float sv = __ldg(scales + g);
+          dst[u] = make_float4(wv[u], sv, rcp_refined(sv), float(__ldg(zeros + g)));
+        } else {
+          dst[u] = make_float4(0.f, 1.f, 1.f, 0.f);
         }
+      }
+    }
+  }
+  stamp(trace, 7);
+  stamp(trace, 1);
+
+  // ---- lookahead: G[blk, sb0:ib] D[sb0:ib] on the tensor cores (3xTF32,
+  // double-buffered K chunks); warp w owns rows 32w..32w+31, all 16 columns
+  if (bprev > 0) {
+    float c1[2][2][4] = {}, c2[2][2][4] = {};  // hi*hi, cross terms
+    const int gq = lane >> 2, tq = lane & 3, rb = 32 * warp;
+    const int nch = (bprev + kLa4 - 1) / kLa4;
+#pragma unroll 1
+    for (int ch = 0; ch < nch; ++ch) {
+      const int buf = ch & 1;
+      if (ch + 1 < nch) {
+        stage_la(sm, buf ^ 1, gpl, dprev, n, m, ib, bsz, kprev, bprev, (ch + 1) * kLa4, j0, ldd,
+                 tid);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k8 = 0; k8 < kLa4; k8 += 8) {
+        uint32_t ah[2][4], al[2][4], bh[2][2], bl[2][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const float* g0 = &sm.u.la.gc[buf][rb + 16 * mt + gq][k8 + tq];
+          const float* g8 = g0 + 8 * (kLa4 + 4);
+          split_tf32(g0[0], ah[mt][0], al[mt][0]);
+          split_tf32(g8[0], ah[mt][1], al[mt][1]);
+          split_tf32(g0[4], ah[mt][2], al[mt][2]);
+          split_tf32(g8[4], ah[mt][3], al[mt][3]);
+        }
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const float* d0 = &sm.u.la.dp[buf][8 * nt + gq][k8 + tq];
+          split_tf32(d0[0], bh[nt][0], bl[nt][0]);
+          split_tf32(d0[4], bh[nt][1], bl[nt][1]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            mma_tf32(c1[mt][nt], ah[mt], bh[nt][0], bh[nt][1]);
+            mma_tf32(c2[mt][nt], ah[mt], bl[nt][0], bl[nt][1]);
+            mma_tf32(c2[mt][nt], al[mt], bh[nt][0], bh[nt][1]);
+          }
       }
       __syncthreads();
     }
+    // the lookahead buffers are dead: stage the early G rows over them
+    stage_gt(sm, gpb, ib, bsz, 0, kGtEarly, tid);
+    cp_async_commit();
+    // hand the 128 x 16 product to the main warps (ds is free until the chain)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int row = rb + 16 * mt + gq, col = 8 * nt + 2 * tq;
+        sm.ds[col][row] = c1[mt][nt][0] + c2[mt][nt][0];
+        sm.ds[col + 1][row] = c1[mt][nt][1] + c2[mt][nt][1];
+        sm.ds[col][row + 8] = c1[mt][nt][2] + c2[mt][nt][2];
+        sm.ds[col + 1][row + 8] = c1[mt][nt][3] + c2[mt][nt][3];
+      }
   }
   stamp(trace, 2);
-  // ---- the block's rows of G^T (already in lane order): 16-byte copies
-  for (int e = tid; e < kB * kB / 4; e += 64) {
-    const int li = e / (kB / 4), q = (e % (kB / 4)) * 4;
-    float* dst = &sm.u.gt[li * kB + q];
-    if (li < bsz)
-      cp_async16(dst, gpb + (ib + li) * kB + q);
-    else
-      *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  if (tid < 8) reinterpret_cast<float4*>(&sm.u.gt[kB * kB])[tid] = make_float4(0.f, 0.f, 0.f, 0.f);
-  cp_async_wait_all();
-  __syncthreads();
-  for (int e = tid; e < kB * kCols4; e += 64) {  // 1/s and float(z) for the table
-    float4& v = sm.tab[e / kCols4][e % kCols4];
-    v.z = rcp_refined(v.y);
-    v.w = float(__float_as_int(v.w));
-  }
+  cp_async_wait<0>();
   __syncthreads();
   stamp(trace, 3);
 
-  const float qminf = float(c.qmin), qmaxf = float(c.qmax);
-  // Rows li >= bsz of a short last block run as padding (w = 0, s = 1, z = 0,
-  // zero G rows): finite d that no real row picks up, never stored -- so the
-  // step loop has no per-row branch and the next row's loads hoist freely.
+  if (__any_sync(0xffffffffu, h == 0)) {  // (vote: warp-uniform, no divergent-shuffle path)
+    if (bprev > 0) {
+#pragma unroll
+      for (int k = 0; k < kRpt; ++k) r[k] += sm.ds[cj][rg + 4 * k];
+    }
+    const float qminf = float(c.qmin), qmaxf = float(c.qmax);
+    // Rows li >= bsz of a short last block run as padding (w = 0, s = 1, z = 0,
+    // zero G rows): finite d that no real row picks up, never stored -- so the
+    // step loop has no per-row branch and the next row's loads hoist freely.
 #pragma unroll 1
-  for (int T = 0; T < kRpt / 4; ++T) {
-    if (16 * T >= bsz) break;
-    int off[8];  // chunk offsets of this lane's slots k = 4m .. 4m+3 (logical chunk T + m)
+    for (int T = 0; T < kRpt / 4; ++T) {
+      if (16 * T >= bsz) break;
+      int off[8];  // chunk offsets of this lane's slots k = 4m .. 4m+3 (logical chunk T + m)
 #pragma unroll
-    for (int mm = 0; mm < 8; ++mm) off[mm] = rg * 32 + 4 * ((T + mm) ^ (2 * rg));
+      for (int mm = 0; mm < 8; ++mm) off[mm] = rg * 32 + 4 * ((T + mm) ^ (2 * rg));
 #pragma unroll
-    for (int tt = 0; tt < 4; ++tt) {
+      for (int tt = 0; tt < 4; ++tt) {
 #pragma unroll
-      for (int o = 0; o < kLpc; ++o) {
-        const int li = 16 * T + 4 * tt + o;
-        {
+        for (int o = 0; o < kLpc; ++o) {
+          const int li = 16 * T + 4 * tt + o;
           float g[kRpt];
           const float* gp = &sm.u.gt[li * kB];
 #pragma unroll
@@ -446,26 +576,43 @@ __global__ void __launch_bounds__(64, 1) inblock4_kernel(
           for (int k = 0; k < kRpt; ++k) r[k] = fmaf(g[k], d, r[k]);
         }
       }
-    }
 #pragma unroll
-    for (int k = 0; k < kRpt; ++k) r[k] = k + 4 < kRpt ? r[k + 4] : 0.f;
+      for (int k = 0; k < kRpt; ++k) r[k] = k + 4 < kRpt ? r[k + 4] : 0.f;
+    }
   }
   __syncthreads();
   stamp(trace, 4);
-  for (int e = tid; e < kCols4 * kB; e += 64) {
-    const int cl = e / kB, li = e % kB;
+  // ---- D (K-major, the trailing GEMM's B operand), then codes / W_hat in
+  // original row order (layerwise.cpp:75)
+  for (int e = tid; e < kCols4 * kB / 4; e += kThreads) {
+    const int cl = e / (kB / 4), li = (e % (kB / 4)) * 4;
     if (j0 + cl >= m || li >= bsz) continue;
-    const float v = sm.ds[cl][li];
     const long long off = (j0 + cl) * ldd + li;
-    dcur[off] = v;
-    if (dcur_hi) {
-      const float hi = tf32_hi(v);
-      dcur_hi[off] = hi;
-      dcur_lo[off] = v - hi;
+    const float4 v = make_float4(sm.ds[cl][li], sm.ds[cl][li + 1], sm.ds[cl][li + 2],
+                                 sm.ds[cl][li + 3]);
+    if (li + 4 <= bsz) {
+      *reinterpret_cast<float4*>(dcur + off) = v;
+      if (dcur_hi) {
+        const float4 hi = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+        *reinterpret_cast<float4*>(dcur_hi + off) = hi;
+        *reinterpret_cast<float4*>(dcur_lo + off) =
+            make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+      }
+    } else {
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (li + u >= bsz) break;
+        dcur[off + u] = vv[u];
+        if (dcur_hi) {
+          const float hi = tf32_hi(vv[u]);
+          dcur_hi[off + u] = hi;
+          dcur_lo[off + u] = vv[u] - hi;
+        }
+      }
     }
   }
-  // codes / W_hat in original row order (layerwise.cpp:75), row-contiguous
-  for (int e = tid; e < kB * kCols4; e += 64) {
+  for (int e = tid; e < kB * kCols4; e += kThreads) {
     const int li = e / kCols4, cl = e % kCols4;
     if (li >= bsz || j0 + cl >= m) continue;
     const int16_t q = sm.cs[cl][li];
@@ -495,7 +642,7 @@ void launch_inblock4(const float* w, long long ldw, const int32_t* order, const 
   (void)attr;
   const unsigned ctas = unsigned((m + l4::kCols4 - 1) / l4::kCols4);
   count_launches(1);
-  l4::inblock4_kernel<<<ctas, 64, sizeof(l4::Smem), st>>>(w, ldw, order, acc, use_acc, gpl, gtt,
+  l4::inblock4_kernel<<<ctas, l4::kThreads, sizeof(l4::Smem), st>>>(w, ldw, order, acc, use_acc, gpl, gtt,
                                                           dprev, bprev, dcur, dch, dcl, c, scales,
                                                           zeros, n, m, ib, bsz, codes, w_hat, ldo,
                                                           ldd, trace);
@@ -544,7 +691,12 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
   // block size is a pure re-association of the trailing update (SURVEY §0
   // item 11); blocks above 128 rows run as 128-row blocks.
   const long long B = block < 1 ? 1 : (block > kB ? kB : block);
-  const long long SB = std::max<long long>(1, kSuperRows / B);  // blocks per super-block
+  static const long long super_rows = [] {  // tuning switch: OCWG_SWEEP_SUPER=128..512
+    const char* e = getenv("OCWG_SWEEP_SUPER");
+    const long long v = e ? atoll(e) : kSuperRows;
+    return std::min(kSuperRows, std::max<long long>(kB, v));
+  }();
+  const long long SB = std::max<long long>(1, super_rows / B);  // blocks per super-block
   const long long SBK = SB * B;
   const bool split = glo != nullptr;
   // debug timing switch (results invalid): OCWG_SWEEP_SKIP=inblock|gemm

@@ -25,11 +25,15 @@ torch.cuda.synchronize()
 tr = np.zeros(1024 * 8, np.uint64)
 k = g.lib().ocwg_debug_sweep_trace(g.context().handle, tr.ctypes.data, tr.size)
 ctas = bench.M_OUT // 16
-t = tr[:ctas * 8].reshape(ctas, 8)[:, :6].astype(np.int64)
+t8 = tr[:ctas * 8].reshape(ctas, 8).astype(np.int64)
+t = t8[:, :6]
 t0 = t[:, 0].min()
 names = ["table+acc", "lookahead", "G stage", "main loop", "epilogue"]
 print(f"ib={os.environ.get('OCWG_SWEEP_TRACE_IB')}: launch span {(t[:, 5].max() - t0) / 1e3:.1f} us, "
       f"CTA start spread {(t[:, 0].max() - t0) / 1e3:.1f} us")
+for nm, a, b in [("  order", 0, 6), ("  gather", 6, 7), ("  acc", 7, 1)]:
+    d = (t8[:, b] - t8[:, a]) / 1e3
+    print(f"  {nm:10s} mean {d.mean():6.2f} us  max {d.max():6.2f}")
 for i, nm in enumerate(names):
     d = (t[:, i + 1] - t[:, i]) / 1e3
     print(f"  {nm:10s} mean {d.mean():6.2f} us  max {d.max():6.2f}")
