@@ -55,6 +55,34 @@ __global__ void build_input_kernel(const float* __restrict__ h, long long n,
   }
 }
 
+// Same gather, one CTA per output row: H row order[n-1-i] is staged in shared
+// memory with coalesced loads, then a[i, j] = row[order[n-1-j]] (j <= i) is
+// written coalesced -- the column permutation happens on chip.
+template <typename T>
+__global__ void __launch_bounds__(256) build_input_rows_kernel(const float* __restrict__ h,
+                                                               long long n,
+                                                               const int32_t* __restrict__ order,
+                                                               const double* damp, T* a) {
+  extern __shared__ float hrow[];
+  const long long i = blockIdx.x;
+  const long long oi = order[n - 1 - i];
+  const float* src = h + oi * n;
+  if ((n & 3) == 0) {
+    for (long long t = threadIdx.x; t < n / 4; t += blockDim.x)
+      reinterpret_cast<float4*>(hrow)[t] = __ldg(reinterpret_cast<const float4*>(src) + t);
+  } else {
+    for (long long t = threadIdx.x; t < n; t += blockDim.x) hrow[t] = __ldg(src + t);
+  }
+  __syncthreads();
+  const double dmp = *damp;
+  T* dst = a + i * n;
+  for (long long j = threadIdx.x; j <= i; j += blockDim.x) {
+    double v = double(hrow[order[n - 1 - j]]);
+    if (j == i) v = __dadd_rn(v, dmp);
+    dst[j] = T(v);
+  }
+}
+
 // damp = percdamp * mean(diag(fp64 H))  (layerwise.cpp:32-33)
 __global__ void damp_kernel(const float* __restrict__ h, long long n, double percdamp,
                             double* damp) {
@@ -699,7 +727,18 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
                                T* a, double* damp, cudaStream_t st) {
   count_launches(2);
   damp_kernel<<<1, 1024, 0, st>>>(h, n, percdamp, damp);
-  build_input_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(h, n, order, damp, a);
+  const size_t row_bytes = size_t(n) * sizeof(float);
+  if (row_bytes <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(build_input_rows_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr = true;
+    }
+    build_input_rows_kernel<T><<<unsigned(n), 256, row_bytes, st>>>(h, n, order, damp, a);
+  } else {
+    build_input_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(h, n, order, damp, a);
+  }
 }
 
 template <typename T>

@@ -292,26 +292,32 @@ __global__ void unpack_meta_kernel(const uint8_t* __restrict__ meta, long long n
 }
 
 // Stable descending rank of diag(H): rank_i = #{j: d_j > d_i} + #{j < i: d_j == d_i}.
-// O(n^2) comparisons, tiled through shared memory; bit-exact with
+// O(n^2) comparisons: 8 threads per row i split the j range (diag tiles staged
+// in shared memory), then a shuffle reduction; bit-exact with
 // std::stable_sort(order, h[a][a] > h[b][b]) for NaN-free diagonals.
-__global__ void order_rank_kernel(const float* __restrict__ h, long long n, int32_t* order) {
-  __shared__ float tile[1024];
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int kOrdThreads = 256, kOrdSplit = 8, kOrdTile = 8192;
+__global__ void __launch_bounds__(kOrdThreads) order_rank_kernel(const float* __restrict__ h,
+                                                                 long long n, int32_t* order) {
+  __shared__ float tile[kOrdTile];
+  const int part = threadIdx.x % kOrdSplit;
+  const long long i = (long long)blockIdx.x * (kOrdThreads / kOrdSplit) + threadIdx.x / kOrdSplit;
   const float di = i < n ? h[i * n + i] : 0.0f;
   long long rank = 0;
-  for (long long j0 = 0; j0 < n; j0 += 1024) {
+  for (long long j0 = 0; j0 < n; j0 += kOrdTile) {
+    const int cnt = int(min((long long)kOrdTile, n - j0));
     __syncthreads();
-    for (long long t = threadIdx.x; t < 1024 && j0 + t < n; t += blockDim.x)
-      tile[t] = h[(j0 + t) * n + (j0 + t)];
+    for (int t = threadIdx.x; t < cnt; t += kOrdThreads) tile[t] = h[(j0 + t) * (n + 1)];
     __syncthreads();
-    const long long cnt = min(1024LL, n - j0);
-    if (i < n)
-      for (long long t = 0; t < cnt; ++t) {
-        const float dj = tile[t];
-        rank += (dj > di) || (dj == di && j0 + t < i);
-      }
+    const long long lim = i - j0;  // t < lim  <=>  j0 + t < i
+    int cnt_r = 0;
+    for (int t = part; t < cnt; t += kOrdSplit) {
+      const float dj = tile[t];
+      cnt_r += (dj > di) | ((dj == di) & (t < lim));
+    }
+    rank += cnt_r;
   }
-  if (i < n) order[rank] = int32_t(i);
+  for (int o = 1; o < kOrdSplit; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+  if (part == 0 && i < n) order[rank] = int32_t(i);
 }
 
 __global__ void iota_kernel(long long n, int32_t* order) {
@@ -388,7 +394,9 @@ void launch_order(const float* h, long long n, int actorder, int32_t* order, cud
     iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, order);
     return;
   }
-  order_rank_kernel<<<int((n + 255) / 256), 256, 0, st>>>(h, n, order);
+  const long long rows_per_cta = kOrdThreads / kOrdSplit;
+  order_rank_kernel<<<int((n + rows_per_cta - 1) / rows_per_cta), kOrdThreads, 0, st>>>(h, n,
+                                                                                      order);
 }
 
 }  // namespace ocwg
