@@ -117,6 +117,32 @@ __device__ __forceinline__ T ldcg(const T* p) {
   return __ldcg(p);
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Raw copy of a 64 x 64 tile (rows x cols valid, row stride n) into dst
+// (row-major, ld 64); 16-byte cp.async when aligned, zero outside.
+template <typename T>
+__device__ __forceinline__ void stage_tile(T* dst, const T* src, long long n, int rows, int cols,
+                                           bool vec_ok) {
+  constexpr int V = 16 / sizeof(T);
+  for (int e = threadIdx.x; e < TB * TB / V; e += CT) {
+    const int rr = e / (TB / V), cc = (e % (TB / V)) * V;
+    T* d = dst + rr * TB + cc;
+    if (vec_ok && rr < rows && cc + V <= cols) {
+      cp_async16(d, src + (long long)rr * n + cc);
+    } else {
+#pragma unroll
+      for (int q = 0; q < V; ++q) d[q] = (rr < rows && cc + q < cols) ? ldcg(src + (long long)rr * n + cc + q) : T(0);
+    }
+  }
+}
+
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t u = __float_as_uint(x);
   u = (u + 0xFFFu + ((u >> 13) & 1u)) & ~0x1FFFu;  // RNE to 10 mantissa bits
@@ -235,9 +261,10 @@ struct CholSmem {
   T ps[TB * TB];
   T qs[TB * TB];
   T lt[TB][TB + 4];   // diag tile L_cc transposed (lt[j][c] = L[c][j]); also G staging
-  T col[2][TB];       // (unused)
   T sf[TB][TB + 1];   // diagonal tile being factored
   T wcol[2][72];      // warp elimination: published pivot column (shifted, + zero pad)
+  T wcol3[3][2][72];  // the same, per warp, for factor_tile64's three eliminating warps
+  T sb[2][TB * TB + 64];  // owner: staging of the next tiles (raw row-major, cp.async)
   T lt32[32][40];     // warp elimination: L columns, shifted like wcol (for the solve)
   T rdiag[TB];
   int item;
@@ -278,31 +305,43 @@ __device__ void emit_g(const T (&t)[4][4], CholSmem<T>& sm, const T* diag, int r
 }
 
 // Warp-synchronous right-looking Cholesky of a 32 x 32 block held one row per
-// lane (a[k] = A[lane][j0 + k], lower part used), written to out[lane][j0 + j].
-// The register array rotates as it is updated (a[0] is always the pivot
-// column).  Per pivot each lane publishes its pivot-column entry to shared
-// memory (one store + warp sync, double-buffered, zero-padded past 32) and
-// reads the others as broadcasts: no block barrier, no shuffles.
-// With WITH_B, each lane also carries row 32 + lane (b[k] = A[32 + lane][j0 + k])
-// through the same pivots: b ends as L21 = A21 L11^-T (written to out_b), off
-// the pivot chain.
-template <typename T, bool WITH_B>
+// lane (a[k] = A[lane][j0 + k], lower part used).  The register array rotates
+// as it is updated (a[0] is always the pivot column).  Per pivot each lane
+// publishes its pivot-column entry to shared memory (double-buffered,
+// zero-padded past 32) and reads the pivot and the others as broadcasts.  The
+// loop is software-pipelined: right after the new a[0] is formed, the next
+// column's store is issued, so its latency hides under the remaining updates.
+//   CARRY = false: writes L[lane][j] to out_row[j] and 1/L[j][j] to rdiag[j].
+//   CARRY = true : the lane also carries a row b through the same pivots (the
+//                  eliminated block itself is discarded): b ends as
+//                  b L^-T, written to out_b[j].
+template <typename T>
+__device__ __forceinline__ T rsqrt_fast(T x) {
+  if constexpr (sizeof(T) == 4) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  } else {
+    return rsqrt(x);
+  }
+}
+template <typename T, bool CARRY>
 __device__ __forceinline__ bool warp_chol32(T (&a)[32], T (&b)[32], T* out_row, T* out_b,
-                                            T* rdiag, T (*wcol)[72], T (*lt32)[40] = nullptr) {
+                                            T* rdiag, T (*wcol)[72]) {
   const int lane = threadIdx.x & 31;
   bool ok = true;
-#pragma unroll 1
+  // stored at lane + sh so that entry j+1 starts a 16-byte chunk: the 31
+  // entries a lane needs are 8 LDS.128 broadcasts
+  wcol[0][lane + 3] = a[0];
+  // (unrolled by 4: buffer parity and shifts are static and ptxas sees the loop-carried
+  // chain a0 -> store -> next pivot load, so it issues a0 first)
+#pragma unroll 4
   for (int j = 0; j < 32; ++j) {
-    // stored at lane + sh so that entry j+1 starts a 16-byte chunk: the 31
-    // entries a lane needs are 8 LDS.128 broadcasts
     const int sh = (3 - j) & 3;
-    T* cb = wcol[j & 1];
-    cb[lane + sh] = a[0];
-    const T p = __shfl_sync(0xffffffffu, a[0], j);  // pivot off the shared-memory round trip
     __syncwarp();
-    // the column entries first: their load latency overlaps the rsqrt chain
+    const T p = wcol[j & 1][j + sh];  // the pivot, lane j's entry (broadcast load: no shuffle)
     T v[32];
-    const T* nxt = cb + j + sh + 1;  // 16-byte aligned
+    const T* nxt = wcol[j & 1] + j + sh + 1;  // 16-byte aligned
 #pragma unroll
     for (int k4 = 0; k4 < 32; k4 += 4) {
       T v4[4];
@@ -311,33 +350,41 @@ __device__ __forceinline__ bool warp_chol32(T (&a)[32], T (&b)[32], T* out_row, 
       for (int e = 0; e < 4; ++e) v[k4 + e] = v4[e];
     }
     ok &= (p > T(0));
-    const T rs = rsqrt_nr(p);
+    const T rs = rsqrt_fast(p);
     const T l = a[0] * rs;  // L[lane][j]; lane j: sqrt(p)
     const T lrs = l * rs;   // a[k] -= L[lane][j] L[j+k][j] = lrs * a_{j+k}[j]
+    const T a0 = fma(-lrs, v[0], a[1]);
+    if (j + 1 < 32) wcol[(j + 1) & 1][lane + ((2 - j) & 3)] = a0;  // next column, early
 #pragma unroll
-    for (int k = 0; k + 1 < 32; ++k) a[k] = fma(-lrs, v[k], a[k + 1]);
+    for (int k = 1; k + 1 < 32; ++k) a[k] = fma(-lrs, v[k], a[k + 1]);
+    a[0] = a0;
     a[31] = T(0);
-    const T lo = lane >= j ? l : T(0);
-    out_row[j] = lo;
-    if (lt32) lt32[j][lane + sh] = lo;  // column j of L, shifted like cb (for the solve)
-    if (lane == j) rdiag[j] = rs;  // 1 / L[j][j]
-    if (WITH_B) {
-      const T lb = b[0] * rs;  // L21[lane][j]
+    if constexpr (CARRY) {
+      const T lb = b[0] * rs;  // (b L^-T)[j]
       const T lbrs = lb * rs;
 #pragma unroll
       for (int k = 0; k + 1 < 32; ++k) b[k] = fma(-lbrs, v[k], b[k + 1]);
       b[31] = T(0);
       out_b[j] = lb;
+    } else {
+      out_row[j] = lane >= j ? l : T(0);
+      if (lane == j) rdiag[j] = rs;  // 1 / L[j][j]
     }
   }
   return ok;
 }
 
-// Factor the 64 x 64 tile in sm.sf (lower, padded with identity) in place:
-// L11 = chol(A11) and L21 = A21 L11^-T by warp 0, A22 -= L21 L21^T by the
-// CTA, L22 = chol(A22) by warp 0.  Upper entries are zeroed; sm.rdiag gets
-// 1 / L[j][j].  All threads call.
-template <typename T>
+// Factor the 64 x 64 tile in sm.sf (lower, padded with identity) in place.
+// Three warps run the same 32-column eliminations (warp_chol32), on distinct
+// SM sub-partitions, so the rows they carry cost no chain length:
+//   h = 0: warp 0 -> L11 = chol(A11); warp 2 carries A21 -> L21 = A21 L11^-T;
+//          [INV] warp 1 carries identity rows 0-31 -> X rows of L^-T;
+//          CTA: A22 -= L21 L21^T  [INV: X[0:32, 32:] = -X[0:32, :32] L21^T];
+//   h = 1: warp 0 -> L22 = chol(A22);
+//          [INV] warps 1, 2 carry X rows 0-31 / identity rows 32-63.
+// With INV, sm.lt receives X = L^-T (upper triangular, ld TB + 4).  Upper
+// entries of sf are zeroed; sm.rdiag gets 1 / L[j][j].  All threads call.
+template <typename T, bool INV = false>
 __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   bool ok = true;
@@ -345,59 +392,76 @@ __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr) {
     if (prof && tid == 0) prof[i] = clock64();
   };
   pstamp(0);
-  for (int e = tid; e < 2 * 72; e += CT) sm.wcol[e / 72][e % 72] = T(0);
-  for (int e = tid; e < 32 * 40; e += CT) sm.lt32[e / 40][e % 40] = T(0);
+  for (int e = tid; e < 3 * 2 * 72; e += CT) (&sm.wcol3[0][0][0])[e] = T(0);
   __syncthreads();
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
     const int o = 32 * h;  // diagonal block [o, o+32)
-    if (warp == 0) {
-      T av[32];
+    const bool active = warp == 0 || (warp == 2 && h == 0) || (INV && warp <= 2);
+    // (votes make the warp-uniform branches visible to ptxas: no divergent-shuffle
+    // fallback paths, which would pin the loads behind branch checks)
+    if (__any_sync(0xffffffffu, active)) {
+      T av[32], bv[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) av[k] = sm.sf[o + lane][o + k];
-      ok &= warp_chol32<T, false>(av, av, &sm.sf[o + lane][o], nullptr, &sm.rdiag[o], sm.wcol,
-                                  sm.lt32);
-      pstamp(1 + 3 * h);
-      if (h == 0) {
-        __syncwarp();
-        // L21: rows 32 + lane solve x L11^T = a (forward substitution, rotating)
+      T* brow = nullptr;  // carried row (written back in place)
+      if (warp == 2 && h == 0) {
+        brow = &sm.sf[32 + lane][0];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) av[k] = sm.sf[32 + lane][k];
-#pragma unroll 1
-        for (int j = 0; j < 32; ++j) {
-          T v[32];
-          const T* lcol = &sm.lt32[j][j + ((3 - j) & 3) + 1];  // L11[j+1..][j], aligned
+        for (int k = 0; k < 32; ++k) bv[k] = brow[k];
+      } else if (warp > 0) {  // INV
+        const bool ident = (warp == 1) == (h == 0);
+        brow = &sm.lt[32 * (warp - 1) + lane][o];
 #pragma unroll
-          for (int k4 = 0; k4 < 32; k4 += 4) {
-            T v4[4];
-            ld4(lcol + k4, v4);
+        for (int k = 0; k < 32; ++k) bv[k] = ident ? T(k == lane ? 1 : 0) : brow[k];
+        if (h == 1 && warp == 2) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) v[k4 + e] = v4[e];
-          }
-          const T x = av[0] * sm.rdiag[j];
-#pragma unroll
-          for (int k = 0; k + 1 < 32; ++k) av[k] = fma(-x, v[k], av[k + 1]);
-          av[31] = T(0);
-          sm.sf[32 + lane][j] = x;
+          for (int k = 0; k < 32; ++k) sm.lt[32 + lane][k] = T(0);
         }
+      } else {
 #pragma unroll
-        for (int k = 0; k < 32; ++k) sm.sf[lane][32 + k] = T(0);
-        pstamp(2);
+        for (int k = 0; k < 32; ++k) bv[k] = T(0);
       }
+      const bool w0 = __any_sync(0xffffffffu, warp == 0);
+      const bool okw = w0 ? warp_chol32<T, false>(av, bv, &sm.sf[o + lane][o], nullptr,
+                                                  &sm.rdiag[o], sm.wcol3[0])
+                          : warp_chol32<T, true>(av, bv, nullptr, brow, nullptr, sm.wcol3[warp]);
+      if (w0) {
+        ok &= okw;
+        if (h == 0) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) sm.sf[lane][32 + k] = T(0);
+        }
+      }
+      pstamp(1 + 3 * h);
     }
     __syncthreads();
-    if (h == 0) {  // A22 -= L21 L21^T: thread -> row i, 4 columns
-      const int i = tid >> 3, j0 = (tid & 7) * 4;
-      T s4[4] = {T(0), T(0), T(0), T(0)};
+    if (h == 0) {
+      if (!INV || tid < 128) {  // A22 -= L21 L21^T: thread -> row i, (INV ? 8 : 4) columns
+        constexpr int NJ = INV ? 8 : 4;
+        const int i = tid / (32 / NJ), j0 = (tid % (32 / NJ)) * NJ;
+        T s4[NJ] = {};
 #pragma unroll 8
-      for (int k = 0; k < 32; ++k) {
-        const T li = sm.sf[32 + i][k];
+        for (int k = 0; k < 32; ++k) {
+          const T li = sm.sf[32 + i][k];
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) s4[jj] = fma(li, sm.sf[32 + j0 + jj][k], s4[jj]);
+          for (int jj = 0; jj < NJ; ++jj) s4[jj] = fma(li, sm.sf[32 + j0 + jj][k], s4[jj]);
+        }
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj)
+          if (j0 + jj <= i) sm.sf[32 + i][32 + j0 + jj] -= s4[jj];
+      } else {  // X[0:32, 32:] = -X[0:32, :32] L21^T: thread -> row i, 8 columns
+        const int q = tid - 128, i = q >> 2, j0 = (q & 3) * 8;
+        T s8[8] = {};
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+          const T xi = sm.lt[i][k];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) s8[jj] = fma(xi, sm.sf[32 + j0 + jj][k], s8[jj]);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) sm.lt[i][32 + j0 + jj] = -s8[jj];
       }
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj)
-        if (j0 + jj <= i) sm.sf[32 + i][32 + j0 + jj] -= s4[jj];
       __syncthreads();
       pstamp(3);
     }
@@ -405,26 +469,327 @@ __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr) {
   return ok;
 }
 
+// ---- pieces shared by the owner and the worker CTAs -------------------------
+// t (thread block rows 4ty+u, cols 4tx+v) <- tile at ab; identity padding of a
+// diagonal tile's rows past n
+template <typename T>
+__device__ __forceinline__ void load_t(T (&t)[4][4], const T* ab, long long n, int rows, int cols,
+                                       bool diag, bool vec_ok) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int rr = 4 * ty + u;
+    const T* p = ab + (long long)rr * n + 4 * tx;
+    if (vec_ok && rr < rows && 4 * tx + 4 <= cols) {
+      if constexpr (sizeof(T) == 4) {
+        const float4 f = __ldcg(reinterpret_cast<const float4*>(p));
+        t[u][0] = f.x, t[u][1] = f.y, t[u][2] = f.z, t[u][3] = f.w;
+      } else {
+        const double2 f0 = __ldcg(reinterpret_cast<const double2*>(p));
+        const double2 f1 = __ldcg(reinterpret_cast<const double2*>(p + 2));
+        t[u][0] = f0.x, t[u][1] = f0.y, t[u][2] = f1.x, t[u][3] = f1.y;
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int cc = 4 * tx + v;
+        t[u][v] = (rr < rows && cc < cols) ? ldcg(p + v) : T(0);
+      }
+    }
+    if (diag) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (rr == 4 * tx + v && rr >= rows) t[u][v] = T(1);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void store_t(const T (&t)[4][4], T* ab, long long n, int rows, int cols,
+                                        bool lower) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int rr = 4 * ty + u;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int cl = 4 * tx + v;
+      if (rr < rows && cl < cols && (!lower || cl <= rr)) ab[(long long)rr * n + cl] = t[u][v];
+    }
+  }
+}
+
+// t (row 4ty+u, col 4tx+v) -> the transposed swizzled k-major layout of
+// store_tile_t (S[k][i], k = column): operand of tile_mma
+template <typename T>
+__device__ __forceinline__ void store_t_swz(const T (&t)[4][4], T* S) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) S[(4 * tx + v) * TB + ((ty ^ tx) << 2) + u] = t[u][v];
+}
+
+// X L^T = t by forward substitution (warp shuffles; sm.lt[j][c] = L[c][j],
+// sm.rdiag[j] = 1 / L[j][j]); t <- X
+template <typename T>
+__device__ __forceinline__ void solve_rows(T (&t)[4][4], CholSmem<T>& sm) {
+  const int tid = threadIdx.x, tx = tid & 15, lane = tid & 31;
+  const int src0 = lane & 16;
+#pragma unroll 1
+  for (int j0 = 0; j0 < TB; j0 += 4) {
+    const bool own = tx == (j0 >> 2), later = tx > (j0 >> 2);
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = j0 + jj;
+      const T rd = sm.rdiag[j];
+      T x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __shfl_sync(0xffffffffu, t[u][jj] * rd, src0 + (j >> 2));
+      if (own) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u][jj] = x[u];
+      }
+      T l[4];
+      ld4(&sm.lt[j][4 * tx], l);
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (later || (own && v > jj)) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) t[u][v] = fma(-x[u], l[v], t[u][v]);
+        }
+    }
+  }
+}
+
+// Publish a finalised tile L[r,c] (values t) into G: the sweep's lane-ordered
+// diagonal blocks of G^T (gtt) and the GEMM / lookahead operands (emit_g).
+// sm.rdiag holds L[a][a] of column tile c.
+template <typename T>
+__device__ __forceinline__ void emit_tile(const T (&t)[4][4], CholSmem<T>& sm, int r, int c,
+                                          long long n, T* ghi, float* glo, float* gpl,
+                                          float* gtt) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  if (gtt) {
+    // diagonal 128 x 128 blocks of G^T in the sweep's lane order (sweep.cu
+    // gp_pos): row i = n-1-b, column k = n-1-a, only when i, k share a block
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long b = (long long)r * TB + 4 * ty + u;
+      if (b >= n) continue;
+      const long long i = n - 1 - b;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const long long av = (long long)c * TB + 4 * tx + v;
+        if (av >= n || b <= av) continue;
+        const long long k = n - 1 - av;
+        if ((i >> 7) != (k >> 7)) continue;
+        gtt[i * 128 + gp_pos(int(k & 127))] = float(t[u][v] / sm.rdiag[4 * tx + v]);
+      }
+    }
+  }
+  if (ghi) emit_g(t, sm, sm.rdiag, r, c, n, ghi, glo, gpl);
+}
+
+// CTA 0 is the owner of the critical path: per column c it factors tile
+// (c, c) and solves tile (c+1, c), keeping L[c+1, c] in shared memory for the
+// next column's k = c terms, so the chain diag -> sub -> diag has no
+// inter-CTA hand-off.  The other CTAs take work items of column c, in order:
+//   0, 1 -> partial S[c+q,c] = A - sum_{c0<=k<c-1} L[c+q,k] L[c,k]^T, stored in
+//           place (the owner applies k = c-1);
+//   2..  -> tiles (c+2.., c): full accumulation, then X L[c,c]^T = S;
+//   last -> emission of the owner's two tiles into G.
+enum ItemKind { kFull = 0, kPartial = 1, kEmit = 2, kOwner = 3 };
+
 template <typename T>
 __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
     chol_tile_kernel(T* __restrict__ a, long long n, int nt, int c0, int c1, int* flags,
-                     int* counter, unsigned* status, T* ghi, float* glo, float* gpl, float* gtt,
-                     unsigned long long* trace) {
+                     int* pflags, int* counter, unsigned* status, T* ghi, float* glo, float* gpl,
+                     float* gtt, unsigned long long* trace) {
   extern __shared__ __align__(16) unsigned char smraw[];
   CholSmem<T>& sm = *reinterpret_cast<CholSmem<T>*>(smraw);
-  // optional timeline (debug): per item {r, c, start, k-loop done, solve done, published}
-  auto stamp = [&](long long item, int slot) {
+  // optional timeline (debug): per entry {r, c + 1000 kind, start, k-loop done,
+  // factor/solve done, published}
+  auto stamp = [&](long long e, int slot) {
     if (trace && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      trace[item * 6 + slot] = t;
+      trace[e * 6 + slot] = t;
     }
   };
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15, lane = tid & 31;
+  auto tag = [&](long long e, int r, int c, int kind) {
+    if (trace && threadIdx.x == 0) {
+      trace[e * 6 + 0] = (unsigned long long)r;
+      trace[e * 6 + 1] = (unsigned long long)(c + 1000 * kind);
+    }
+  };
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   const bool vec_ok = (sizeof(T) == 4 ? (n & 3) == 0 : (n & 1) == 0);
   long long total = 0;
-  for (int c = c0; c < c1; ++c) total += nt - c;
+  for (int c = c0; c < c1; ++c) total += nt - c + 1;
+  const long long tile = (long long)TB * n;  // elements per tile row
 
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  int* owner_sm = counter + 32;  // (zeroed with the flags)
+  if (blockIdx.x == 0) {
+    if (tid == 0) st_release(owner_sm, int(smid) + 1);
+    // ================= owner: the critical path diag(c) -> sub(c+1, c) -> diag(c+1)
+    // Kept in shared memory between columns:
+    //   sm.qs (= sm.ps) : L[c, c-1], transposed / swizzled (tile_mma operand)
+    //   sm.sb[1]        : S'[c, c] (partial) staged by cp.async during column c-1
+    // Tiles are published by warp 7 while the other warps go on (its fence
+    // only stalls itself).
+    bool staged = false;  // sm.sb[1] holds S'[c, c]
+    for (int c = c0; c < c1; ++c) {
+      const long long e0 = total + 2LL * (c - c0);
+      const int rows = int(std::min<long long>(TB, n - (long long)c * TB));
+      const bool sub = c + 1 < nt;
+      const int rows1 = sub ? int(std::min<long long>(TB, n - (long long)(c + 1) * TB)) : 0;
+      const bool prev = c > c0;
+      tag(e0, c, c, kOwner);
+      stamp(e0, 2);
+      if (!staged) {
+        if (tid == 0) wait_flag(pflags + 2 * c);
+        __syncthreads();
+        stage_tile(sm.sb[1], a + c * tile + (long long)c * TB, n, rows, rows, vec_ok);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      // S[c,c] = S' - L[c,c-1] L[c,c-1]^T  -> sf (identity padding past n)
+      {
+        T t[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int rr = 4 * ty + u, cl = 4 * tx + v;
+            t[u][v] = (rr == cl && rr >= rows) ? T(1) : sm.sb[1][rr * TB + cl];
+          }
+        if (prev) {
+          T acc[4][4] = {};
+          tile_mma(acc, sm.qs, sm.qs);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) t[u][v] -= acc[u][v];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) sm.sf[4 * ty + u][4 * tx + v] = t[u][v];
+      }
+      // stage S'[c+1,c] and, when already published, L[c+1,c-1]
+      if (tid == 0) sm.ready = sub && ld_acquire(pflags + 2 * c + 1);
+      if (tid == 32) sm.item = sub && prev && ld_acquire(flags + (c + 1) * nt + (c - 1));
+      __syncthreads();
+      const bool s_staged = sm.ready, l_staged = sm.item;
+      if (s_staged) stage_tile(sm.sb[1], a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, vec_ok);
+      if (l_staged)
+        stage_tile(sm.sb[0], a + (c + 1) * tile + (long long)(c - 1) * TB, n, rows1, TB, vec_ok);
+      stamp(e0, 3);
+      const bool ok = factor_tile64<T, true>(sm);  // sm.lt = L[c,c]^-T
+      if (!ok && tid == 0 && rows > 0) atomicOr(status, kFlagNotPD);
+      stamp(e0, 4);
+      {
+        T t[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) t[u][v] = sm.sf[4 * ty + u][4 * tx + v];
+        store_t(t, a + c * tile + (long long)c * TB, n, rows, rows, true);
+      }
+      // publish: one thread of warp 7 fences (release is cumulative over the
+      // CTA's stores ordered by the barrier); the chain warps go on
+      __syncthreads();
+      if (tid == CT - 32) {
+        __threadfence();
+        st_release(flags + c * nt + c, 1);
+      }
+      stamp(e0, 5);
+      if (!sub) break;
+
+      // ---- sub tile (c+1, c): S = S' - L[c+1,c-1] L[c,c-1]^T;  X L[c,c]^T = S
+      const long long e1 = e0 + 1;
+      tag(e1, c + 1, c, kOwner);
+      stamp(e1, 2);
+      if (!s_staged) {
+        if (tid == 0) wait_flag(pflags + 2 * c + 1);
+        __syncthreads();
+        stage_tile(sm.sb[1], a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, vec_ok);
+      }
+      if (prev && !l_staged) {
+        if (tid == 0) wait_flag(flags + (c + 1) * nt + (c - 1));
+        __syncthreads();
+        stage_tile(sm.sb[0], a + (c + 1) * tile + (long long)(c - 1) * TB, n, rows1, TB, vec_ok);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      T t[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) t[u][v] = sm.sb[1][(4 * ty + u) * TB + 4 * tx + v];
+      if (prev) {
+        TileRegs<T> P;  // L[c+1,c-1] -> swizzled P operand (ps is free: qs holds L[c,c-1])
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            P.v[ii][e] = sm.sb[0][((tid >> 4) + 16 * ii) * TB + (tid & 15) * 4 + e];
+        store_tile_t(P, sm.ps);
+        __syncthreads();
+        T acc[4][4] = {};
+        tile_mma(acc, sm.ps, sm.qs);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) t[u][v] -= acc[u][v];
+      }
+      // X = S L[c,c]^-T as a tile product: P = S, Q[j][k] = L^-T[k][j] (sm.lt)
+      __syncthreads();  // sb[1], ps, qs consumed
+      if (tid == 0) sm.ready = ld_acquire(pflags + 2 * (c + 1));
+      store_t_swz(t, sm.ps);
+      for (int e = tid; e < TB * TB; e += CT) {
+        const int k = e >> 6, j = e & 63;
+        sm.qs[k * TB + (((j >> 2) ^ ((k >> 2) & 15)) << 2) + (j & 3)] = sm.lt[k][j];
+      }
+      __syncthreads();
+      staged = sm.ready;  // stage the next column's S'[c+1,c+1] under the product
+      if (staged)
+        stage_tile(sm.sb[1], a + (c + 1) * tile + (long long)(c + 1) * TB, n, rows1, rows1, vec_ok);
+      stamp(e1, 3);
+      {
+        T acc[4][4] = {};
+        tile_mma(acc, sm.ps, sm.qs);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) t[u][v] = acc[u][v];
+      }
+      stamp(e1, 4);
+      store_t(t, a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, false);
+      __syncthreads();
+      if (tid == CT - 32) {
+        __threadfence();
+        st_release(flags + (c + 1) * nt + c, 1);
+      }
+      stamp(e1, 5);
+      __syncthreads();  // everyone is done reading qs
+      store_t_swz(t, sm.qs);  // next column: L[c+1, c]
+      __syncthreads();
+    }
+    return;
+  }
+
+  // ================= workers (none on the owner's SM: it keeps its issue slots)
+  if (tid == 0) {
+    int o;
+    while ((o = ld_acquire(owner_sm)) == 0) __nanosleep(100);
+    sm.ready = o == int(smid) + 1;
+  }
+  __syncthreads();
+  if (sm.ready) return;
   while (true) {
     if (tid == 0) sm.item = atomicAdd(counter, 1);
     __syncthreads();
@@ -433,18 +798,44 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
     if (idx >= total) break;
     const long long item_id = idx;
     int c = c0;
-    while (idx >= nt - c) {
-      idx -= nt - c;
+    while (idx >= nt - c + 1) {
+      idx -= nt - c + 1;
       ++c;
     }
-    const int r = c + int(idx);
-    if (trace && tid == 0) {
-      trace[item_id * 6 + 0] = (unsigned long long)r;
-      trace[item_id * 6 + 1] = (unsigned long long)c;
+    const int cols = int(std::min<long long>(TB, n - (long long)c * TB));
+
+    if (idx == nt - c) {
+      // ---- emission of the owner's tiles L[c..c+2, c]
+      tag(item_id, c, c, kEmit);
+      stamp(item_id, 2);
+      if (tid == 0) wait_flag(flags + c * nt + c);
+      __syncthreads();
+      T t[4][4];
+      load_t(t, a + c * tile + (long long)c * TB, n, cols, cols, false, vec_ok);
+      if (tx == ty) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sm.rdiag[4 * ty + u] = t[u][u];
+      }
+      __syncthreads();
+      emit_tile(t, sm, c, c, n, ghi, glo, gpl, gtt);
+      for (int q = 1; q <= 1 && c + q < nt; ++q) {
+        const int rq = int(std::min<long long>(TB, n - (long long)(c + q) * TB));
+        if (tid == 0) wait_flag(flags + (c + q) * nt + c);
+        __syncthreads();
+        load_t(t, a + (c + q) * tile + (long long)c * TB, n, rq, TB, false, vec_ok);
+        emit_tile(t, sm, c + q, c, n, ghi, glo, gpl, gtt);
+      }
+      stamp(item_id, 5);
+      __syncthreads();
+      continue;
     }
+
+    const int r = c + int(idx);
+    const bool partial = r <= c + 1;
+    tag(item_id, r, c, partial ? kPartial : kFull);
     stamp(item_id, 2);
     const int rows = int(std::min<long long>(TB, n - (long long)r * TB));
-    const int cols = int(std::min<long long>(TB, n - (long long)c * TB));
+    const int kend = partial ? c - 1 : c;  // partial items leave k = c-1 to the owner
 
     // ---- S = A[r,c] - sum_k L[r,k] L[c,k]^T
     T acc[4][4];
@@ -453,19 +844,19 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
 #pragma unroll
       for (int v = 0; v < 4; ++v) acc[u][v] = T(0);
     TileRegs<T> P, Q;
-    if (c0 < c) {
+    if (c0 < kend) {
       if (tid == 0) {
         wait_flag(flags + r * nt + c0);
         wait_flag(flags + c * nt + c0);
       }
       __syncthreads();
-      load_tile(P, a + (long long)r * TB * n + (long long)c0 * TB, n, rows, TB, vec_ok);
-      load_tile(Q, a + (long long)c * TB * n + (long long)c0 * TB, n, cols, TB, vec_ok);
+      load_tile(P, a + (long long)r * tile + (long long)c0 * TB, n, rows, TB, vec_ok);
+      load_tile(Q, a + (long long)c * tile + (long long)c0 * TB, n, cols, TB, vec_ok);
     }
-    for (int k = c0; k < c; ++k) {
+    for (int k = c0; k < kend; ++k) {
       store_tile_t(P, sm.ps);
       store_tile_t(Q, sm.qs);
-      const bool more = k + 1 < c;
+      const bool more = k + 1 < kend;
       const int* fr = flags + r * nt + k + 1;
       const int* fc = flags + c * nt + k + 1;
       if (tid == 0) sm.ready = more && ld_acquire(fr) && ld_acquire(fc);
@@ -473,8 +864,8 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       const bool ready = sm.ready;
       // prefetch k+1 under the MMA when its tiles are already published
       if (ready) {
-        load_tile(P, a + (long long)r * TB * n + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
-        load_tile(Q, a + (long long)c * TB * n + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+        load_tile(P, a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
+        load_tile(Q, a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
       }
       tile_mma(acc, sm.ps, sm.qs);
       if (more && !ready) {  // at the dependency frontier: wait, then load
@@ -483,138 +874,59 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
           wait_flag(fc);
         }
         __syncthreads();
-        load_tile(P, a + (long long)r * TB * n + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
-        load_tile(Q, a + (long long)c * TB * n + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+        load_tile(P, a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
+        load_tile(Q, a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
       }
       __syncthreads();
     }
-    // t = A[r,c] - acc (own 4x4 block: rows 4ty+u, cols 4tx+v)
     T t[4][4];
-    {
-      const T* ab = a + (long long)r * TB * n + (long long)c * TB;
+    load_t(t, a + (long long)r * tile + (long long)c * TB, n, rows, cols, false, vec_ok);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int rr = 4 * ty + u;
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int cc = 4 * tx + v;
-          T x = (rr < rows && cc < cols) ? ab[(long long)rr * n + cc] : T(0);
-          if (r == c && rr == cc && rr >= rows) x = T(1);  // identity padding
-          t[u][v] = x - acc[u][v];
-        }
-      }
-    }
-
+      for (int v = 0; v < 4; ++v) t[u][v] -= acc[u][v];
     stamp(item_id, 3);
-    if (r == c) {
-      // ---- diagonal tile: warp-level factorisation in shared memory (factor_tile64)
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) sm.sf[4 * ty + u][4 * tx + v] = t[u][v];
+
+    if (partial) {
+      store_t(t, a + (long long)r * tile + (long long)c * TB, n, rows, cols, false);
+      __threadfence();
       __syncthreads();
-      const bool ok = factor_tile64(sm);
-      if (!ok && tid == 0 && cols > 0) atomicOr(status, kFlagNotPD);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) t[u][v] = sm.sf[4 * ty + u][4 * tx + v];
-      // diag values for G scaling
-      if (tx == ty) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) sm.rdiag[4 * ty + u] = t[u][u];
-      }
-    } else {
-      // ---- off-diagonal tile: X L_cc^T = t by forward substitution
-      if (tid == 0) wait_flag(flags + c * nt + c);
-      __syncthreads();
-      {
-        const T* lb = a + (long long)c * TB * n + (long long)c * TB;
-        T x[TB * TB / CT];
-#pragma unroll
-        for (int q = 0; q < TB * TB / CT; ++q) {
-          const int e = tid + q * CT, rr = e >> 6, cl = e & 63;
-          x[q] = (rr < cols && cl <= rr) ? ldcg(lb + (long long)rr * n + cl) : T(rr == cl ? 1 : 0);
-        }
-#pragma unroll
-        for (int q = 0; q < TB * TB / CT; ++q) {
-          const int e = tid + q * CT, rr = e >> 6, cl = e & 63;
-          sm.lt[cl][rr] = x[q];  // lt[j][c] = L[c][j]
-        }
-      }
-      __syncthreads();
-      if (tid < TB) sm.rdiag[tid] = T(1) / sm.lt[tid][tid];
-      __syncthreads();
-      const int src0 = lane & 16;
-#pragma unroll 1
-      for (int j0 = 0; j0 < TB; j0 += 4) {
-        const bool own = tx == (j0 >> 2), later = tx > (j0 >> 2);
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int j = j0 + jj;
-          const T rd = sm.rdiag[j];
-          T x[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) x[u] = __shfl_sync(0xffffffffu, t[u][jj] * rd, src0 + (j >> 2));
-          if (own) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) t[u][jj] = x[u];
-          }
-          T l[4];
-          ld4(&sm.lt[j][4 * tx], l);
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            if (later || (own && v > jj)) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u) t[u][v] = fma(-x[u], l[v], t[u][v]);
-            }
-        }
-      }
-      // diag values of L_cc for G scaling: lt[j][j]
-      __syncthreads();
-      if (tid < TB) sm.rdiag[tid] = sm.lt[tid][tid];
+      if (tid == 0) st_release(pflags + 2 * c + (r - c), 1);
+      stamp(item_id, 5);
+      continue;
     }
 
-    stamp(item_id, 4);
-    // ---- store L[r,c], publish
+    // ---- off-diagonal tile: X L_cc^T = t by forward substitution
+    if (tid == 0) wait_flag(flags + c * nt + c);
+    __syncthreads();
     {
-      T* ab = a + (long long)r * TB * n + (long long)c * TB;
+      const T* lb = a + (long long)c * tile + (long long)c * TB;
+      T x[TB * TB / CT];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int rr = 4 * ty + u;
+      for (int q = 0; q < TB * TB / CT; ++q) {
+        const int e = tid + q * CT, rr = e >> 6, cl = e & 63;
+        x[q] = (rr < cols && cl <= rr) ? ldcg(lb + (long long)rr * n + cl) : T(rr == cl ? 1 : 0);
+      }
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int cl = 4 * tx + v;
-          if (rr < rows && cl < cols && (r != c || cl <= rr)) ab[(long long)rr * n + cl] = t[u][v];
-        }
+      for (int q = 0; q < TB * TB / CT; ++q) {
+        const int e = tid + q * CT, rr = e >> 6, cl = e & 63;
+        sm.lt[cl][rr] = x[q];  // lt[j][c] = L[c][j]
       }
     }
+    __syncthreads();
+    if (tid < TB) sm.rdiag[tid] = T(1) / sm.lt[tid][tid];
+    __syncthreads();
+    solve_rows(t, sm);
+    // diag values of L_cc for G scaling: lt[j][j]
+    __syncthreads();
+    if (tid < TB) sm.rdiag[tid] = sm.lt[tid][tid];
+    stamp(item_id, 4);
+    store_t(t, a + (long long)r * tile + (long long)c * TB, n, rows, cols, false);
     __threadfence();
     __syncthreads();
     if (tid == 0) st_release(flags + r * nt + c, 1);
     stamp(item_id, 5);
-    if (gtt) {
-      // diagonal 128 x 128 blocks of G^T in the sweep's lane order (sweep.cu
-      // gp_pos): row i = n-1-b, column k = n-1-a, only when i, k share a block
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long long b = (long long)r * TB + 4 * ty + u;
-        if (b >= n) continue;
-        const long long i = n - 1 - b;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const long long av = (long long)c * TB + 4 * tx + v;
-          if (av >= n || b <= av) continue;
-          const long long k = n - 1 - av;
-          if ((i >> 7) != (k >> 7)) continue;
-          gtt[i * 128 + gp_pos(int(k & 127))] = float(t[u][v] / sm.rdiag[4 * tx + v]);
-        }
-      }
-    }
-    if (ghi) {
-      // rdiag holds L[a][a] of column tile c (written before the last barrier)
-      emit_g(t, sm, sm.rdiag, r, c, n, ghi, glo, gpl);
-    }
+    emit_tile(t, sm, r, c, n, ghi, glo, gpl, gtt);
     __syncthreads();
   }
 }
@@ -719,7 +1031,7 @@ void debug_factor_bench(int iters, long long* cycles, float* out, cudaStream_t s
 
 size_t cholesky_flag_ints(long long n) {
   const long long nt = (n + TB - 1) / TB;
-  return size_t(nt * nt + 64);
+  return size_t(nt * nt + 2 * nt + 64);  // tile flags, partial flags, launch counters
 }
 
 template <typename T>
@@ -751,7 +1063,8 @@ void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, float* gtt, i
   }();
   (void)attr;
   const int nt = int((n + TB - 1) / TB);
-  int* counters = flags + (long long)nt * nt;
+  int* pflags = flags + (long long)nt * nt;
+  int* counters = pflags + 2LL * nt;
   cudaMemsetAsync(flags, 0, cholesky_flag_ints(n) * sizeof(int), st);
   if (gtt) cudaMemsetAsync(gtt, 0, size_t(n) * 128 * sizeof(float), st);  // non-emitted = 0
   int occ = 1;
@@ -762,18 +1075,22 @@ void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, float* gtt, i
   int ci = 0;
   for (int c0 = 0; c0 < nt; c0 += step, ++ci) {
     const int c1 = std::min(nt, c0 + step);
-    long long items = 0;
-    for (int c = c0; c < c1; ++c) items += nt - c;
-    const int grid = int(std::min<long long>(items, max_ctas));
+    long long items = 0;  // worker items; CTA 0 is the owner of the critical path
+    for (int c = c0; c < c1; ++c) items += nt - c + 1;
+    const int grid = 1 + int(std::min<long long>(items, std::max(1, max_ctas - 1)));
     count_launches(1);
     unsigned long long* trace = nullptr;
     const char* tp = getenv("OCWG_CHOL_TRACE");
-    if (tp) cudaMallocAsync(&trace, size_t(items) * 6 * 8, st);
-    chol_tile_kernel<T><<<grid, CT, sizeof(CholSmem<T>), st>>>(a, n, nt, c0, c1, flags,
+    const long long entries = items + 2LL * (c1 - c0);
+    if (tp) {
+      cudaMallocAsync(&trace, size_t(entries) * 6 * 8, st);
+      cudaMemsetAsync(trace, 0, size_t(entries) * 6 * 8, st);
+    }
+    chol_tile_kernel<T><<<grid, CT, sizeof(CholSmem<T>), st>>>(a, n, nt, c0, c1, flags, pflags,
                                                                 counters + ci, status, ghi, glo, gpl,
                                                                 gtt, trace);
     if (tp) {
-      std::vector<unsigned long long> h(size_t(items) * 6);
+      std::vector<unsigned long long> h(size_t(entries) * 6);
       cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       cudaFreeAsync(trace, st);
