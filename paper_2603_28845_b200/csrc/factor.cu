@@ -124,16 +124,18 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
                : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // Raw copy of a 64 x 64 tile (rows x cols valid, row stride n) into dst
 // (row-major, ld 64); 16-byte cp.async when aligned, zero outside.
 template <typename T>
 __device__ __forceinline__ void stage_tile(T* dst, const T* src, long long n, int rows, int cols,
-                                           bool vec_ok) {
+                                           bool vec_ok, int ldd = TB + 4) {
   constexpr int V = 16 / sizeof(T);
   for (int e = threadIdx.x; e < TB * TB / V; e += CT) {
     const int rr = e / (TB / V), cc = (e % (TB / V)) * V;
-    T* d = dst + rr * TB + cc;
+    T* d = dst + rr * ldd + cc;
     if (vec_ok && rr < rows && cc + V <= cols) {
       cp_async16(d, src + (long long)rr * n + cc);
     } else {
@@ -256,16 +258,17 @@ __device__ __forceinline__ void tile_mma(T (&acc)[4][4], const T* Ps, const T* Q
   }
 }
 
+constexpr int LD = TB + 4;  // row stride of the owner's row-major tiles
+
 template <typename T>
 struct CholSmem {
-  T ps[TB * TB];
-  T qs[TB * TB];
-  T lt[TB][TB + 4];   // diag tile L_cc transposed (lt[j][c] = L[c][j]); also G staging
+  T ps[TB * LD];      // workers: swizzled tile_mma operands; owner: row-major tiles (ld LD)
+  T qs[TB * LD];
+  T lt[TB][LD];       // workers: L_cc transposed / G staging; owner: X = L_cc^-T
   T sf[TB][TB + 1];   // diagonal tile being factored
   T wcol[2][72];      // warp elimination: published pivot column (shifted, + zero pad)
   T wcol3[3][2][72];  // the same, per warp, for factor_tile64's three eliminating warps
-  T sb[2][TB * TB + 64];  // owner: staging of the next tiles (raw row-major, cp.async)
-  T lt32[32][40];     // warp elimination: L columns, shifted like wcol (for the solve)
+  T sb[2][TB * LD];   // owner: staged partial tiles (row-major, ld LD, cp.async)
   T rdiag[TB];
   int item;
   int ready;
@@ -469,6 +472,174 @@ __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr) {
   return ok;
 }
 
+// ---- the owner's 64 x 64 x 64 tile products ---------------------------------
+// D = src + sgn * A B'  with B' = B^T (B row-major [j][k]) or, BT, B' = B
+// ([k][j]); A, B, src: row-major ld LD; D: ld ldd (may alias src).  With
+// pad >= 0, D[i][i] = 1 for i >= pad (identity padding of a diagonal tile).
+// fp32: 3xTF32 on the warp-level tensor cores (m16n8k8), warp w computes rows
+// 16 (w & 3).., columns 32 (w >> 2)..: conflict-free fragment loads at ld 68.
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = h;
+  lo = __float_as_uint(x - __uint_as_float(h));
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+template <typename T, bool BT>
+__device__ __forceinline__ void owner_prod(const T* A, const T* B, const T* src, T* D, int ldd,
+                                           T sgn, int pad) {
+  const int tid = threadIdx.x;
+  if constexpr (sizeof(T) == 4) {
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int r0 = 16 * (warp & 3), n0 = 32 * (warp >> 2);
+    float c1[4][4] = {}, c2[4][4] = {};
+#pragma unroll 2
+    for (int k8 = 0; k8 < TB; k8 += 8) {
+      uint32_t ah[4], al[4];
+      split_tf32(A[(r0 + g) * LD + k8 + t], ah[0], al[0]);
+      split_tf32(A[(r0 + g + 8) * LD + k8 + t], ah[1], al[1]);
+      split_tf32(A[(r0 + g) * LD + k8 + t + 4], ah[2], al[2]);
+      split_tf32(A[(r0 + g + 8) * LD + k8 + t + 4], ah[3], al[3]);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int nn = n0 + 8 * nt + g;
+        const float b0 = BT ? B[(k8 + t) * LD + nn] : B[nn * LD + k8 + t];
+        const float b1 = BT ? B[(k8 + t + 4) * LD + nn] : B[nn * LD + k8 + t + 4];
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(b0, bh0, bl0);
+        split_tf32(b1, bh1, bl1);
+        mma_tf32(c1[nt], ah, bh0, bh1);
+        mma_tf32(c2[nt], ah, bl0, bl1);
+        mma_tf32(c2[nt], al, bh0, bh1);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = r0 + g + 8 * (q >> 1), j = n0 + 8 * nt + 2 * t + (q & 1);
+        float v = (src ? src[i * LD + j] : 0.f) + sgn * (c1[nt][q] + c2[nt][q]);
+        if (pad >= 0 && i == j && i >= pad) v = 1.f;
+        D[i * ldd + j] = v;
+      }
+  } else {
+    const int ty = tid >> 4, tx = tid & 15;
+    T acc[4][4] = {};
+    for (int k = 0; k < TB; ++k) {
+      T av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        av[u] = A[(4 * ty + u) * LD + k];
+        bv[u] = BT ? B[k * LD + 4 * tx + u] : B[(4 * tx + u) * LD + k];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i = 4 * ty + u, j = 4 * tx + v;
+        T val = (src ? src[i * LD + j] : T(0)) + sgn * acc[u][v];
+        if (pad >= 0 && i == j && i >= pad) val = T(1);
+        D[i * ldd + j] = val;
+      }
+  }
+}
+
+// Running tile product acc += A B^T over k steps (A, B row-major ld LD), in
+// the tensor-core fragment layout for fp32 (3xTF32), 4x4 register blocks for
+// fp64; acc_store writes it out row-major.
+template <typename T>
+struct TileAcc {
+  T c[4][4];
+};
+template <>
+struct TileAcc<float> {
+  float c1[4][4], c2[4][4];
+};
+template <typename T>
+__device__ __forceinline__ void acc_zero(TileAcc<T>& s) {
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s.c1[i][j] = s.c2[i][j] = 0.f;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s.c[i][j] = T(0);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void acc_mma(TileAcc<T>& s, const T* A, const T* B) {
+  const int tid = threadIdx.x;
+  if constexpr (sizeof(T) == 4) {
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int r0 = 16 * (warp & 3), n0 = 32 * (warp >> 2);
+#pragma unroll 2
+    for (int k8 = 0; k8 < TB; k8 += 8) {
+      uint32_t ah[4], al[4];
+      split_tf32(A[(r0 + g) * LD + k8 + t], ah[0], al[0]);
+      split_tf32(A[(r0 + g + 8) * LD + k8 + t], ah[1], al[1]);
+      split_tf32(A[(r0 + g) * LD + k8 + t + 4], ah[2], al[2]);
+      split_tf32(A[(r0 + g + 8) * LD + k8 + t + 4], ah[3], al[3]);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int nn = n0 + 8 * nt + g;
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(B[nn * LD + k8 + t], bh0, bl0);
+        split_tf32(B[nn * LD + k8 + t + 4], bh1, bl1);
+        mma_tf32(s.c1[nt], ah, bh0, bh1);
+        mma_tf32(s.c2[nt], ah, bl0, bl1);
+        mma_tf32(s.c2[nt], al, bh0, bh1);
+      }
+    }
+  } else {
+    const int ty = tid >> 4, tx = tid & 15;
+    for (int k = 0; k < TB; ++k) {
+      T av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        av[u] = A[(4 * ty + u) * LD + k];
+        bv[u] = B[(4 * tx + u) * LD + k];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) s.c[u][v] = fma(av[u], bv[v], s.c[u][v]);
+    }
+  }
+}
+template <typename T>
+__device__ __forceinline__ void acc_store(const TileAcc<T>& s, T* D, int ldd) {
+  const int tid = threadIdx.x;
+  if constexpr (sizeof(T) == 4) {
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int r0 = 16 * (warp & 3), n0 = 32 * (warp >> 2);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        D[(r0 + g + 8 * (q >> 1)) * ldd + n0 + 8 * nt + 2 * t + (q & 1)] = s.c1[nt][q] + s.c2[nt][q];
+  } else {
+    const int ty = tid >> 4, tx = tid & 15;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) D[(4 * ty + u) * ldd + 4 * tx + v] = s.c[u][v];
+  }
+}
+
 // ---- pieces shared by the owner and the worker CTAs -------------------------
 // t (thread block rows 4ty+u, cols 4tx+v) <- tile at ab; identity padding of a
 // diagonal tile's rows past n
@@ -635,12 +806,12 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
   if (blockIdx.x == 0) {
     if (tid == 0) st_release(owner_sm, int(smid) + 1);
     // ================= owner: the critical path diag(c) -> sub(c+1, c) -> diag(c+1)
-    // Kept in shared memory between columns:
-    //   sm.qs (= sm.ps) : L[c, c-1], transposed / swizzled (tile_mma operand)
-    //   sm.sb[1]        : S'[c, c] (partial) staged by cp.async during column c-1
-    // Tiles are published by warp 7 while the other warps go on (its fence
-    // only stalls itself).
-    bool staged = false;  // sm.sb[1] holds S'[c, c]
+    // Row-major tiles (ld LD) in shared memory:
+    //   qs: L[c, c-1] (kept from the previous column)    ps: L[c+1, c-1] (staged)
+    //   sb[1]: S'[c, c] (partial, staged during column c-1)
+    //   sb[0]: S'[c+1, c] -> S[c+1, c]                    lt: X = L[c,c]^-T
+    // Tiles are published by one thread of warp 7 (its fence only stalls itself).
+    bool staged = false;  // sb[1] holds S'[c, c]
     for (int c = c0; c < c1; ++c) {
       const long long e0 = total + 2LL * (c - c0);
       const int rows = int(std::min<long long>(TB, n - (long long)c * TB));
@@ -657,36 +828,21 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       cp_async_wait_all();
       __syncthreads();
       // S[c,c] = S' - L[c,c-1] L[c,c-1]^T  -> sf (identity padding past n)
-      {
-        T t[4][4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int rr = 4 * ty + u, cl = 4 * tx + v;
-            t[u][v] = (rr == cl && rr >= rows) ? T(1) : sm.sb[1][rr * TB + cl];
-          }
-        if (prev) {
-          T acc[4][4] = {};
-          tile_mma(acc, sm.qs, sm.qs);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) t[u][v] -= acc[u][v];
+      if (prev) {
+        owner_prod<T, false>(sm.qs, sm.qs, sm.sb[1], &sm.sf[0][0], TB + 1, T(-1), rows);
+      } else {
+        for (int e = tid; e < TB * TB; e += CT) {
+          const int i = e >> 6, j = e & 63;
+          sm.sf[i][j] = (i == j && i >= rows) ? T(1) : sm.sb[1][i * LD + j];
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) sm.sf[4 * ty + u][4 * tx + v] = t[u][v];
       }
       // stage S'[c+1,c] and, when already published, L[c+1,c-1]
       if (tid == 0) sm.ready = sub && ld_acquire(pflags + 2 * c + 1);
       if (tid == 32) sm.item = sub && prev && ld_acquire(flags + (c + 1) * nt + (c - 1));
       __syncthreads();
       const bool s_staged = sm.ready, l_staged = sm.item;
-      if (s_staged) stage_tile(sm.sb[1], a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, vec_ok);
-      if (l_staged)
-        stage_tile(sm.sb[0], a + (c + 1) * tile + (long long)(c - 1) * TB, n, rows1, TB, vec_ok);
+      if (s_staged) stage_tile(sm.sb[0], a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, vec_ok);
+      if (l_staged) stage_tile(sm.ps, a + (c + 1) * tile + (long long)(c - 1) * TB, n, rows1, TB, vec_ok);
       stamp(e0, 3);
       const bool ok = factor_tile64<T, true>(sm);  // sm.lt = L[c,c]^-T
       if (!ok && tid == 0 && rows > 0) atomicOr(status, kFlagNotPD);
@@ -696,8 +852,13 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) t[u][v] = sm.sf[4 * ty + u][4 * tx + v];
-        store_t(t, a + c * tile + (long long)c * TB, n, rows, rows, true);
+          for (int v = 0; v < 4; ++v) {
+            const int i = 4 * ty + u, j = 4 * tx + v;
+            t[u][v] = j <= i ? sm.sf[i][j] : sm.lt[i][j];
+          }
+        // lower: L[c,c]; strict upper: X = L[c,c]^-T (the workers' solve operand;
+        // the upper triangle of a diagonal tile is otherwise unused)
+        store_t(t, a + c * tile + (long long)c * TB, n, rows, rows, false);
       }
       // publish: one thread of warp 7 fences (release is cumulative over the
       // CTA's stores ordered by the barrier); the chain warps go on
@@ -709,75 +870,50 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       stamp(e0, 5);
       if (!sub) break;
 
-      // ---- sub tile (c+1, c): S = S' - L[c+1,c-1] L[c,c-1]^T;  X L[c,c]^T = S
+      // ---- sub tile (c+1, c): S = S' - L[c+1,c-1] L[c,c-1]^T;  X = S L[c,c]^-T
       const long long e1 = e0 + 1;
       tag(e1, c + 1, c, kOwner);
       stamp(e1, 2);
       if (!s_staged) {
         if (tid == 0) wait_flag(pflags + 2 * c + 1);
         __syncthreads();
-        stage_tile(sm.sb[1], a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, vec_ok);
+        stage_tile(sm.sb[0], a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, vec_ok);
       }
       if (prev && !l_staged) {
         if (tid == 0) wait_flag(flags + (c + 1) * nt + (c - 1));
         __syncthreads();
-        stage_tile(sm.sb[0], a + (c + 1) * tile + (long long)(c - 1) * TB, n, rows1, TB, vec_ok);
+        stage_tile(sm.ps, a + (c + 1) * tile + (long long)(c - 1) * TB, n, rows1, TB, vec_ok);
       }
       cp_async_wait_all();
       __syncthreads();
-      T t[4][4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) t[u][v] = sm.sb[1][(4 * ty + u) * TB + 4 * tx + v];
       if (prev) {
-        TileRegs<T> P;  // L[c+1,c-1] -> swizzled P operand (ps is free: qs holds L[c,c-1])
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            P.v[ii][e] = sm.sb[0][((tid >> 4) + 16 * ii) * TB + (tid & 15) * 4 + e];
-        store_tile_t(P, sm.ps);
+        owner_prod<T, false>(sm.ps, sm.qs, sm.sb[0], sm.sb[0], LD, T(-1), -1);
         __syncthreads();
-        T acc[4][4] = {};
-        tile_mma(acc, sm.ps, sm.qs);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) t[u][v] -= acc[u][v];
       }
-      // X = S L[c,c]^-T as a tile product: P = S, Q[j][k] = L^-T[k][j] (sm.lt)
-      __syncthreads();  // sb[1], ps, qs consumed
+      stamp(e1, 3);
+      // stage the next column's S'[c+1,c+1] (sb[1] is free) under the product
       if (tid == 0) sm.ready = ld_acquire(pflags + 2 * (c + 1));
-      store_t_swz(t, sm.ps);
-      for (int e = tid; e < TB * TB; e += CT) {
-        const int k = e >> 6, j = e & 63;
-        sm.qs[k * TB + (((j >> 2) ^ ((k >> 2) & 15)) << 2) + (j & 3)] = sm.lt[k][j];
-      }
       __syncthreads();
-      staged = sm.ready;  // stage the next column's S'[c+1,c+1] under the product
+      staged = sm.ready;
       if (staged)
         stage_tile(sm.sb[1], a + (c + 1) * tile + (long long)(c + 1) * TB, n, rows1, rows1, vec_ok);
-      stamp(e1, 3);
+      owner_prod<T, true>(sm.sb[0], &sm.lt[0][0], nullptr, sm.qs, LD, T(1), -1);  // -> L[c+1,c]
+      __syncthreads();
+      stamp(e1, 4);
       {
-        T acc[4][4] = {};
-        tile_mma(acc, sm.ps, sm.qs);
+        T t[4][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) t[u][v] = acc[u][v];
+          for (int v = 0; v < 4; ++v) t[u][v] = sm.qs[(4 * ty + u) * LD + 4 * tx + v];
+        store_t(t, a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, false);
       }
-      stamp(e1, 4);
-      store_t(t, a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, false);
       __syncthreads();
       if (tid == CT - 32) {
         __threadfence();
         st_release(flags + (c + 1) * nt + c, 1);
       }
       stamp(e1, 5);
-      __syncthreads();  // everyone is done reading qs
-      store_t_swz(t, sm.qs);  // next column: L[c+1, c]
-      __syncthreads();
     }
     return;
   }
@@ -837,54 +973,60 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
     const int rows = int(std::min<long long>(TB, n - (long long)r * TB));
     const int kend = partial ? c - 1 : c;  // partial items leave k = c-1 to the owner
 
-    // ---- S = A[r,c] - sum_k L[r,k] L[c,k]^T
-    T acc[4][4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] = T(0);
-    TileRegs<T> P, Q;
+    // ---- S = A[r,c] - sum_k L[r,k] L[c,k]^T: row-major tiles staged by cp.async
+    // (double-buffered while the next k is already published), tensor-core products
+    TileAcc<T> acc;
+    acc_zero(acc);
+    T* const Pb[2] = {sm.ps, sm.sb[0]};
+    T* const Qb[2] = {sm.qs, sm.sb[1]};
     if (c0 < kend) {
       if (tid == 0) {
         wait_flag(flags + r * nt + c0);
         wait_flag(flags + c * nt + c0);
       }
       __syncthreads();
-      load_tile(P, a + (long long)r * tile + (long long)c0 * TB, n, rows, TB, vec_ok);
-      load_tile(Q, a + (long long)c * tile + (long long)c0 * TB, n, cols, TB, vec_ok);
+      stage_tile(Pb[0], a + (long long)r * tile + (long long)c0 * TB, n, rows, TB, vec_ok);
+      stage_tile(Qb[0], a + (long long)c * tile + (long long)c0 * TB, n, cols, TB, vec_ok);
+      cp_async_commit();
     }
-    for (int k = c0; k < kend; ++k) {
-      store_tile_t(P, sm.ps);
-      store_tile_t(Q, sm.qs);
+    int buf = 0;
+    for (int k = c0; k < kend; ++k, buf ^= 1) {
       const bool more = k + 1 < kend;
       const int* fr = flags + r * nt + k + 1;
       const int* fc = flags + c * nt + k + 1;
       if (tid == 0) sm.ready = more && ld_acquire(fr) && ld_acquire(fc);
-      __syncthreads();
+      __syncthreads();  // (also: everyone is done with buffer buf ^ 1)
       const bool ready = sm.ready;
-      // prefetch k+1 under the MMA when its tiles are already published
-      if (ready) {
-        load_tile(P, a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
-        load_tile(Q, a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+      if (ready) {  // prefetch k+1 under this product
+        stage_tile(Pb[buf ^ 1], a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
+        stage_tile(Qb[buf ^ 1], a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+        cp_async_commit();
+        cp_async_wait_1();
+      } else {
+        cp_async_wait_all();
       }
-      tile_mma(acc, sm.ps, sm.qs);
+      __syncthreads();
+      acc_mma(acc, Pb[buf], Qb[buf]);
       if (more && !ready) {  // at the dependency frontier: wait, then load
         if (tid == 0) {
           wait_flag(fr);
           wait_flag(fc);
         }
         __syncthreads();
-        load_tile(P, a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
-        load_tile(Q, a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+        stage_tile(Pb[buf ^ 1], a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
+        stage_tile(Qb[buf ^ 1], a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+        cp_async_commit();
       }
-      __syncthreads();
     }
+    __syncthreads();
+    acc_store(acc, &sm.sf[0][0], TB + 1);
     T t[4][4];
     load_t(t, a + (long long)r * tile + (long long)c * TB, n, rows, cols, false, vec_ok);
+    __syncthreads();
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) t[u][v] -= acc[u][v];
+      for (int v = 0; v < 4; ++v) t[u][v] -= sm.sf[4 * ty + u][4 * tx + v];
     stamp(item_id, 3);
 
     if (partial) {
@@ -896,30 +1038,30 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       continue;
     }
 
-    // ---- off-diagonal tile: X L_cc^T = t by forward substitution
+    // ---- off-diagonal tile: X = S L[c,c]^-T, with L^-T from the diagonal
+    // tile's upper triangle (written by the owner; its diagonal is 1 / L[j][j])
     if (tid == 0) wait_flag(flags + c * nt + c);
     __syncthreads();
-    {
-      const T* lb = a + (long long)c * tile + (long long)c * TB;
-      T x[TB * TB / CT];
+    stage_tile(sm.ps, a + (long long)c * tile + (long long)c * TB, n, cols, cols, vec_ok);
 #pragma unroll
-      for (int q = 0; q < TB * TB / CT; ++q) {
-        const int e = tid + q * CT, rr = e >> 6, cl = e & 63;
-        x[q] = (rr < cols && cl <= rr) ? ldcg(lb + (long long)rr * n + cl) : T(rr == cl ? 1 : 0);
-      }
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int q = 0; q < TB * TB / CT; ++q) {
-        const int e = tid + q * CT, rr = e >> 6, cl = e & 63;
-        sm.lt[cl][rr] = x[q];  // lt[j][c] = L[c][j]
-      }
+      for (int v = 0; v < 4; ++v) sm.sb[0][(4 * ty + u) * LD + 4 * tx + v] = t[u][v];
+    cp_async_wait_all();
+    __syncthreads();
+    for (int e = tid; e < TB * TB; e += CT) {  // qs = X (row-major [k][j]), rdiag = L[j][j]
+      const int i = e >> 6, j = e & 63;
+      const T d = sm.ps[i * LD + i];
+      sm.qs[i * LD + j] = j > i ? sm.ps[i * LD + j] : (j == i ? (i < cols ? T(1) / d : T(1)) : T(0));
+      if (j == 0) sm.rdiag[i] = i < cols ? d : T(1);
     }
     __syncthreads();
-    if (tid < TB) sm.rdiag[tid] = T(1) / sm.lt[tid][tid];
+    owner_prod<T, true>(sm.sb[0], sm.qs, nullptr, &sm.sf[0][0], TB + 1, T(1), -1);
     __syncthreads();
-    solve_rows(t, sm);
-    // diag values of L_cc for G scaling: lt[j][j]
-    __syncthreads();
-    if (tid < TB) sm.rdiag[tid] = sm.lt[tid][tid];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) t[u][v] = sm.sf[4 * ty + u][4 * tx + v];
     stamp(item_id, 4);
     store_t(t, a + (long long)r * tile + (long long)c * TB, n, rows, cols, false);
     __threadfence();
