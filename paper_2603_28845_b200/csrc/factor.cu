@@ -272,6 +272,7 @@ struct CholSmem {
   T rdiag[TB];
   int item;
   int ready;
+  int stg[3];  // owner: which tiles the factor's idle warps staged
 };
 
 // Publish the finalised tile (values in t, rows b = 64r + 4ty + u, cols
@@ -387,8 +388,13 @@ __device__ __forceinline__ bool warp_chol32(T (&a)[32], T (&b)[32], T* out_row, 
 //          [INV] warps 1, 2 carry X rows 0-31 / identity rows 32-63.
 // With INV, sm.lt receives X = L^-T (upper triangular, ld TB + 4).  Upper
 // entries of sf are zeroed; sm.rdiag gets 1 / L[j][j].  All threads call.
-template <typename T, bool INV = false>
-__device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr) {
+struct NoSide {
+  __device__ void operator()() const {}
+};
+// Side: work for the warps the eliminations leave idle (warps 3-7 call it once,
+// at the start of h = 0).
+template <typename T, bool INV = false, typename Side = NoSide>
+__device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr, const Side& side = Side()) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   bool ok = true;
   auto pstamp = [&](int i) {
@@ -401,6 +407,7 @@ __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr) {
   for (int h = 0; h < 2; ++h) {
     const int o = 32 * h;  // diagonal block [o, o+32)
     const bool active = warp == 0 || (warp == 2 && h == 0) || (INV && warp <= 2);
+    if (h == 0 && warp >= 3) side();
     // (votes make the warp-uniform branches visible to ptxas: no divergent-shuffle
     // fallback paths, which would pin the loads behind branch checks)
     if (__any_sync(0xffffffffu, active)) {
@@ -836,16 +843,41 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
           sm.sf[i][j] = (i == j && i >= rows) ? T(1) : sm.sb[1][i * LD + j];
         }
       }
-      // stage S'[c+1,c] and, when already published, L[c+1,c-1]
-      if (tid == 0) sm.ready = sub && ld_acquire(pflags + 2 * c + 1);
-      if (tid == 32) sm.item = sub && prev && ld_acquire(flags + (c + 1) * nt + (c - 1));
       __syncthreads();
-      const bool s_staged = sm.ready, l_staged = sm.item;
-      if (s_staged) stage_tile(sm.sb[0], a + (c + 1) * tile + (long long)c * TB, n, rows1, TB, vec_ok);
-      if (l_staged) stage_tile(sm.ps, a + (c + 1) * tile + (long long)(c - 1) * TB, n, rows1, TB, vec_ok);
       stamp(e0, 3);
-      const bool ok = factor_tile64<T, true>(sm);  // sm.lt = L[c,c]^-T
+      // the factor's idle warps (3-7) stage what is already published: S'[c+1,c],
+      // L[c+1,c-1] and the next column's S'[c+1,c+1] (sm.stg bits tell which)
+      auto side = [&]() {
+        const int st = tid - 96;  // 0..159
+        if (st == 0) sm.stg[0] = sub && ld_acquire(pflags + 2 * c + 1);
+        if (st == 32) sm.stg[1] = sub && prev && ld_acquire(flags + (c + 1) * nt + (c - 1));
+        if (st == 64) sm.stg[2] = sub && ld_acquire(pflags + 2 * (c + 1));
+        asm volatile("bar.sync 1, 160;" ::: "memory");
+        constexpr int V = 16 / sizeof(T);
+        const T* src[3] = {a + (c + 1) * tile + (long long)c * TB,
+                           a + (c + 1) * tile + (long long)(c - 1) * TB,
+                           a + (c + 1) * tile + (long long)(c + 1) * TB};
+        T* dst[3] = {sm.sb[0], sm.ps, sm.sb[1]};
+        const int rws[3] = {rows1, rows1, rows1};
+        const int cls[3] = {TB, TB, rows1};
+        for (int q = 0; q < 3; ++q) {
+          if (!sm.stg[q]) continue;
+          for (int e = st; e < TB * TB / V; e += 160) {
+            const int rr = e / (TB / V), cc = (e % (TB / V)) * V;
+            T* d = dst[q] + rr * LD + cc;
+            if (vec_ok && rr < rws[q] && cc + V <= cls[q]) {
+              cp_async16(d, src[q] + (long long)rr * n + cc);
+            } else {
+#pragma unroll
+              for (int u = 0; u < V; ++u)
+                d[u] = (rr < rws[q] && cc + u < cls[q]) ? ldcg(src[q] + (long long)rr * n + cc + u) : T(0);
+            }
+          }
+        }
+      };
+      const bool ok = factor_tile64<T, true>(sm, nullptr, side);  // sm.lt = L[c,c]^-T
       if (!ok && tid == 0 && rows > 0) atomicOr(status, kFlagNotPD);
+      const bool s_staged = sm.stg[0], l_staged = sm.stg[1];
       stamp(e0, 4);
       {
         T t[4][4];
@@ -891,12 +923,7 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
         __syncthreads();
       }
       stamp(e1, 3);
-      // stage the next column's S'[c+1,c+1] (sb[1] is free) under the product
-      if (tid == 0) sm.ready = ld_acquire(pflags + 2 * (c + 1));
-      __syncthreads();
-      staged = sm.ready;
-      if (staged)
-        stage_tile(sm.sb[1], a + (c + 1) * tile + (long long)(c + 1) * TB, n, rows1, rows1, vec_ok);
+      staged = sm.stg[2];  // the next column's S'[c+1,c+1], staged under the factor
       owner_prod<T, true>(sm.sb[0], &sm.lt[0][0], nullptr, sm.qs, LD, T(1), -1);  // -> L[c+1,c]
       __syncthreads();
       stamp(e1, 4);
@@ -990,13 +1017,23 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       cp_async_commit();
     }
     int buf = 0;
+    int horizon = c0 + 1;  // every k < horizon is known to be published
     for (int k = c0; k < kend; ++k, buf ^= 1) {
       const bool more = k + 1 < kend;
       const int* fr = flags + r * nt + k + 1;
       const int* fc = flags + c * nt + k + 1;
-      if (tid == 0) sm.ready = more && ld_acquire(fr) && ld_acquire(fc);
+      const bool probe = more && k + 1 >= horizon;
+      if (probe && tid < 64) {
+        // refresh the horizon: warps 0 / 1 probe the next 32 k of row r / row c
+        // (one acquire round trip, all in parallel)
+        const int kk = k + 1 + (tid & 31);
+        const int* f = flags + (tid < 32 ? r : c) * nt + kk;
+        const unsigned bal = __ballot_sync(0xffffffffu, kk < kend && ld_acquire(f));
+        if ((tid & 31) == 0) sm.stg[tid >> 5] = ~bal ? __ffs(~bal) - 1 : 32;
+      }
       __syncthreads();  // (also: everyone is done with buffer buf ^ 1)
-      const bool ready = sm.ready;
+      if (probe) horizon = k + 1 + min(sm.stg[0], sm.stg[1]);
+      const bool ready = more && k + 1 < horizon;
       if (ready) {  // prefetch k+1 under this product
         stage_tile(Pb[buf ^ 1], a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
         stage_tile(Qb[buf ^ 1], a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
@@ -1008,11 +1045,10 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       __syncthreads();
       acc_mma(acc, Pb[buf], Qb[buf]);
       if (more && !ready) {  // at the dependency frontier: wait, then load
-        if (tid == 0) {
-          wait_flag(fr);
-          wait_flag(fc);
-        }
+        if (tid == 0) wait_flag(fr);
+        if (tid == 32) wait_flag(fc);
         __syncthreads();
+        horizon = k + 2;
         stage_tile(Pb[buf ^ 1], a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
         stage_tile(Qb[buf ^ 1], a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
         cp_async_commit();

@@ -36,3 +36,16 @@ for name, v in seg:
 late = [max(0, pb[par[(k, k)]] - st[D[k]]) for k in range(1, nt) if (k, k) in par]
 late1 = [max(0, pb[par[(k + 1, k)]] - st[S[k]]) for k in range(1, nt - 1) if (k + 1, k) in par]
 print(f"  partial diag published after owner start: mean {np.mean(late) / 1e3:.2f} us; partial sub: {np.mean(late1) / 1e3:.2f} us")
+pdi = np.array([par[(k, k)] for k in range(2, nt) if (k, k) in par])
+kk = c[pdi]
+dur = (kd[pdi] - st[pdi]) / 1e3
+print(f"  partial diag items: k-loop time mean {dur.mean():.1f} us, per k-step {np.mean(dur / np.maximum(kk - 1, 1)):.2f} us;"
+      f" start before owner needs it: mean {np.mean(st[D[kk]] - st[pdi]) / 1e3:.1f} us")
+fi = np.where((kind == 0) & (c >= 8))[0]
+per = (kd[fi] - st[fi]) / np.maximum(c[fi], 1) / 1e3
+print(f"  full items (c >= 8): k-loop per k-step min {per.min():.2f} p10 {np.percentile(per, 10):.2f} us; "
+      f"dispatch-to-owner lead (column c) mean {np.mean(st[D[c[fi]]] - st[fi]) / 1e3:.1f} us")
+print(f"  full items (c >= 8): k-loop per k-step mean {per.mean():.2f} us, median {np.median(per):.2f}; "
+      f"solve+publish mean {np.mean(pb[fi] - kd[fi]) / 1e3:.2f} us; items {len(fi)}")
+busy = np.sum(pb[kind < 3] - st[kind < 3]) / 1e3
+print(f"  worker busy time {busy:.0f} us over span {pb.max() / 1e3:.0f} us -> {busy / (pb.max() / 1e3):.0f} CTAs busy on average")
