@@ -742,7 +742,16 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
       const long long kk = se - s0;
       bool done = false;
       if constexpr (sizeof(T) == 4) {
-        if (split)
+        static const bool pairs = [] {  // OCWG_SWEEP_GEMM2=0: 1-SM 128 x 128 tiles
+          const char* e = getenv("OCWG_SWEEP_GEMM2");
+          return !(e && e[0] == '0');
+        }();
+        if (split && pairs)
+          done = tc_gemm2_presplit(n - se, m, kk, 1.0f,
+                                   reinterpret_cast<const float*>(ghi) + se * n + s0,
+                                   glo + se * n + s0, n, dhi[p], dlo[p], kSuperRows, float(beta),
+                                   reinterpret_cast<float*>(acc) + se * m, m, st);
+        if (split && !done)
           done = tc_gemm_presplit(n - se, m, kk, 1.0f,
                                   reinterpret_cast<const float*>(ghi) + se * n + s0,
                                   glo + se * n + s0, n, dhi[p], dlo[p], kSuperRows, float(beta),
