@@ -296,7 +296,9 @@ def main():
             buf = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
             return buf.numpy().view(dtype).reshape(shape)
 
-        outs = g.LayerOutputs(N_IN, M_OUT, cfg, alloc=pinned, with_h=False)
+        # the reference quantize_layer's outputs (codes + grids, layerwise.cpp:120-126)
+        # plus the OCW1 payload; W_hat is dequantize(), a separate call
+        outs = g.LayerOutputs(N_IN, M_OUT, cfg, alloc=pinned, with_h=False, with_w_hat=False)
         g.quantize_layer_x(wb, xb, cfg, opts, out=outs)  # warm (allocations)
         times = []
         for _ in range(args.e2e_steps):
@@ -307,11 +309,12 @@ def main():
         t_e2e = statistics.mean(times)
         h2d = TOKENS * N_IN * 2 + N_IN * M_OUT * 4
         ng = N_IN * (M_OUT // GROUP)
-        d2h = N_IN * M_OUT * 2 + ng * 8 + N_IN * M_OUT * 4 + len(payload)
+        d2h = N_IN * M_OUT * 2 + ng * 8 + len(payload)
         e2e = {"value": world * N_IN * M_OUT / t_e2e, "unit": "weights/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e * 1e3,
                "api": "paper_2603_28845_b200.quantize_layer_x -> ocwg_quantize_layer_x (host buffers: "
-                      "W, X in; codes, scales, zeros, W_hat, payload out; X streamed in 32768-token "
+                      "W, X in; codes, scales, zeros, payload out -- the reference quantize_layer's result plus the "
+                      "OCW1 payload; X streamed in 32768-token "
                       "chunks under the Hessian)"}
 
     if rank != 0:

@@ -173,6 +173,20 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
                           const ocwg_gptq_options* opts, int scale_mode, int16_t* codes,
                           float* scales, int32_t* zeros, float* w_hat, uint8_t* payload,
                           uint64_t payload_len, float* h_out);
+/* ---- layers sharing one calibration input (the sweep
+ * driver's q/k/v and gate/up groups, run_layerwise_sweep pipeline.cpp:215-226
+ * and model.cpp:301-307) -- `count` weights W_i (N x M_i fp32, host) that see
+ * the same X (T x N bf16, host): ONE Hessian, one order + factorisation (they
+ * depend on H only, layerwise.cpp:31-51), then one grid + sweep + pack per W.
+ * Results equal `count` separate ocwg_quantize_layer_x calls bit for bit.
+ * Per-layer outputs codes[i] (N x M_i), scales[i], zeros[i], payload[i]
+ * (payload_len[i] bytes); any output pointer may be NULL. */
+int ocwg_quantize_layers_x(ocwg_ctx* ctx, int count, const float* const* w, const uint64_t* m,
+                           const uint16_t* x, uint64_t tokens, uint64_t n,
+                           const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
+                           int scale_mode, int16_t* const* codes, float* const* scales,
+                           int32_t* const* zeros, uint8_t* const* payload,
+                           const uint64_t* payload_len);
 /* Same with every pointer in device memory (inputs resident in HBM). */
 int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint64_t tokens,
                               uint64_t n, uint64_t m, const ocwg_quant_config* cfg,

@@ -211,6 +211,8 @@ _SIGS = {
                                       C.POINTER(_GOpt), C.c_int, C.c_int, _P, _P, _P, _P]),
     "ocwg_quantize_layer_x": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, C.POINTER(_QCfg),
                                         C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P, _U64, _P]),
+    "ocwg_quantize_layers_x": (C.c_int, [_P, C.c_int, _P, _P, _P, _U64, _U64, C.POINTER(_QCfg),
+                                         C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P]),
     "ocwg_quantize_layer_x_dev": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, C.POINTER(_QCfg),
                                             C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P, _P]),
     "ocwg_hessian_bf16_dev": (C.c_int, [_P, _P, _U64, _U64, _P, C.c_int]),
@@ -498,15 +500,59 @@ class LayerOutputs:
     """Caller-owned host buffers for quantize_layer_x (e.g. views of pinned
     memory, so the device-to-host copies run at full PCIe rate)."""
 
-    def __init__(self, n: int, m: int, cfg: QuantConfig, alloc=np.zeros, with_h: bool = True):
+    def __init__(self, n: int, m: int, cfg: QuantConfig, alloc=np.zeros, with_h: bool = True,
+                 with_w_hat: bool = True):
         ng = quant_group_count(cfg, n, m)
         self.payload_bytes = uniform_storage_bytes(cfg, n, m)
         self.codes = alloc((n, m), np.int16)
         self.scales = alloc(ng, np.float32)
         self.zeros = alloc(ng, np.int32)
-        self.w_hat = alloc((n, m), np.float32)
+        # (the reference's quantize_layer returns codes + grids; W_hat is the
+        # separate dequantize(), so it is optional here)
+        self.w_hat = alloc((n, m), np.float32) if with_w_hat else None
         self.payload = alloc(max(self.payload_bytes, 1), np.uint8)
         self.h = alloc((n, n), np.float32) if with_h else None
+
+
+def quantize_layers_x(ws, x_bf16_bits, cfg: QuantConfig, opts: GptqOptions,
+                      mode: ScaleMode = ScaleMode.minmax, device: int = 0):
+    """Layers that share one calibration input (q/k/v, gate/up):
+    one Hessian and one factorisation, then a sweep per W.  Returns one
+    (QuantizedMatrix, payload bytes) per W, equal to separate quantize_layer_x
+    calls."""
+    ws = [_f32(w) for w in ws]
+    x = np.ascontiguousarray(x_bf16_bits, np.uint16)
+    if not ws:
+        raise InvalidInput("quantize_layers_x: no layers")
+    n = ws[0].shape[0]
+    if any(w.shape[0] != n for w in ws) or x.shape[1] != n:
+        raise InvalidInput("quantize_layers_x: every W must be N x M_i with N = columns of X")
+    k = len(ws)
+    outs = []
+    for w in ws:
+        m = w.shape[1]
+        ng = quant_group_count(cfg, n, m)
+        outs.append((np.zeros((n, m), np.int16), np.zeros(ng, np.float32), np.zeros(ng, np.int32),
+                     np.zeros(max(uniform_storage_bytes(cfg, n, m), 1), np.uint8)))
+    arr = lambda vals, t: (t * k)(*vals)  # noqa: E731
+    wp = arr([w.ctypes.data for w in ws], C.c_void_p)
+    mp = arr([w.shape[1] for w in ws], C.c_uint64)
+    cp = arr([o[0].ctypes.data for o in outs], C.c_void_p)
+    sp = arr([o[1].ctypes.data for o in outs], C.c_void_p)
+    zp = arr([o[2].ctypes.data for o in outs], C.c_void_p)
+    pp = arr([o[3].ctypes.data for o in outs], C.c_void_p)
+    pl = arr([o[3].size for o in outs], C.c_uint64)
+    c, o = cfg._c(), opts._c()
+    _check(lib().ocwg_quantize_layers_x(context(device).handle, k, C.cast(wp, C.c_void_p),
+                                        C.cast(mp, C.c_void_p), _ptr(x), x.shape[0], n,
+                                        C.byref(c), C.byref(o), int(mode), C.cast(cp, C.c_void_p),
+                                        C.cast(sp, C.c_void_p), C.cast(zp, C.c_void_p),
+                                        C.cast(pp, C.c_void_p), C.cast(pl, C.c_void_p)))
+    res = []
+    for w, (codes, s_, z_, pay) in zip(ws, outs):
+        pb = uniform_storage_bytes(cfg, n, w.shape[1])
+        res.append((QuantizedMatrix(n, w.shape[1], cfg, codes, s_, z_), pay[:pb].tobytes()))
+    return res
 
 
 def quantize_layer_x(w, x_bf16_bits, cfg: QuantConfig, opts: GptqOptions,

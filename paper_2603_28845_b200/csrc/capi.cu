@@ -1092,4 +1092,106 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
   });
 }
 
+int ocwg_quantize_layers_x(ocwg_ctx* ctx, int count, const float* const* w, const uint64_t* m,
+                           const uint16_t* x, uint64_t tokens, uint64_t n,
+                           const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
+                           int mode, int16_t* const* codes, float* const* scales,
+                           int32_t* const* zeros, uint8_t* const* payload,
+                           const uint64_t* payload_len) {
+  return guard([&] {
+    if (count < 1 || !w || !m) fail(OCWG_INVALID_INPUT, "quantize_layers_x: no layers");
+    uint64_t mmax = 0;
+    for (int i = 0; i < count; ++i) {
+      check_gptq_args(cfg, opts, n, m[i]);
+      if (n == 0 || m[i] == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
+      if (payload && payload[i] && (!payload_len || payload_len[i] < storage_bytes(cfg, n, m[i])))
+        fail(OCWG_INVALID_INPUT, "payload buffer too small");
+      mmax = std::max(mmax, m[i]);
+    }
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    cudaStream_t st = ctx->stream;
+    const uint64_t ngmax = group_count(cfg, n, mmax), pbmax = storage_bytes(cfg, n, mmax);
+    size_t off = 0;
+    auto take = [&](size_t b) {
+      const size_t o = off;
+      off += (b + 255) & ~size_t(255);
+      return o;
+    };
+    const size_t ow = take(n * mmax * 4), ox = take(std::max<uint64_t>(1, tokens) * n * 2),
+                 oc = take(n * mmax * 2), os = take(ngmax * 4), oz = take(ngmax * 4),
+                 opl = take(pbmax), oh = take(n * n * 4);
+    if (off > ctx->io_bytes) {
+      ck(cudaStreamSynchronize(st), "sync");
+      if (ctx->io) cudaFree(ctx->io);
+      ctx->io = nullptr;
+      ctx->io_bytes = 0;
+      ck(cudaMalloc(&ctx->io, off), "cudaMalloc(io)");
+      ctx->io_bytes = off;
+    }
+    char* io = static_cast<char*>(ctx->io);
+    float* wd = reinterpret_cast<float*>(io + ow);
+    uint16_t* xd = reinterpret_cast<uint16_t*>(io + ox);
+    int16_t* cd = reinterpret_cast<int16_t*>(io + oc);
+    float* sd = reinterpret_cast<float*>(io + os);
+    int32_t* zd = reinterpret_cast<int32_t*>(io + oz);
+    uint8_t* pd = reinterpret_cast<uint8_t*>(io + opl);
+    float* hd = reinterpret_cast<float*>(io + oh);
+    Arena ar(ctx);
+    size_t o[11];
+    gptq_reserve(ar, ctx, n, mmax, o);
+    const size_t om = ar.reserve(4096 * 4);
+    const long long chunk = 32768;
+    const size_t hws = hessian_tc_workspace_bytes(std::min<long long>(chunk, (long long)tokens),
+                                                  (long long)n);
+    const size_t ohw = ar.reserve(hws);
+    ar.commit();
+    const GptqBufs b = gptq_bufs(ar, ctx, o, n, mmax);
+    // ---- H = X^T X, X streamed chunk by chunk under the Hessian (as quantize_layer_x)
+    const long long nchunks = tokens ? ((long long)tokens + chunk - 1) / chunk : 0;
+    while ((long long)ctx->cev.size() < nchunks + 2) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      ctx->cev.push_back(e);
+    }
+    ck(cudaEventRecord(ctx->cev[0], st), "event");
+    ck(cudaStreamWaitEvent(ctx->cpy, ctx->cev[0], 0), "event");
+    if (tokens == 0) ck(cudaMemsetAsync(hd, 0, n * n * 4, st), "memset");
+    for (long long k = 0; k < nchunks; ++k) {
+      const long long t0 = k * chunk, tc = std::min<long long>(chunk, (long long)tokens - t0);
+      ck(cudaMemcpyAsync(xd + t0 * n, x + t0 * n, size_t(tc) * n * 2, cudaMemcpyHostToDevice,
+                         ctx->cpy),
+         "H2D(X)");
+      ck(cudaEventRecord(ctx->cev[2 + k], ctx->cpy), "event");
+      ck(cudaStreamWaitEvent(st, ctx->cev[2 + k], 0), "event");
+      const int r = hessian_tc(xd + t0 * n, tc, (long long)n, hd, k > 0 ? 1 : 0, ar.at<void>(ohw),
+                               hws, st);
+      if (r == -1) hessian_simt(xd + t0 * n, tc, (long long)n, hd, k > 0 ? 1 : 0, st);
+      else if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
+    }
+    // ---- one order + factorisation for every layer
+    run_factor(ctx, hd, n, opts->actorder, opts->percdamp, b);
+    // ---- per layer: W in, grids + sweep + pack, results out
+    for (int i = 0; i < count; ++i) {
+      const uint64_t mi = m[i];
+      const QCfg c = qcfg(cfg, mi);
+      const uint64_t ng = group_count(cfg, n, mi), pb = storage_bytes(cfg, n, mi);
+      ck(cudaMemcpyAsync(wd, w[i], n * mi * 4, cudaMemcpyHostToDevice, st), "H2D(W)");
+      launch_calibrate_grids(wd, (long long)n, (long long)mi, (long long)mi, c, mode, sd, zd,
+                             ctx->flag, ar.at<float>(om), st);
+      if (ctx->precision == OCWG_FP64)
+        run_sweep_t<double>(ctx, wd, mi, n, mi, c, opts, cd, sd, zd, nullptr, b);
+      else
+        run_sweep_t<float>(ctx, wd, mi, n, mi, c, opts, cd, sd, zd, nullptr, b);
+      const bool pk = payload && payload[i];
+      if (pk) launch_pack(cd, (long long)(n * mi), (long long)ng, c, sd, zd, pd, st);
+      if (codes && codes[i]) d2h(codes[i], cd, n * mi * 2, ctx);
+      if (scales && scales[i]) d2h(scales[i], sd, ng * 4, ctx);
+      if (zeros && zeros[i]) d2h(zeros[i], zd, ng * 4, ctx);
+      if (pk) d2h(payload[i], pd, pb, ctx);
+    }
+    finish(ctx);
+  });
+}
+
 }  // extern "C"
