@@ -107,6 +107,14 @@ int ocwg_calibrate_grids(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t 
                          const ocwg_quant_config* cfg, int scale_mode, float* scales,
                          int32_t* zeros);
 /* quantize_matrix (quant.cpp:198-210): codes int16 row-major */
+/* AutoBit's default candidate grid (autobit.cpp:45-61 candidate_grid with
+ * estimate_error :16-34): RTN error of W (rows x cols, host) under bits 2..8 x
+ * {per_group 128, per_channel}, symmetric -- errors[14] / cost_bytes[14] in
+ * the reference's order (bits ascending, grouped first), one pass over W on
+ * the GPU.  mode 0 naive ||dW||^2; 1 act-aware 1/2 sum_ij in_diag[i] dW_ij^2
+ * (in_diag: rows doubles, NULL = ones).  SURVEY §8 f3. */
+int ocwg_candidate_grid(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t cols, int mode,
+                        const double* in_diag, double* errors, uint64_t* cost_bytes);
 int ocwg_quantize_matrix(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t cols,
                          const ocwg_quant_config* cfg, int scale_mode, int16_t* codes,
                          float* scales, int32_t* zeros);

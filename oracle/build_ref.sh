@@ -23,7 +23,10 @@ mkdir -p "$OUT"
 CXX=${CXX:-g++}
 FLAGS="-std=c++20 -O2 -fPIC -Wall -Wextra -Wno-unused-parameter -I$REF/include -I$ROOT/paper_2603_28845_b200/compat -I$HERE/shim"
 SRCS="$REF/src/matrix.cpp $REF/src/quant.cpp $REF/src/stats.cpp $REF/src/layerwise.cpp"
-$CXX $FLAGS -shared -o "$OUT/libocw_ref.so" $SRCS "$HERE/ref_capi.cpp" -ldl
+# autobit.cpp (candidate_grid / estimate_error) uses std::function
+# without including <functional>; it is force-included, the source is unmodified
+$CXX $FLAGS -shared -o "$OUT/libocw_ref.so" $SRCS "$REF/src/autobit.cpp" -include functional \
+    "$HERE/ref_capi.cpp" -ldl
 for t in test_core test_layerwise; do
   $CXX $FLAGS -o "$OUT/ref_$t" "$REF/tests/test_main.cpp" "$REF/tests/$t.cpp" $SRCS -ldl
 done

@@ -28,6 +28,7 @@ _SIGS = {
     "ocwref_random_gaussian": (_I, [_U64, _U64, _U64, C.c_float, _P]),
     "ocwref_calibrate_grids": (_I, [_P, _U64, _U64, _I, _I, _I, _U64, _I, _P, _P]),
     "ocwref_quantize_matrix": (_I, [_P, _U64, _U64, _I, _I, _I, _U64, _I, _P, _P, _P]),
+    "ocwref_candidate_grid": (_I, [_P, _U64, _U64, _I, _P, _P, _P]),
     "ocwref_dequantize": (_I, [_P, _P, _P, _U64, _U64, _I, _I, _I, _U64, _P]),
     "ocwref_activation_objective": (_I, [_P, _P, _P, _U64, _U64, _P]),
     "ocwref_gptq_order": (_I, [_P, _U64, _I, _P]),
@@ -139,6 +140,16 @@ def gptq_order(h, actorder: bool) -> np.ndarray:
     out = np.zeros(h.shape[0], np.int64)
     _ck(lib().ocwref_gptq_order(_p(h), h.shape[0], int(actorder), _p(out)))
     return out
+
+
+def candidate_grid(w, mode=0, in_diag=None):
+    """autobit.cpp:45-61: (errors[14], cost_bytes[14]) of the default grid."""
+    w = _f32(w)
+    errs, costs = np.zeros(14), np.zeros(14, np.uint64)
+    d = None if in_diag is None else np.ascontiguousarray(in_diag, np.float64)
+    _ck(lib().ocwref_candidate_grid(_p(w), w.shape[0], w.shape[1], int(mode),
+                                    None if d is None else _p(d), _p(errs), _p(costs)))
+    return errs, costs
 
 
 def gptq_quantize(w, h, bits, scheme, gran, group, actorder=False, percdamp=0.01, block=32,

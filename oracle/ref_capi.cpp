@@ -18,6 +18,7 @@
 #include "ocw/errors.hpp"
 #include "ocw/eigen_map.hpp"
 #include "ocw/layerwise.hpp"
+#include "ocw/autobit.hpp"
 #include "ocw/quant.hpp"
 #include "ocw/stats.hpp"
 
@@ -136,6 +137,23 @@ int ocwref_quantize_matrix(const float* w, size_t rows, size_t cols, int bits, i
     auto q = ocw::quantize_matrix(to_matrix(w, rows, cols), make_cfg(bits, scheme, gran, group),
                                   mse ? ocw::ScaleMode::mse_grid : ocw::ScaleMode::minmax);
     export_q(q, codes, scales, zeros);
+  });
+}
+
+// autobit.cpp:45-61 (candidate_grid) with estimate_error :16-34: errors and
+// storage costs of bits {2..8} x {per_group 128, per_channel}, symmetric
+int ocwref_candidate_grid(const float* w, size_t rows, size_t cols, int mode,
+                          const double* in_diag, double* errs, size_t* costs) {
+  return guard([&] {
+    std::vector<double> diag;
+    if (in_diag) diag.assign(in_diag, in_diag + rows);
+    auto cands = ocw::candidate_grid(to_matrix(w, rows, cols),
+                                     mode ? ocw::ErrorMode::act_aware : ocw::ErrorMode::naive,
+                                     in_diag ? &diag : nullptr);
+    for (size_t k = 0; k < cands.size(); ++k) {
+      errs[k] = cands[k].err;
+      costs[k] = cands[k].cost_bytes;
+    }
   });
 }
 

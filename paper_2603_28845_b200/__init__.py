@@ -211,6 +211,7 @@ _SIGS = {
                                       C.POINTER(_GOpt), C.c_int, C.c_int, _P, _P, _P, _P]),
     "ocwg_quantize_layer_x": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, C.POINTER(_QCfg),
                                         C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P, _U64, _P]),
+    "ocwg_candidate_grid": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _P, _P, _P]),
     "ocwg_quantize_layers_x": (C.c_int, [_P, C.c_int, _P, _P, _P, _U64, _U64, C.POINTER(_QCfg),
                                          C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P]),
     "ocwg_quantize_layer_x_dev": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, C.POINTER(_QCfg),
@@ -512,6 +513,31 @@ class LayerOutputs:
         self.w_hat = alloc((n, m), np.float32) if with_w_hat else None
         self.payload = alloc(max(self.payload_bytes, 1), np.uint8)
         self.h = alloc((n, n), np.float32) if with_h else None
+
+
+def candidate_grid(w, mode: str = "naive", in_diag=None, device: int = 0):
+    """autobit.cpp:45-61: the default AutoBit candidate grid -- for bits 2..8 x
+    {per_group 128, per_channel}, symmetric, the RTN error (estimate_error
+    :16-34; mode "naive" or "act"/"act_aware") and storage cost.  Returns a
+    list of (QuantConfig, cost_bytes, err) in the reference's order."""
+    w = _f32(w)
+    modes = {"naive": 0, "act": 1, "act_aware": 1}
+    if mode not in modes:
+        raise InvalidInput(f"unknown error mode: {mode}")
+    if in_diag is not None:
+        in_diag = np.ascontiguousarray(in_diag, np.float64)
+        if in_diag.shape != (w.shape[0],):
+            raise InvalidInput("estimate_error: input diagonal length mismatch")
+    errs = np.zeros(14, np.float64)
+    costs = np.zeros(14, np.uint64)
+    _check(lib().ocwg_candidate_grid(context(device).handle, _ptr(w), w.shape[0], w.shape[1],
+                                     modes[mode], _ptr(in_diag), _ptr(errs), _ptr(costs)))
+    out = []
+    for k in range(14):
+        cfg = QuantConfig(2 + k // 2, Scheme.symmetric,
+                          Granularity.per_channel if k & 1 else Granularity.per_group, 128)
+        out.append((cfg, int(costs[k]), float(errs[k])))
+    return out
 
 
 def quantize_layers_x(ws, x_bf16_bits, cfg: QuantConfig, opts: GptqOptions,

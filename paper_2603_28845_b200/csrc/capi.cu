@@ -550,6 +550,36 @@ int ocwg_calibrate_grids(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t 
   });
 }
 
+int ocwg_candidate_grid(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t cols, int mode,
+                        const double* in_diag, double* errors, uint64_t* cost_bytes) {
+  return guard([&] {
+    if (mode != 0 && mode != 1) fail(OCWG_INVALID_INPUT, "unknown error mode");
+    if (rows == 0 || cols == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
+    for (int k = 0; k < 14; ++k) {  // autobit.cpp:47-58
+      ocwg_quant_config c{};
+      c.bits = 2 + k / 2;
+      c.scheme = 0;                       // symmetric
+      c.granularity = (k & 1) ? 1 : 2;    // grouped first, then per-channel
+      c.group_size = 128;
+      if (cost_bytes) cost_bytes[k] = storage_bytes(&c, rows, cols);
+    }
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    Arena ar(ctx);
+    const size_t ow = ar.reserve(rows * cols * 4), od = ar.reserve(rows * 8),
+                 op = ar.reserve(rows * 14 * 8), oe = ar.reserve(14 * 8);
+    ar.commit();
+    h2d(ar.at<float>(ow), w, rows * cols * 4, ctx);
+    if (in_diag) h2d(ar.at<double>(od), in_diag, rows * 8, ctx);
+    launch_candidate_grid(ar.at<float>(ow), (long long)rows, (long long)cols, (long long)cols, mode,
+                          in_diag ? ar.at<double>(od) : nullptr, ar.at<double>(op),
+                          ar.at<double>(oe), ctx->flag, ctx->stream);
+    finish(ctx);
+    d2h(errors, ar.at<double>(oe), 14 * 8, ctx);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
 int ocwg_quantize_matrix(ocwg_ctx* ctx, const float* w, uint64_t rows, uint64_t cols,
                          const ocwg_quant_config* cfg, int mode, int16_t* codes, float* scales,
                          int32_t* zeros) {

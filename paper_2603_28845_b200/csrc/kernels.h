@@ -42,6 +42,11 @@ void launch_unpack(const uint8_t* payload, long long n_codes, long long n_groups
                    int16_t* codes, float* scales, int32_t* zeros, cudaStream_t st);
 // act-order: stable descending sort of diag(H) (layerwise.cpp:11-18)
 void launch_order(const float* h, long long n, int actorder, int32_t* order, cudaStream_t st);
+// AutoBit candidate grid (autobit.cpp:45-61): out[14] = RTN errors of bits
+// {2..8} x {per_group 128, per_channel}, symmetric; partial: rows x 14 doubles
+void launch_candidate_grid(const float* w, long long rows, long long cols, long long ld, int act,
+                           const double* in_diag, double* partial, double* out, unsigned* flag,
+                           cudaStream_t st);
 
 // ---- factorisation (factor.cu), T = float (default) or double ---------------
 // A = reversed-permuted, dampened copy of H (layerwise.cpp:31-41):

@@ -399,4 +399,114 @@ void launch_order(const float* h, long long n, int actorder, int32_t* order, cud
                                                                                       order);
 }
 
+// ---- AutoBit's default candidate grid (autobit.cpp:45-61, estimate_error
+// :16-34): RTN error of W under bits {2..8} x {per_group 128, per_channel},
+// symmetric, for all 14 configurations in one pass over W.  One CTA per row:
+// group and row extremes first, then per element and configuration
+// code = clamp(rint(w / s)), w_hat = s code, d = w_hat - w (fp64), summed per
+// row; a second kernel adds the rows in order.
+namespace {
+constexpr int kCand = 14, kCandThreads = 256;
+__global__ void __launch_bounds__(kCandThreads) candidate_rows_kernel(
+    const float* __restrict__ w, long long cols, long long ld, int act,
+    const double* __restrict__ in_diag, double* __restrict__ partial, unsigned* flag) {
+  extern __shared__ float gmax[];  // per 128-group |w| max, then the row max at [ngroups]
+  __shared__ double red[kCandThreads / 32][kCand];
+  __shared__ float s_cfg[kCand];
+  const long long row = blockIdx.x;
+  const float* wr = w + row * ld;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long ng = (cols + 127) / 128;
+  // group extremes: warp w covers columns 32 w.. of each 256-column stride
+  bool bad = false;
+  for (long long g0 = 0; g0 < ng; g0 += 2) {
+    const long long col = g0 * 128 + tid;
+    float a = 0.f;
+    if (col < cols) {
+      const float v = wr[col];
+      bad |= !isfinite(v);
+      a = fabsf(v);
+    }
+    for (int o = 16; o; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane == 0) red[warp][0] = a;
+    __syncthreads();
+    if (tid < 2 && g0 + tid < ng) {
+      const int w0 = 4 * tid;
+      gmax[g0 + tid] = fmaxf(fmaxf(float(red[w0][0]), float(red[w0 + 1][0])),
+                             fmaxf(float(red[w0 + 2][0]), float(red[w0 + 3][0])));
+    }
+    __syncthreads();
+  }
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) atomicOr(flag, kFlagNonFinite);
+    return;
+  }
+  if (tid == 0) {
+    float m = 0.f;
+    for (long long g = 0; g < ng; ++g) m = fmaxf(m, gmax[g]);
+    gmax[ng] = m;
+    for (int k = 0; k < kCand; k += 2) {  // per-channel scales (k odd below)
+      const int qmax = (1 << (2 + k / 2 - 1)) - 1;
+      s_cfg[k + 1] = m == 0.f ? 1.f : positive_fp16(__fdiv_rn(m, float(qmax)));
+    }
+  }
+  __syncthreads();
+  double e[kCand];
+#pragma unroll
+  for (int k = 0; k < kCand; ++k) e[k] = 0.0;
+  for (long long col = tid; col < cols; col += kCandThreads) {
+    const float v = wr[col];
+    const float ga = gmax[col / 128];
+#pragma unroll
+    for (int b = 0; b < 7; ++b) {
+      const int qmax = (1 << (b + 1)) - 1;  // bits b + 2, symmetric
+#pragma unroll
+      for (int gr = 0; gr < 2; ++gr) {  // grouped first (autobit.cpp:48-49)
+        float sv;
+        if (gr == 0) sv = ga == 0.f ? 1.f : positive_fp16(__fdiv_rn(ga, float(qmax)));
+        else sv = s_cfg[2 * b + 1];
+        const int code = quantize_code(v, sv, 0, -qmax, qmax);
+        const double d = double(dequantize_code(code, sv, 0)) - double(v);
+        e[2 * b + gr] = fma(d, d, e[2 * b + gr]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kCand; ++k) {
+    double x = e[k];
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) red[warp][k] = x;
+  }
+  __syncthreads();
+  if (tid < kCand) {
+    double x = 0.0;
+    for (int q = 0; q < kCandThreads / 32; ++q) x += red[q][tid];
+    if (act) x *= 0.5 * (in_diag ? in_diag[row] : 1.0);
+    partial[row * kCand + tid] = x;
+  }
+}
+__global__ void candidate_sum_kernel(const double* __restrict__ partial, long long rows,
+                                     double* out) {
+  const int k = threadIdx.x;
+  if (k >= kCand) return;
+  double x = 0.0;
+  for (long long r = 0; r < rows; ++r) x += partial[r * kCand + k];
+  out[k] = x;
+}
+}  // namespace
+
+void launch_candidate_grid(const float* w, long long rows, long long cols, long long ld, int act,
+                           const double* in_diag, double* partial, double* out, unsigned* flag,
+                           cudaStream_t st) {
+  const long long ng = (cols + 127) / 128;
+  const size_t smem = size_t(ng + 1) * sizeof(float);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(candidate_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+  count_launches(2);
+  candidate_rows_kernel<<<unsigned(rows), kCandThreads, smem, st>>>(w, cols, ld, act, in_diag,
+                                                                    partial, flag);
+  candidate_sum_kernel<<<1, 32, 0, st>>>(partial, rows, out);
+}
+
 }  // namespace ocwg
