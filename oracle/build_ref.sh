@@ -27,6 +27,15 @@ SRCS="$REF/src/matrix.cpp $REF/src/quant.cpp $REF/src/stats.cpp $REF/src/layerwi
 # without including <functional>; it is force-included, the source is unmodified
 $CXX $FLAGS -shared -o "$OUT/libocw_ref.so" $SRCS "$REF/src/autobit.cpp" -include functional \
     "$HERE/ref_capi.cpp" -ldl
+# container.cpp (OCW1 writer / parser) needs nlohmann/json: the
+# image ships 3.11.3 inside cudnn_frontend; without it the container checker is
+# skipped (tests that need it skip too)
+JSON_DIR=${OCW_JSON_DIR:-$(python3 -c "import os, site; ps = [os.path.join(p, 'include/cudnn_frontend/thirdparty/nlohmann') for p in site.getsitepackages()]; print(next((p for p in ps if os.path.exists(os.path.join(p, 'json.hpp'))), ''))" 2>/dev/null)}
+if [ -n "$JSON_DIR" ] && [ -f "$JSON_DIR/json.hpp" ]; then
+  $CXX $FLAGS -I"$JSON_DIR" -include functional -shared -o "$OUT/libocw_ref_container.so" \
+      "$REF/src/container.cpp" "$REF/src/matrix.cpp" "$REF/src/quant.cpp" \
+      "$HERE/ref_out_of_path_stubs.cpp" "$HERE/ref_container_capi.cpp" -ldl
+fi
 for t in test_core test_layerwise; do
   $CXX $FLAGS -o "$OUT/ref_$t" "$REF/tests/test_main.cpp" "$REF/tests/$t.cpp" $SRCS -ldl
 done

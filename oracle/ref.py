@@ -222,3 +222,77 @@ def set_threads(n: int) -> None:
 
 def blas_name() -> str:
     return lib().ocwref_blas_name().decode()
+
+
+# ---- the reference's own OCW1 container (src/container.cpp), SURVEY §8 f2 ----
+CONTAINER_LIB = HERE / "_ref" / "libocw_ref_container.so"
+_clib = None
+
+
+def container_lib():
+    """libocw_ref_container.so, or None when the image lacks nlohmann/json."""
+    global _clib
+    if _clib is None and CONTAINER_LIB.exists():
+        l = C.CDLL(str(CONTAINER_LIB))
+        l.ocwref_container_error.restype = C.c_char_p
+        l.ocwref_serialize_ocw.restype = _I
+        l.ocwref_roundtrip_ocw.restype = _I
+        _clib = l
+    return _clib
+
+
+def _arr(vals, t):
+    return (t * len(vals))(*vals)
+
+
+def serialize_ocw(records, meta_json: str | None = None) -> bytes:
+    """serialize_ocw (container.cpp:344-373) over records of
+    ("f32", name, array) or ("uniform", name, codes, scales, zeros, bits, scheme, gran, group)."""
+    l = container_lib()
+    k = len(records)
+    keep = []
+    names, kind, rows, cols, bits, sch, gran, grp, f32, cds, scs, zrs = ([] for _ in range(12))
+    for r in records:
+        names.append(r[1].encode())
+        if r[0] == "f32":
+            a = np.ascontiguousarray(r[2], np.float32)
+            keep.append(a)
+            kind.append(0), rows.append(a.shape[0]), cols.append(a.shape[1])
+            bits.append(0), sch.append(0), gran.append(0), grp.append(0)
+            f32.append(a.ctypes.data), cds.append(None), scs.append(None), zrs.append(None)
+        else:
+            c = np.ascontiguousarray(r[2], np.int16)
+            s = np.ascontiguousarray(r[3], np.float32)
+            z = np.ascontiguousarray(r[4], np.int32)
+            keep += [c, s, z]
+            kind.append(1), rows.append(c.shape[0]), cols.append(c.shape[1])
+            bits.append(r[5]), sch.append(r[6]), gran.append(r[7]), grp.append(r[8])
+            f32.append(None), cds.append(c.ctypes.data), scs.append(s.ctypes.data)
+            zrs.append(z.ctypes.data)
+    cap = 64 + 1024 * (k + 1) + sum(a.nbytes for a in keep) * 2 + (len(meta_json or "") * 2)
+    out = np.zeros(cap, np.uint8)
+    ln = C.c_size_t()
+    st = l.ocwref_serialize_ocw(
+        k, _arr(names, C.c_char_p), _arr(kind, C.c_int), _arr(rows, C.c_size_t),
+        _arr(cols, C.c_size_t), _arr(bits, C.c_int), _arr(sch, C.c_int), _arr(gran, C.c_int),
+        _arr(grp, C.c_size_t), _arr(f32, C.c_void_p), _arr(cds, C.c_void_p),
+        _arr(scs, C.c_void_p), _arr(zrs, C.c_void_p),
+        None if meta_json is None else meta_json.encode(), out.ctypes.data_as(C.c_void_p),
+        C.c_size_t(cap), C.byref(ln))
+    if st != 0:
+        raise RuntimeError(l.ocwref_container_error().decode())
+    return out[:ln.value].tobytes()
+
+
+def roundtrip_ocw(data: bytes) -> bytes:
+    """serialize_ocw(deserialize_ocw(data)) -- the reference's parser."""
+    l = container_lib()
+    src = np.frombuffer(data, np.uint8).copy()
+    cap = len(data) * 2 + 4096
+    out = np.zeros(cap, np.uint8)
+    ln = C.c_size_t()
+    st = l.ocwref_roundtrip_ocw(src.ctypes.data_as(C.c_void_p), C.c_size_t(len(data)),
+                                out.ctypes.data_as(C.c_void_p), C.c_size_t(cap), C.byref(ln))
+    if st != 0:
+        raise RuntimeError(l.ocwref_container_error().decode())
+    return out[:ln.value].tobytes()
