@@ -267,7 +267,7 @@ struct CholSmem {
   T lt[TB][LD];       // workers: L_cc transposed / G staging; owner: X = L_cc^-T
   T sf[TB][TB + 1];   // diagonal tile being factored
   T wcol[2][72];      // warp elimination: published pivot column (shifted, + zero pad)
-  T wcol3[3][2][72];  // the same, per warp, for factor_tile64's three eliminating warps
+  T wcol4[4][72];     // factor_tile64: the producer's pivot-column ring (shared-pivot elimination)
   T sb[2][TB * LD];   // owner: staged partial tiles (row-major, ld LD, cp.async)
   T rdiag[TB];
   int item;
@@ -378,6 +378,75 @@ __device__ __forceinline__ bool warp_chol32(T (&a)[32], T (&b)[32], T* out_row, 
   return ok;
 }
 
+// Shared-pivot elimination for factor_tile64: the eliminating warp (producer)
+// publishes each pivot column in a 4-deep shared ring (wcol4[j & 3], shifted
+// as in warp_chol32) and 1/L[j][j] in rdiag[j]; carrying warps (consumers)
+// apply the same pivots to their rows without redoing the elimination.  One
+// named barrier (id 2, nthreads = the participating warps) per pivot: after
+// it, column j and rdiag[j] are visible; the ring is deep enough that the
+// producer never overwrites a column a consumer may still read.
+template <typename T>
+__device__ __forceinline__ bool warp_chol32_prod(T (&a)[32], T* out_row, T* rdiag,
+                                                 T (*wcol4)[72], int nthreads) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+  wcol4[0][lane + 3] = a[0];
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j) {
+    const int sh = (3 - j) & 3;
+    __syncwarp();
+    const T p = wcol4[j & 3][j + sh];
+    T v[32];
+    const T* nxt = wcol4[j & 3] + j + sh + 1;
+#pragma unroll
+    for (int k4 = 0; k4 < 32; k4 += 4) {
+      T v4[4];
+      ld4(nxt + k4, v4);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[k4 + e] = v4[e];
+    }
+    ok &= (p > T(0));
+    const T rs = rsqrt_fast(p);
+    const T l = a[0] * rs;
+    const T lrs = l * rs;
+    const T a0 = fma(-lrs, v[0], a[1]);
+    if (j + 1 < 32) wcol4[(j + 1) & 3][lane + ((2 - j) & 3)] = a0;
+    if (lane == j) rdiag[j] = rs;  // 1 / L[j][j]
+    if (nthreads > 32) asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+#pragma unroll
+    for (int k = 1; k + 1 < 32; ++k) a[k] = fma(-lrs, v[k], a[k + 1]);
+    a[0] = a0;
+    a[31] = T(0);
+    out_row[j] = lane >= j ? l : T(0);
+  }
+  return ok;
+}
+template <typename T>
+__device__ __forceinline__ void warp_carry32_cons(T (&b)[32], T* out_b, const T* rdiag,
+                                                  const T (*wcol4)[72], int nthreads) {
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j) {
+    const int sh = (3 - j) & 3;
+    asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+    T v[32];
+    const T* nxt = wcol4[j & 3] + j + sh + 1;
+#pragma unroll
+    for (int k4 = 0; k4 < 32; k4 += 4) {
+      T v4[4];
+      ld4(nxt + k4, v4);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[k4 + e] = v4[e];
+    }
+    const T rs = rdiag[j];
+    const T lb = b[0] * rs;  // (b L^-T)[j]
+    const T lbrs = lb * rs;
+#pragma unroll
+    for (int k = 0; k + 1 < 32; ++k) b[k] = fma(-lbrs, v[k], b[k + 1]);
+    b[31] = T(0);
+    out_b[j] = lb;
+  }
+}
+
 // Factor the 64 x 64 tile in sm.sf (lower, padded with identity) in place.
 // Three warps run the same 32-column eliminations (warp_chol32), on distinct
 // SM sub-partitions, so the rows they carry cost no chain length:
@@ -401,7 +470,7 @@ __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr, const 
     if (prof && tid == 0) prof[i] = clock64();
   };
   pstamp(0);
-  for (int e = tid; e < 3 * 2 * 72; e += CT) (&sm.wcol3[0][0][0])[e] = T(0);
+  for (int e = tid; e < 4 * 72; e += CT) (&sm.wcol4[0][0])[e] = T(0);
   __syncthreads();
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
@@ -411,9 +480,7 @@ __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr, const 
     // (votes make the warp-uniform branches visible to ptxas: no divergent-shuffle
     // fallback paths, which would pin the loads behind branch checks)
     if (__any_sync(0xffffffffu, active)) {
-      T av[32], bv[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) av[k] = sm.sf[o + lane][o + k];
+      T bv[32];
       T* brow = nullptr;  // carried row (written back in place)
       if (warp == 2 && h == 0) {
         brow = &sm.sf[32 + lane][0];
@@ -433,11 +500,17 @@ __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr, const 
         for (int k = 0; k < 32; ++k) bv[k] = T(0);
       }
       const bool w0 = __any_sync(0xffffffffu, warp == 0);
-      const bool okw = w0 ? warp_chol32<T, false>(av, bv, &sm.sf[o + lane][o], nullptr,
-                                                  &sm.rdiag[o], sm.wcol3[0])
-                          : warp_chol32<T, true>(av, bv, nullptr, brow, nullptr, sm.wcol3[warp]);
+      // producer + consumers: h = 0 warps 0, 2 (+1 with INV); h = 1 warp 0 (+1, 2 with INV)
+      const int nthreads = 32 * (h == 0 ? 2 + (INV ? 1 : 0) : 1 + (INV ? 2 : 0));
       if (w0) {
-        ok &= okw;
+        T av[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) av[k] = sm.sf[o + lane][o + k];
+        ok &= warp_chol32_prod(av, &sm.sf[o + lane][o], &sm.rdiag[o], sm.wcol4, nthreads);
+      } else {
+        warp_carry32_cons(bv, brow, &sm.rdiag[o], sm.wcol4, nthreads);
+      }
+      if (w0) {
         if (h == 0) {
 #pragma unroll
           for (int k = 0; k < 32; ++k) sm.sf[lane][32 + k] = T(0);
