@@ -173,12 +173,14 @@ __device__ __forceinline__ void st4(double* p, double a, double b, double c, dou
   reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
 }
 
-// Position of block-local column kk (0..127) of a sweep block row in the
-// in-block kernel's order: lane group rg = kk % 4 owns slots s = kk / 4,
-// stored in 16-byte chunks c = s / 4, XOR-swizzled by 2 rg (sweep.cu).
+// Position of block-local row kk (0..127) in a lane-ordered row of G^T for
+// the sweep's in-block kernel: lane group rg = kk % 8 owns slots s = kk / 8,
+// stored as 8-byte pairs p = s / 2 at rg*16 + 2*((p + 2*(rg/2)) % 8) -- the
+// rotation makes the eight lane groups' reads of one slot pair hit distinct
+// banks (sweep.cu).
 __host__ __device__ inline int gp_pos(int kk) {
-  const int rg = kk & 3, s = kk >> 2;
-  return rg * 32 + 4 * ((s >> 2) ^ (2 * rg)) + (s & 3);
+  const int rg = kk & 7, s = kk >> 3;
+  return rg * 16 + 2 * (((s >> 1) + 2 * (rg >> 1)) & 7) + (s & 1);
 }
 
 // A 64x64 tile (row-major, ld) <-> 16 elements per thread: rows tid/16 + 16*ii,

@@ -270,11 +270,11 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
 // distinct banks): 8 LDS.128 per row.  The owner's (w, s, 1/s, z) come from a
 // per-row table gathered once with cp.async.
 namespace l4 {
-// 4 warps: warps 0-1 run the row chain of 16 columns (4 lanes per column,
-// lane (cc, rg) holds rows rg + 4k); warps 2-3 help with the prologue
-// (gather, acc, lookahead rows 64..127) and the epilogue, and idle at a
-// barrier during the chain.
-constexpr int kLpc = 4, kRpt = 32, kCpw = 8, kCols4 = 16, kThreads = 128;
+// 4 warps, all on the row chain: warp w owns columns 4w..4w+3, 8 lanes per
+// column; lane (cc, rg) holds rows rg + 8s (s = 0..15) of column 4w + cc.
+// Two CTAs per SM give two chain warps per SM sub-partition, whose
+// quantise chains interleave.
+constexpr int kLpc = 8, kRpt = 16, kCpw = 4, kCols4 = 16, kThreads = 128;
 constexpr int kLa4 = 32;      // lookahead K chunk (double-buffered)
 constexpr int kGtEarly = 88;  // G rows >= this are staged before the lookahead
 
@@ -291,7 +291,6 @@ struct Smem {
   int16_t cs[kCols4][kB + 2];  // codes of (column, row)
   long long orow[kB];
   int og[kB];
-  int role[4];
 };
 static_assert(sizeof(((Smem*)0)->u.la) <= kGtEarly * kB * sizeof(float), "early G rows overlap");
 
@@ -373,40 +372,19 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
   Smem& sm = *reinterpret_cast<Smem*>(smraw);
   stamp(trace, 0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cc = lane & 7, rg = lane >> 3;
-  // Roles: the two chain warps should sit on different SM sub-partitions
-  // from the co-resident CTA's chain warps.  Warp slots are handed out in
-  // CTA-sized runs, so take SMSPs {0,1} in even runs and {2,3} in odd runs
-  // (fall back to warps 0-1 if the slot layout is not as assumed).
-  unsigned wid;
-  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
-  const int cand = ((wid & 3) >> 1) == ((wid >> 2) & 1);
-  if (lane == 0) sm.role[warp] = cand;
+  const int cc = lane & 3, rg = lane >> 2;
   const int og = tid < bsz ? order[ib + tid] : 0;
-  __syncthreads();
-  int h, rank;  // h: 0 = chain warp; rank: column half of a chain warp
-  {
-    const int nm = sm.role[0] + sm.role[1] + sm.role[2] + sm.role[3];
-    if (nm == 2) {
-      h = cand ? 0 : 1;
-      rank = 0;
-      for (int q = 0; q < warp; ++q) rank += sm.role[q];
-    } else {
-      h = warp >> 1;
-      rank = warp & 1;
-    }
-  }
-  const int cj = rank * kCpw + cc;
+  const int cj = warp * kCpw + cc;
   const long long j0 = (long long)blockIdx.x * kCols4;
   const long long j = j0 + cj;
   const bool col_ok = j < m;
 
   // ---- row order (one row per thread) and this thread's acc rows, in flight together
-  float r[kRpt];  // main warps: slots k = rows rg + 4k (acc = earlier super-blocks)
+  float r[kRpt];  // slot s = row rg + 8s (acc = earlier super-blocks)
 #pragma unroll
   for (int k = 0; k < kRpt; ++k) {
-    const int li = rg + 4 * k;
-    r[k] = (h == 0 && use_acc && col_ok && li < bsz) ? acc[(ib + li) * m + j] : 0.f;
+    const int li = rg + 8 * k;
+    r[k] = (use_acc && col_ok && li < bsz) ? acc[(ib + li) * m + j] : 0.f;
   }
   // ---- async: late G rows (never overlapped by the lookahead buffers), lookahead chunk 0
   const long long kprev = ib - bprev;
@@ -533,34 +511,34 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
   __syncthreads();
   stamp(trace, 3);
 
-  if (__any_sync(0xffffffffu, h == 0)) {  // (vote: warp-uniform, no divergent-shuffle path)
+  {
     if (bprev > 0) {
 #pragma unroll
-      for (int k = 0; k < kRpt; ++k) r[k] += sm.ds[cj][rg + 4 * k];
+      for (int k = 0; k < kRpt; ++k) r[k] += sm.ds[cj][rg + 8 * k];
     }
     const float qminf = float(c.qmin), qmaxf = float(c.qmax);
     // Rows li >= bsz of a short last block run as padding (w = 0, s = 1, z = 0,
     // zero G rows): finite d that no real row picks up, never stored -- so the
     // step loop has no per-row branch and the next row's loads hoist freely.
+    // Per 16 rows (T) the slots rotate by 2; logical slot pair T + mm of lane
+    // group rg sits at off[mm] (factor.cu gp_pos: conflict-free 8-byte loads).
 #pragma unroll 1
-    for (int T = 0; T < kRpt / 4; ++T) {
+    for (int T = 0; T < kRpt / 2; ++T) {
       if (16 * T >= bsz) break;
-      int off[8];  // chunk offsets of this lane's slots k = 4m .. 4m+3 (logical chunk T + m)
+      int off[8];
 #pragma unroll
-      for (int mm = 0; mm < 8; ++mm) off[mm] = rg * 32 + 4 * ((T + mm) ^ (2 * rg));
+      for (int mm = 0; mm < 8; ++mm)
+        off[mm] = 16 * T * kB + rg * 16 + 2 * ((T + mm + 2 * (rg >> 1)) & 7);
 #pragma unroll
-      for (int tt = 0; tt < 4; ++tt) {
+      for (int tt = 0; tt < 2; ++tt) {
 #pragma unroll
         for (int o = 0; o < kLpc; ++o) {
-          const int li = 16 * T + 4 * tt + o;
+          const int lj = 8 * tt + o, li = 16 * T + lj;
           float g[kRpt];
-          const float* gp = &sm.u.gt[li * kB];
 #pragma unroll
           for (int mm = 0; mm < 8; ++mm) {
-            float g4[4];
-            ld4(gp + off[mm], g4);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) g[4 * mm + e] = g4[e];
+            const float2 g2 = *reinterpret_cast<const float2*>(&sm.u.gt[off[mm] + lj * kB]);
+            g[2 * mm] = g2.x, g[2 * mm + 1] = g2.y;
           }
           const float4 tv = sm.tab[li][cj];  // (w, s, 1/s, z) of row li
           const float x = __fadd_rn(tv.x, r[tt]);  // w_cur = w + sum G D (owner lanes)
@@ -571,13 +549,13 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
             sm.ds[cj][li] = d;
             sm.cs[cj][li] = int16_t(int(cf));
           }
-          d = __shfl_sync(0xffffffffu, d, cc + kCpw * o);
+          d = __shfl_sync(0xffffffffu, d, cc + 4 * o);
 #pragma unroll
           for (int k = 0; k < kRpt; ++k) r[k] = fmaf(g[k], d, r[k]);
         }
       }
 #pragma unroll
-      for (int k = 0; k < kRpt; ++k) r[k] = k + 4 < kRpt ? r[k + 4] : 0.f;
+      for (int k = 0; k < kRpt; ++k) r[k] = k + 2 < kRpt ? r[k + 2] : 0.f;
     }
   }
   __syncthreads();
