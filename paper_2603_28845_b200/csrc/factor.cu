@@ -274,7 +274,7 @@ struct CholSmem {
   T rdiag[TB];
   int item;
   int ready;
-  int stg[3];  // owner: which tiles the factor's idle warps staged
+  int stg[4];  // owner: which tiles the factor's idle warps staged; [3]: product done
 };
 
 // Publish the finalised tile (values in t, rows b = 64r + 4ty + u, cols
@@ -460,10 +460,10 @@ __device__ __forceinline__ void warp_carry32_cons(T (&b)[32], T* out_b, const T*
 // With INV, sm.lt receives X = L^-T (upper triangular, ld TB + 4).  Upper
 // entries of sf are zeroed; sm.rdiag gets 1 / L[j][j].  All threads call.
 struct NoSide {
-  __device__ void operator()() const {}
+  __device__ void operator()(int) const {}
 };
-// Side: work for the warps the eliminations leave idle (warps 3-7 call it once,
-// at the start of h = 0).
+// Side: work for the warps the eliminations leave idle (warps 3-7 call it at
+// the start of each half, side(0) and side(1)).
 template <typename T, bool INV = false, typename Side = NoSide>
 __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr, const Side& side = Side()) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -478,7 +478,7 @@ __device__ bool factor_tile64(CholSmem<T>& sm, long long* prof = nullptr, const 
   for (int h = 0; h < 2; ++h) {
     const int o = 32 * h;  // diagonal block [o, o+32)
     const bool active = warp == 0 || (warp == 2 && h == 0) || (INV && warp <= 2);
-    if (h == 0 && warp >= 3) side();
+    if (warp >= 3) side(h);
     // (votes make the warp-uniform branches visible to ptxas: no divergent-shuffle
     // fallback paths, which would pin the loads behind branch checks)
     if (__any_sync(0xffffffffu, active)) {
@@ -633,6 +633,42 @@ __device__ __forceinline__ void owner_prod(const T* A, const T* B, const T* src,
         T val = (src ? src[i * LD + j] : T(0)) + sgn * acc[u][v];
         if (pad >= 0 && i == j && i >= pad) val = T(1);
         D[i * ldd + j] = val;
+      }
+  }
+}
+
+// D = src - A B^T on warps 4-7 only (fp32): the owner's sub-tile update runs
+// beside the factorisation on warps the elimination leaves idle.
+__device__ __forceinline__ void owner_prod_w47(const float* A, const float* B, float* D) {
+  const int warp = (threadIdx.x >> 5) - 4, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int r0 = 16 * warp;
+#pragma unroll 1
+  for (int n0 = 0; n0 < TB; n0 += 32) {
+    float c1[4][4] = {}, c2[4][4] = {};
+#pragma unroll 2
+    for (int k8 = 0; k8 < TB; k8 += 8) {
+      uint32_t ah[4], al[4];
+      split_tf32(A[(r0 + g) * LD + k8 + t], ah[0], al[0]);
+      split_tf32(A[(r0 + g + 8) * LD + k8 + t], ah[1], al[1]);
+      split_tf32(A[(r0 + g) * LD + k8 + t + 4], ah[2], al[2]);
+      split_tf32(A[(r0 + g + 8) * LD + k8 + t + 4], ah[3], al[3]);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int nn = n0 + 8 * nt + g;
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(B[nn * LD + k8 + t], bh0, bl0);
+        split_tf32(B[nn * LD + k8 + t + 4], bh1, bl1);
+        mma_tf32(c1[nt], ah, bh0, bh1);
+        mma_tf32(c2[nt], ah, bl0, bl1);
+        mma_tf32(c2[nt], al, bh0, bh1);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = r0 + g + 8 * (q >> 1), j = n0 + 8 * nt + 2 * t + (q & 1);
+        D[i * LD + j] -= c1[nt][q] + c2[nt][q];
       }
   }
 }
@@ -922,8 +958,23 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       stamp(e0, 3);
       // the factor's idle warps (3-7) stage what is already published: S'[c+1,c],
       // L[c+1,c-1] and the next column's S'[c+1,c+1] (sm.stg bits tell which)
-      auto side = [&]() {
+      auto side = [&](int half) {
         const int st = tid - 96;  // 0..159
+        if (half == 1) {
+          // S[c+1,c] -= L[c+1,c-1] L[c,c-1]^T beside the h = 1 elimination when both
+          // tiles were staged (fp32; otherwise it runs after the factor)
+          if (sizeof(T) == 4 && prev && sm.stg[0] && sm.stg[1]) {
+            cp_async_wait_all();
+            asm volatile("bar.sync 1, 160;" ::: "memory");
+            if (tid >= 128)
+              owner_prod_w47(reinterpret_cast<const float*>(sm.ps),
+                             reinterpret_cast<const float*>(sm.qs),
+                             reinterpret_cast<float*>(sm.sb[0]));
+            if (st == 0) sm.stg[3] = 1;
+          }
+          return;
+        }
+        if (st == 0) sm.stg[3] = 0;
         if (st == 0) sm.stg[0] = sub && ld_acquire(pflags + 2 * c + 1);
         if (st == 32) sm.stg[1] = sub && prev && ld_acquire(flags + (c + 1) * nt + (c - 1));
         if (st == 64) sm.stg[2] = sub && ld_acquire(pflags + 2 * (c + 1));
@@ -993,7 +1044,7 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       }
       cp_async_wait_all();
       __syncthreads();
-      if (prev) {
+      if (prev && !sm.stg[3]) {
         owner_prod<T, false>(sm.ps, sm.qs, sm.sb[0], sm.sb[0], LD, T(-1), -1);
         __syncthreads();
       }
