@@ -308,9 +308,23 @@ void run_gptq(ocwg_ctx* ctx, const float* w, uint64_t ldw, const float* h_dev, u
               float* mm_ws) {
   const QCfg c = qcfg(cfg, m);
   if (ctx->profile) cudaEventRecord(ctx->ev[0], ctx->stream);
+  // the grids depend on W only (quant.cpp:168-196): they are calibrated on the
+  // auxiliary stream while the latency-bound factorisation runs
+  const bool overlap = !ctx->profile;
+  if (overlap) {
+    ck(cudaEventRecord(ctx->sev[0], ctx->stream), "event");
+    ck(cudaStreamWaitEvent(ctx->aux, ctx->sev[0], 0), "event");
+    launch_calibrate_grids(w, (long long)n, (long long)m, (long long)ldw, c, mode, scales, zeros,
+                           ctx->flag, mm_ws, ctx->aux);
+    ck(cudaEventRecord(ctx->sev[1], ctx->aux), "event");
+  }
   run_factor(ctx, h_dev, n, opts->actorder, opts->percdamp, b);
-  launch_calibrate_grids(w, (long long)n, (long long)m, (long long)ldw, c, mode, scales, zeros,
-                         ctx->flag, mm_ws, ctx->stream);
+  if (overlap) {
+    ck(cudaStreamWaitEvent(ctx->stream, ctx->sev[1], 0), "event");
+  } else {
+    launch_calibrate_grids(w, (long long)n, (long long)m, (long long)ldw, c, mode, scales, zeros,
+                           ctx->flag, mm_ws, ctx->stream);
+  }
   if (ctx->profile) cudaEventRecord(ctx->ev[4], ctx->stream);
   if (ctx->precision == OCWG_FP64)
     run_sweep_t<double>(ctx, w, ldw, n, m, c, opts, codes, scales, zeros, w_hat, b);
