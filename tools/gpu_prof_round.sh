@@ -8,7 +8,7 @@ prof() {  # name regex skip
 prof hessian hessian_tc2 0
 prof chol chol_tile 0
 prof inblock inblock4 5
-prof tcgemm tc_gemm 1
+prof tcgemm tc_gemm2 1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
     --log-file gpurun_out/launches.csv python tools/prof_c2.py --reps 2 > gpurun_out/ncu_launch.log 2>&1
 echo "rc=$?" >> gpurun_out/plain.log
