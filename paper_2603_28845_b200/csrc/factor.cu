@@ -14,18 +14,20 @@
 // triangular inverse is on the hot path; the inverse (for the H^-1 / U
 // parity artefacts of ocwg_gptq_factor) is computed only on request.
 //
-// Cholesky: one persistent, dataflow-scheduled kernel over 64x64 tiles.
-// Work items are the lower tiles (r, c) of a column range [c0, c1) in
-// column-major order, handed out by an atomic counter; item (r, c) computes
-//   S = A[r,c] - sum_{c0<=k<c} L[r,k] L[c,k]^T
-// waiting on per-tile ready flags (acquire/release) for each L[.,k], then
-//   r == c: factors S (64-step right-looking elimination, one barrier per step)
-//   r >  c: L[r,c] = S L[c,c]^-T by forward substitution (warp shuffles only)
-// and publishes L[r,c] (and the matching block of G) with a release flag.
-// Items only ever wait on items handed out earlier, so the schedule cannot
-// deadlock whatever the residency.  Large n runs macro panels: the dataflow
-// kernel over a column range, then one tcgen05 3xTF32 SYRK for the trailing
-// matrix (gemm.cu / tc_gemm.cu).
+// Cholesky: one persistent kernel over 64x64 tiles with acquire/release tile
+// flags.  CTA 0 (the owner) runs the critical path alone on its SM: per column
+// c it applies the k = c-1 term to S'[c,c], factors it (factor_tile64, which
+// also yields X = L[c,c]^-T), and forms L[c+1,c] = S[c+1,c] X, keeping
+// L[c+1,c] in shared memory for the next column -- no inter-CTA hand-off on
+// the chain.  The other CTAs take work items in column order from an atomic
+// counter: partial S'[c..c+1, c] (sum over k < c-1), full tiles (c+2.., c)
+// (accumulate, then S X with X read from the diagonal tile's upper triangle)
+// and one emission item per column for the owner's tiles.  Tile products run
+// as 3xTF32 on the warp tensor cores over cp.async-staged row-major tiles.
+// Items only wait on earlier items or on the owner, which only waits on
+// earlier items, so with every CTA resident the schedule cannot deadlock.
+// Large n runs macro panels: the kernel over a column range, then one tcgen05
+// 3xTF32 SYRK for the trailing matrix (gemm.cu / tc_gemm.cu).
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -151,28 +153,6 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(u);
 }
 
-// 1/x and 1/sqrt(x) to fp32 accuracy without the IEEE slow-path checks
-// (pivots are positive normal numbers, or the factorisation has failed)
-__device__ __forceinline__ float rcp_nr(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return fmaf(y, fmaf(-x, y, 1.0f), y);
-}
-__device__ __forceinline__ double rcp_nr(double x) { return 1.0 / x; }
-__device__ __forceinline__ float rsqrt_nr(float x) {
-  float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y * fmaf(-0.5f * x * y, y, 1.5f);
-}
-__device__ __forceinline__ double rsqrt_nr(double x) { return rsqrt(x); }
-__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
-  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
-}
-__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
-  reinterpret_cast<double2*>(p)[0] = make_double2(a, b);
-  reinterpret_cast<double2*>(p)[1] = make_double2(c, d);
-}
-
 // Position of block-local row kk (0..127) in a lane-ordered row of G^T for
 // the sweep's in-block kernel: lane group rg = kk % 8 owns slots s = kk / 8,
 // stored as 8-byte pairs p = s / 2 at rg*16 + 2*((p + 2*(rg/2)) % 8) -- the
@@ -181,54 +161,6 @@ __device__ __forceinline__ void st4(double* p, double a, double b, double c, dou
 __host__ __device__ inline int gp_pos(int kk) {
   const int rg = kk & 7, s = kk >> 3;
   return rg * 16 + 2 * (((s >> 1) + 2 * (rg >> 1)) & 7) + (s & 1);
-}
-
-// A 64x64 tile (row-major, ld) <-> 16 elements per thread: rows tid/16 + 16*ii,
-// cols 4*(tid%16) + e.  Out-of-range elements read as 0.
-template <typename T>
-struct TileRegs {
-  T v[4][4];
-};
-
-template <typename T>
-__device__ __forceinline__ void load_tile(TileRegs<T>& R, const T* base, long long ld, int rows,
-                                          int cols, bool vec_ok) {
-  const int tid = threadIdx.x, c4 = (tid & 15) * 4;
-#pragma unroll
-  for (int ii = 0; ii < 4; ++ii) {
-    const int r = (tid >> 4) + 16 * ii;
-    const T* p = base + (long long)r * ld + c4;
-    if (vec_ok && r < rows && c4 + 4 <= cols) {
-      if constexpr (sizeof(T) == 4) {
-        const float4 f = __ldcg(reinterpret_cast<const float4*>(p));
-        R.v[ii][0] = f.x, R.v[ii][1] = f.y, R.v[ii][2] = f.z, R.v[ii][3] = f.w;
-      } else {
-        const double2 f0 = __ldcg(reinterpret_cast<const double2*>(p));
-        const double2 f1 = __ldcg(reinterpret_cast<const double2*>(p + 2));
-        R.v[ii][0] = f0.x, R.v[ii][1] = f0.y, R.v[ii][2] = f1.x, R.v[ii][3] = f1.y;
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) R.v[ii][e] = (r < rows && c4 + e < cols) ? ldcg(p + e) : T(0);
-    }
-  }
-}
-
-// Store the tile transposed into swizzled k-major smem: S[k][i] at
-// k*64 + ((i/4) ^ ((k/4)&15))*4 + i%4  (conflict-free stores and float4 reads).
-template <typename T>
-__device__ __forceinline__ void store_tile_t(const TileRegs<T>& R, T* S) {
-  const int tid = threadIdx.x, tx = tid & 15;
-#pragma unroll
-  for (int ii = 0; ii < 4; ++ii) {
-    const int i = (tid >> 4) + 16 * ii;
-    const int pg = (i >> 2) ^ tx;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int k = 4 * tx + e;
-      S[k * TB + pg * 4 + (i & 3)] = R.v[ii][e];
-    }
-  }
 }
 
 template <typename T>
@@ -243,32 +175,15 @@ __device__ __forceinline__ void ld4(const T* p, T (&o)[4]) {
   }
 }
 
-// acc[u][v] += sum_k P[4ty+u][k] * Q[4tx+v][k]
-template <typename T>
-__device__ __forceinline__ void tile_mma(T (&acc)[4][4], const T* Ps, const T* Qs) {
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-#pragma unroll 4
-  for (int k = 0; k < TB; ++k) {
-    const int sw = (k >> 2) & 15;
-    T p[4], q[4];
-    ld4(Ps + k * TB + ((ty ^ sw) << 2), p);
-    ld4(Qs + k * TB + ((tx ^ sw) << 2), q);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] = fma(p[u], q[v], acc[u][v]);
-  }
-}
 
 constexpr int LD = TB + 4;  // row stride of the owner's row-major tiles
 
 template <typename T>
 struct CholSmem {
-  T ps[TB * LD];      // workers: swizzled tile_mma operands; owner: row-major tiles (ld LD)
+  T ps[TB * LD];      // row-major tiles (ld LD): tile-product operands / staging
   T qs[TB * LD];
   T lt[TB][LD];       // workers: L_cc transposed / G staging; owner: X = L_cc^-T
   T sf[TB][TB + 1];   // diagonal tile being factored
-  T wcol[2][72];      // warp elimination: published pivot column (shifted, + zero pad)
   T wcol4[4][72];     // factor_tile64: the producer's pivot-column ring (shared-pivot elimination)
   T sb[2][TB * LD];   // owner: staged partial tiles (row-major, ld LD, cp.async)
   T rdiag[TB];
@@ -310,17 +225,8 @@ __device__ void emit_g(const T (&t)[4][4], CholSmem<T>& sm, const T* diag, int r
   }
 }
 
-// Warp-synchronous right-looking Cholesky of a 32 x 32 block held one row per
-// lane (a[k] = A[lane][j0 + k], lower part used).  The register array rotates
-// as it is updated (a[0] is always the pivot column).  Per pivot each lane
-// publishes its pivot-column entry to shared memory (double-buffered,
-// zero-padded past 32) and reads the pivot and the others as broadcasts.  The
-// loop is software-pipelined: right after the new a[0] is formed, the next
-// column's store is issued, so its latency hides under the remaining updates.
-//   CARRY = false: writes L[lane][j] to out_row[j] and 1/L[j][j] to rdiag[j].
-//   CARRY = true : the lane also carries a row b through the same pivots (the
-//                  eliminated block itself is discarded): b ends as
-//                  b L^-T, written to out_b[j].
+// rsqrt to the hardware approximation (pivots are positive normal numbers,
+// or the factorisation has failed and is reported)
 template <typename T>
 __device__ __forceinline__ T rsqrt_fast(T x) {
   if constexpr (sizeof(T) == 4) {
@@ -330,54 +236,6 @@ __device__ __forceinline__ T rsqrt_fast(T x) {
   } else {
     return rsqrt(x);
   }
-}
-template <typename T, bool CARRY>
-__device__ __forceinline__ bool warp_chol32(T (&a)[32], T (&b)[32], T* out_row, T* out_b,
-                                            T* rdiag, T (*wcol)[72]) {
-  const int lane = threadIdx.x & 31;
-  bool ok = true;
-  // stored at lane + sh so that entry j+1 starts a 16-byte chunk: the 31
-  // entries a lane needs are 8 LDS.128 broadcasts
-  wcol[0][lane + 3] = a[0];
-  // (unrolled by 4: buffer parity and shifts are static and ptxas sees the loop-carried
-  // chain a0 -> store -> next pivot load, so it issues a0 first)
-#pragma unroll 4
-  for (int j = 0; j < 32; ++j) {
-    const int sh = (3 - j) & 3;
-    __syncwarp();
-    const T p = wcol[j & 1][j + sh];  // the pivot, lane j's entry (broadcast load: no shuffle)
-    T v[32];
-    const T* nxt = wcol[j & 1] + j + sh + 1;  // 16-byte aligned
-#pragma unroll
-    for (int k4 = 0; k4 < 32; k4 += 4) {
-      T v4[4];
-      ld4(nxt + k4, v4);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) v[k4 + e] = v4[e];
-    }
-    ok &= (p > T(0));
-    const T rs = rsqrt_fast(p);
-    const T l = a[0] * rs;  // L[lane][j]; lane j: sqrt(p)
-    const T lrs = l * rs;   // a[k] -= L[lane][j] L[j+k][j] = lrs * a_{j+k}[j]
-    const T a0 = fma(-lrs, v[0], a[1]);
-    if (j + 1 < 32) wcol[(j + 1) & 1][lane + ((2 - j) & 3)] = a0;  // next column, early
-#pragma unroll
-    for (int k = 1; k + 1 < 32; ++k) a[k] = fma(-lrs, v[k], a[k + 1]);
-    a[0] = a0;
-    a[31] = T(0);
-    if constexpr (CARRY) {
-      const T lb = b[0] * rs;  // (b L^-T)[j]
-      const T lbrs = lb * rs;
-#pragma unroll
-      for (int k = 0; k + 1 < 32; ++k) b[k] = fma(-lbrs, v[k], b[k + 1]);
-      b[31] = T(0);
-      out_b[j] = lb;
-    } else {
-      out_row[j] = lane >= j ? l : T(0);
-      if (lane == j) rdiag[j] = rs;  // 1 / L[j][j]
-    }
-  }
-  return ok;
 }
 
 // Shared-pivot elimination for factor_tile64: the eliminating warp (producer)
@@ -450,7 +308,7 @@ __device__ __forceinline__ void warp_carry32_cons(T (&b)[32], T* out_b, const T*
 }
 
 // Factor the 64 x 64 tile in sm.sf (lower, padded with identity) in place.
-// Three warps run the same 32-column eliminations (warp_chol32), on distinct
+// Three warps share the 32-column eliminations (warp_chol32_prod / _cons), on distinct
 // SM sub-partitions, so the rows they carry cost no chain length:
 //   h = 0: warp 0 -> L11 = chol(A11); warp 2 carries A21 -> L21 = A21 L11^-T;
 //          [INV] warp 1 carries identity rows 0-31 -> X rows of L^-T;
@@ -808,48 +666,7 @@ __device__ __forceinline__ void store_t(const T (&t)[4][4], T* ab, long long n, 
   }
 }
 
-// t (row 4ty+u, col 4tx+v) -> the transposed swizzled k-major layout of
-// store_tile_t (S[k][i], k = column): operand of tile_mma
-template <typename T>
-__device__ __forceinline__ void store_t_swz(const T (&t)[4][4], T* S) {
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) S[(4 * tx + v) * TB + ((ty ^ tx) << 2) + u] = t[u][v];
-}
 
-// X L^T = t by forward substitution (warp shuffles; sm.lt[j][c] = L[c][j],
-// sm.rdiag[j] = 1 / L[j][j]); t <- X
-template <typename T>
-__device__ __forceinline__ void solve_rows(T (&t)[4][4], CholSmem<T>& sm) {
-  const int tid = threadIdx.x, tx = tid & 15, lane = tid & 31;
-  const int src0 = lane & 16;
-#pragma unroll 1
-  for (int j0 = 0; j0 < TB; j0 += 4) {
-    const bool own = tx == (j0 >> 2), later = tx > (j0 >> 2);
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int j = j0 + jj;
-      const T rd = sm.rdiag[j];
-      T x[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) x[u] = __shfl_sync(0xffffffffu, t[u][jj] * rd, src0 + (j >> 2));
-      if (own) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) t[u][jj] = x[u];
-      }
-      T l[4];
-      ld4(&sm.lt[j][4 * tx], l);
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-        if (later || (own && v > jj)) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) t[u][v] = fma(-x[u], l[v], t[u][v]);
-        }
-    }
-  }
-}
 
 // Publish a finalised tile L[r,c] (values t) into G: the sweep's lane-ordered
 // diagonal blocks of G^T (gtt) and the GEMM / lookahead operands (emit_g).

@@ -8,26 +8,23 @@
 // which is, in closed form (factor.cu),
 //   w_cur[k] = w[k] + sum_{i<k} G[k,i] * D[i],   D[i] = w[i] - w_hat[i],
 // with G the unit-lower factor emitted by the Cholesky and w the ORIGINAL
-// (permuted) row.  Per block of B rows [ib, ie):
-//   in-block (inblock_g_kernel): for i in block: w_cur = w + acc; quantize;
-//       D = w - w_hat; acc[k] += G[k,i] D  for the block's later rows k;
-//   trailing: acc[ie + B':, :] += G[ie + B':, blk] * D[blk, :]  (tcgen05 3xTF32).
-// Lookahead: the trailing update of block b skips block b+1's rows; block
-// b+1's in-block kernel applies that slice itself (G[blk b+1, blk b] D_b)
-// from shared memory.  In-block kernels run back to back on the calling
-// stream while the trailing GEMMs run on an auxiliary stream:
-//   inblock(b+1) needs inblock(b) (same stream) and trailing(b-1) (event);
-//   trailing(b)  needs inblock(b) (event).
-// acc needs no initialisation: trailing(0) writes it with beta = 0 and
-// blocks 0 and 1 never read it.
+// (permuted) row.  Two-level blocking, on one stream:
+//   super-blocks of 512 rows (4 blocks of B = 128): after the last block of a
+//   super-block, ONE trailing GEMM applies it to every later row,
+//       acc[se:, :] (+)= G[se:, s0:se] D[s0:se, :]        (tcgen05 3xTF32 pairs);
+//   per block, the in-block kernel adds acc, applies the earlier blocks of
+//   its own super-block by lookahead (G[blk, s0:ib] D[s0:ib], warp tensor
+//   cores), then runs the row chain: quantize; D = w - w_hat; the block's
+//   later rows += G[k, i] D.
+// acc needs no initialisation: the first super-block's GEMM writes it with
+// beta = 0 and the first super-block never reads it.
 //
-// In-block mapping: a CTA owns 32 columns (8 warps x 4); lane = cc + 4*rg
-// keeps rows rg, rg+8, ... of its column in registers (with the column's
-// original weights, scales and zero points for those rows).  The 8-row group
-// body is unrolled and the register arrays rotate by one slot per group, so
-// every register index is a compile-time constant; D is broadcast with one
-// warp shuffle.  The block's strictly-lower G is staged packed in shared
-// memory; D is staged for a coalesced K-major store (the GEMM's B operand).
+// fp32 path (l4::inblock4_kernel, B = 128): 16 columns per 4-warp CTA, 8
+// lanes per column, 16 rotating register slots per lane; see the kernel.
+// Generic path (inblock_g_kernel: fp64, or B != 128): a CTA owns 32 columns
+// (8 warps x 4); lane = cc + 4*rg keeps rows rg, rg+8, ... of its column in
+// registers, rotating by one slot per 8-row group; D is broadcast with one
+// warp shuffle and staged for a coalesced K-major store.
 #include <cstdlib>
 
 #include "kernels.h"
