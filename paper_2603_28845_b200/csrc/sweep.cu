@@ -721,7 +721,11 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
           const char* e = getenv("OCWG_SWEEP_GEMM2");
           return !(e && e[0] == '0');
         }();
-        if (split && pairs)
+        static const long long pair_min_rows = [] {  // OCWG_SWEEP_GEMM2_MIN: smaller M -> 1-SM tiles
+          const char* e = getenv("OCWG_SWEEP_GEMM2_MIN");
+          return e ? atoll(e) : 1600LL;  // (measured: 1-SM 128 x 128 tiles win below ~1600 rows)
+        }();
+        if (split && pairs && n - se >= pair_min_rows)
           done = tc_gemm2_presplit(n - se, m, kk, 1.0f,
                                    reinterpret_cast<const float*>(ghi) + se * n + s0,
                                    glo + se * n + s0, n, dhi[p], dlo[p], kSuperRows, float(beta),
