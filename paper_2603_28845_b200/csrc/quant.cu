@@ -5,6 +5,8 @@
 #include <cfloat>
 #include <cmath>
 
+#include <type_traits>
+
 #include "kernels.h"
 
 namespace ocwg {
@@ -235,8 +237,38 @@ __global__ void pack_codes_kernel(const int16_t* __restrict__ codes, long long n
 #pragma unroll
   for (int i = 0; i < 8; ++i) words[i] = 0;
   const int cnt = int(min(32LL, n_codes - c0));
-  for (int k = 0; k < cnt; ++k) {
-    const uint32_t v = uint32_t(int(codes[c0 + k]) - qmin) & mask;
+  int16_t cv[32];
+  if (cnt == 32 && (reinterpret_cast<uintptr_t>(codes) & 15) == 0) {  // 4 x 16-byte loads
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 v4 = __ldg(reinterpret_cast<const int4*>(codes + c0) + q);
+      const int16_t* p = reinterpret_cast<const int16_t*>(&v4);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) cv[8 * q + e] = p[e];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) cv[k] = k < cnt ? codes[c0 + k] : int16_t(qmin);
+  }
+  // (codes past the end contribute zero bits: they are never written out)
+  auto dense = [&](auto bc) {  // bits dividing 32: whole codes per word
+    constexpr int B = decltype(bc)::value, PER = 32 / B;
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        const int k = i * PER + e;
+        const uint32_t v = k < cnt ? (uint32_t(int(cv[k]) - qmin) & mask) : 0u;
+        words[i] |= v << (e * B);
+      }
+  };
+  if (bits == 4) dense(std::integral_constant<int, 4>());
+  else if (bits == 2) dense(std::integral_constant<int, 2>());
+  else if (bits == 8) dense(std::integral_constant<int, 8>());
+  else
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t v = k < cnt ? (uint32_t(int(cv[k]) - qmin) & mask) : 0u;
     const int bit = k * bits;
     const int wi = bit >> 5, sh = bit & 31;
 #pragma unroll
