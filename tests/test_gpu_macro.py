@@ -44,6 +44,27 @@ def test_macro_panel_factor(g, ref, prec, macro192, n, act):
     assert np.max(np.abs(u - ru)) <= (1e-4 if prec == "fp32" else 1e-9) * np.max(np.abs(ru))
 
 
+def test_factor_odd_size_single_panel(g, ref):
+    # nt = 65 with a 4-row last tile: the owner's last sub tile and the identity
+    # padding of the last diagonal tile (no macro panels).  Checked against a
+    # numpy fp64 restatement of layerwise.cpp:31-51 (the reference's own build
+    # runs fixed-order loops under test: minutes at this size).
+    n = 4100
+    x = np.random.default_rng(4100).standard_normal((2 * n, n)).astype(np.float32)
+    x[:, ::17] *= 20.0
+    h = (x.T.astype(np.float64) @ x.astype(np.float64)).astype(np.float32)
+    order, hinv, u, damp = g.gptq_factor(h, True, 0.01)
+    np.testing.assert_array_equal(order, ref.gptq_order(h, True))
+    hd = h.astype(np.float64)
+    lam = 0.01 * float(np.mean(np.diagonal(hd)))
+    assert abs(damp - lam) <= 1e-12 * lam
+    hp = hd[np.ix_(order, order)] + lam * np.eye(n)
+    rhinv = np.linalg.inv(hp)
+    assert sym_close(hinv, rhinv) <= 1e-4
+    ru = np.linalg.cholesky(rhinv).T  # U = upper Cholesky factor of H_p^-1 (layerwise.cpp:47-51)
+    assert np.max(np.abs(u - ru)) <= 1e-4 * np.max(np.abs(ru))
+
+
 def test_macro_panel_gptq_codes(g, ref, macro192):
     n, m = 700, 256
     h = _gram(ref, n, 4242)
