@@ -302,18 +302,22 @@ void run_sweep_t(ocwg_ctx* ctx, const float* w, uint64_t ldw, uint64_t n, uint64
 }
 
 // gptq_quantize on device buffers (w row stride ldw; codes/w_hat stride ldw)
+// w_ready (optional): event after which W is resident -- only the grids and
+// the sweep wait for it, the factorisation (H only) does not.
 void run_gptq(ocwg_ctx* ctx, const float* w, uint64_t ldw, const float* h_dev, uint64_t n,
               uint64_t m, const ocwg_quant_config* cfg, const ocwg_gptq_options* opts, int mode,
               int16_t* codes, float* scales, int32_t* zeros, float* w_hat, const GptqBufs& b,
-              float* mm_ws) {
+              float* mm_ws, cudaEvent_t w_ready = nullptr) {
   const QCfg c = qcfg(cfg, m);
   if (ctx->profile) cudaEventRecord(ctx->ev[0], ctx->stream);
   // the grids depend on W only (quant.cpp:168-196): they are calibrated on the
   // auxiliary stream while the latency-bound factorisation runs
   const bool overlap = !ctx->profile;
+  if (!overlap && w_ready) ck(cudaStreamWaitEvent(ctx->stream, w_ready, 0), "event");
   if (overlap) {
     ck(cudaEventRecord(ctx->sev[0], ctx->stream), "event");
     ck(cudaStreamWaitEvent(ctx->aux, ctx->sev[0], 0), "event");
+    if (w_ready) ck(cudaStreamWaitEvent(ctx->aux, w_ready, 0), "event");
     launch_calibrate_grids(w, (long long)n, (long long)m, (long long)ldw, c, mode, scales, zeros,
                            ctx->flag, mm_ws, ctx->aux);
     ck(cudaEventRecord(ctx->sev[1], ctx->aux), "event");
@@ -1107,8 +1111,6 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
     }
     ck(cudaEventRecord(ctx->cev[0], st), "event");  // copies start after prior work on st
     ck(cudaStreamWaitEvent(ctx->cpy, ctx->cev[0], 0), "event");
-    ck(cudaMemcpyAsync(wd, w, n * m * 4, cudaMemcpyHostToDevice, ctx->cpy), "H2D(W)");
-    ck(cudaEventRecord(ctx->cev[1], ctx->cpy), "event");
     if (tokens == 0) ck(cudaMemsetAsync(hd, 0, n * n * 4, st), "memset");
     for (long long k = 0; k < nchunks; ++k) {
       const long long t0 = k * chunk, tc = std::min<long long>(chunk, (long long)tokens - t0);
@@ -1122,9 +1124,13 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
       if (r == -1) hessian_simt(xd + t0 * n, tc, (long long)n, hd, k > 0 ? 1 : 0, st);
       else if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
     }
-    ck(cudaStreamWaitEvent(st, ctx->cev[1], 0), "event");  // W resident
+    // W goes over PCIe after X: it is needed only by the grids and the sweep, so
+    // its copy overlaps the factorisation instead of delaying the first X chunk
+    ck(cudaMemcpyAsync(wd, w, n * m * 4, cudaMemcpyHostToDevice, ctx->cpy), "H2D(W)");
+    ck(cudaEventRecord(ctx->cev[1], ctx->cpy), "event");
     run_gptq(ctx, wd, m, hd, n, m, cfg, opts, mode, cd, sd, zd, w_hat ? whd : nullptr,
-             gptq_bufs(ar, ctx, o, n, m), ar.at<float>(om));
+             gptq_bufs(ar, ctx, o, n, m), ar.at<float>(om), ctx->cev[1]);
+    ck(cudaStreamWaitEvent(st, ctx->cev[1], 0), "event");  // (W resident for the D2H order)
     if (payload) launch_pack(cd, (long long)(n * m), (long long)ng, qcfg(cfg, m), sd, zd, pd, st);
     d2h(codes, cd, n * m * 2, ctx);
     d2h(scales, sd, ng * 4, ctx);
