@@ -27,6 +27,8 @@
 // warp shuffle and staged for a coalesced K-major store.
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "kernels.h"
 
 namespace ocwg {
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(256) inblock_g_kernel(
       if (rg == o) {
         if (col_ok) {
           const long long orow = sm.orow[li];  // original row order (:75)
-          code_col[orow] = int16_t(int(cf));
+          code_col[orow] = code_bits(cf);
           if (wh_col) wh_col[orow] = wh;
         }
         sm.ds[cj][li] = d;
@@ -294,7 +296,7 @@ static_assert(sizeof(((Smem*)0)->u.la) <= kGtEarly * kB * sizeof(float), "early 
 // phase timestamps (globaltimer ns) of one traced launch, per CTA
 __device__ unsigned long long g_trace[1024 * 8];
 __device__ __forceinline__ void stamp(int trace, int i) {
-  if (trace && threadIdx.x == 0) {
+  if ((trace & 1) && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (blockIdx.x < 1024) g_trace[blockIdx.x * 8 + i] = t;
@@ -397,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
 
   // ---- per-(row, column) table {w, s, 1/s, z}: task = (row, 4 columns)
   const bool wvec = (ldw & 3) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
+  bool sbad = false;  // a scale outside scale_safe(): the chain divides exactly
 #pragma unroll
   for (int i = 0; i < kB * kCols4 / 4 / kThreads; ++i) {
     const int e = tid + i * kThreads;
@@ -422,6 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
     if (g0 == g3) {
       const float sv = __ldg(scales + g0);
       const float y = rcp_refined(sv), zf = float(__ldg(zeros + g0));
+      sbad |= !scale_safe(sv);
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         dst[u] = jj + u < m ? make_float4(wv[u], sv, y, zf) : make_float4(0.f, 1.f, 1.f, 0.f);
@@ -431,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
         if (jj + u < m) {
           const long long g = group_of(c, orig, jj + u);
           const float sv = __ldg(scales + g);
+          sbad |= !scale_safe(sv);
           dst[u] = make_float4(wv[u], sv, rcp_refined(sv), float(__ldg(zeros + g)));
         } else {
           dst[u] = make_float4(0.f, 1.f, 1.f, 0.f);
@@ -505,10 +510,13 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
   }
   stamp(trace, 2);
   cp_async_wait<0>();
-  __syncthreads();
+  const bool exact_div = __syncthreads_or(sbad || (trace & 2));
   stamp(trace, 3);
 
-  {
+  // the chain, specialised on the division: the residual step alone (all
+  // scales safe, the normal case) or the IEEE routine; no branch per row
+  auto chain = [&](auto exact) {
+    constexpr bool kExact = decltype(exact)::value;
     if (bprev > 0) {
 #pragma unroll
       for (int k = 0; k < kRpt; ++k) r[k] += sm.ds[cj][rg + 8 * k];
@@ -539,14 +547,14 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
           }
           const float4 tv = sm.tab[li][cj];  // (w, s, 1/s, z) of row li
           const float x = __fadd_rn(tv.x, r[tt]);  // w_cur = w + sum G D (owner lanes)
-          const float cf = quantize_code_f(div_rn_fast(x, tv.y, tv.z), tv.w, qminf, qmaxf);
+          const float qv = kExact ? __fdiv_rn(x, tv.y) : div_rn_residual(x, tv.y, tv.z);
+          const float cf = quantize_code_f(qv, tv.w, qminf, qmaxf);
           const float wh = __fmul_rn(tv.y, __fsub_rn(cf, tv.w));  // quant.cpp:33-35
-          float d = __fsub_rn(tv.x, wh);
-          if (rg == o) {  // stores leave with the epilogue
+          const float d = __shfl_sync(0xffffffffu, __fsub_rn(tv.x, wh), cc + 4 * o);
+          if (rg == o) {  // the owner's own d; stores leave with the epilogue
             sm.ds[cj][li] = d;
-            sm.cs[cj][li] = int16_t(int(cf));
+            sm.cs[cj][li] = code_bits(cf);
           }
-          d = __shfl_sync(0xffffffffu, d, cc + 4 * o);
 #pragma unroll
           for (int k = 0; k < kRpt; ++k) r[k] = fmaf(g[k], d, r[k]);
         }
@@ -554,7 +562,11 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
 #pragma unroll
       for (int k = 0; k < kRpt; ++k) r[k] = k + 2 < kRpt ? r[k + 2] : 0.f;
     }
-  }
+  };
+  if (exact_div)
+    chain(std::true_type{});
+  else
+    chain(std::false_type{});
   __syncthreads();
   stamp(trace, 4);
   // ---- D (K-major, the trailing GEMM's B operand), then codes / W_hat in
@@ -615,6 +627,9 @@ void launch_inblock4(const float* w, long long ldw, const int32_t* order, const 
     return true;
   }();
   (void)attr;
+  // OCWG_SWEEP_EXACT_DIV=1 (tests): the IEEE-division chain even with safe scales
+  const char* ex = std::getenv("OCWG_SWEEP_EXACT_DIV");
+  trace = (trace ? 1 : 0) | (ex && std::atoi(ex) ? 2 : 0);
   const unsigned ctas = unsigned((m + l4::kCols4 - 1) / l4::kCols4);
   count_launches(1);
   l4::inblock4_kernel<<<ctas, l4::kThreads, sizeof(l4::Smem), st>>>(w, ldw, order, acc, use_acc, gpl, gtt,

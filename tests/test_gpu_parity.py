@@ -296,3 +296,27 @@ def test_quantize_layer_end_to_end_c1(g, ref, orc):
     obj = ref.activation_objective(w, q.w_hat, h_ref)
     obj0 = ref.activation_objective(w, np.zeros_like(w), h_ref)
     assert abs(np.sqrt(obj / obj0) - float(gd["rel_err"])) <= 1e-3
+
+
+@pytest.mark.parametrize("bits,scheme", [(4, "asymmetric"), (3, "symmetric")])
+def test_sweep_residual_division_equals_ieee(g, ref, monkeypatch, bits, scheme):
+    # The 128-row chain divides by one residual step when every scale is in
+    # [2^-40, 2^40] (always, for fp16 grids) and by the IEEE routine otherwise;
+    # both are correctly rounded, so codes and W_hat agree bit for bit -- with
+    # zeros, outliers and negative (symmetric) codes in the mix.
+    n, m = 1024, 512
+    x = ref.random_gaussian(2 * n, n, 77)
+    x[:, ::13] *= 25.0
+    h = (x.T.astype(np.float64) @ x.astype(np.float64)).astype(np.float32)
+    w = ref.random_gaussian(n, m, 78, 0.02)
+    w[::7, ::5] = 0.0
+    w[3, :] *= 400.0
+    cfg = g.QuantConfig(bits, getattr(g.Scheme, scheme), g.Granularity.per_group, 128)
+    opts = g.GptqOptions(True, 0.01, 128)
+    q1 = g.gptq_quantize(w, h, cfg, opts, want_w_hat=True)
+    monkeypatch.setenv("OCWG_SWEEP_EXACT_DIV", "1")
+    q2 = g.gptq_quantize(w, h, cfg, opts, want_w_hat=True)
+    np.testing.assert_array_equal(q1.codes, q2.codes)
+    np.testing.assert_array_equal(q1.w_hat, q2.w_hat)
+    if scheme == "symmetric":
+        assert q1.codes.min() < 0
