@@ -285,7 +285,7 @@ struct Smem {
       float dp[2][kCols4][kLa4 + 4];
     } la;
   } u;
-  float4 tab[kB][kCols4];  // {w, s, 1/s, z} of (row li, column cj)
+  float4 tab[kB + 1][kCols4];  // {w, s, 1/s, z} of (row li, column cj); +1 row read ahead
   float ds[kCols4][kB + 1];  // D = w - w_hat of (column, row); lookahead hand-off first
   int16_t cs[kCols4][kB + 2];  // codes of (column, row)
   long long orow[kB];
@@ -527,6 +527,10 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
     // step loop has no per-row branch and the next row's loads hoist freely.
     // Per 16 rows (T) the slots rotate by 2; logical slot pair T + mm of lane
     // group rg sits at off[mm] (factor.cu gp_pos: conflict-free 8-byte loads).
+    // the table entry of the next row is read one row ahead: the owner's add
+    // of row li then never waits on shared memory (this row's stores precede
+    // the read in program order, so the compiler cannot hoist it itself)
+    float4 tvn = sm.tab[0][cj];
 #pragma unroll 1
     for (int T = 0; T < kRpt / 2; ++T) {
       if (16 * T >= bsz) break;
@@ -539,13 +543,14 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
 #pragma unroll
         for (int o = 0; o < kLpc; ++o) {
           const int lj = 8 * tt + o, li = 16 * T + lj;
+          const float4 tv = tvn;  // (w, s, 1/s, z) of row li
+          tvn = sm.tab[li + 1][cj];
           float g[kRpt];
 #pragma unroll
           for (int mm = 0; mm < 8; ++mm) {
             const float2 g2 = *reinterpret_cast<const float2*>(&sm.u.gt[off[mm] + lj * kB]);
             g[2 * mm] = g2.x, g[2 * mm + 1] = g2.y;
           }
-          const float4 tv = sm.tab[li][cj];  // (w, s, 1/s, z) of row li
           const float x = __fadd_rn(tv.x, r[tt]);  // w_cur = w + sum G D (owner lanes)
           const float qv = kExact ? __fdiv_rn(x, tv.y) : div_rn_residual(x, tv.y, tv.z);
           const float cf = quantize_code_f(qv, tv.w, qminf, qmaxf);
