@@ -103,12 +103,15 @@ void set_tc_workspace(float* ws, size_t floats);
 bool tc_gemm_presplit(long long m, long long n, long long k, float alpha, const float* a_hi,
                       const float* a_lo, long long lda, const float* b_hi, const float* b_lo,
                       long long ldb, float beta, float* c, long long ldc, cudaStream_t st,
-                      int max_ctas = 0);
+                      int max_ctas = 0, bool pdl = false);
 // The same product on 2-SM pairs (cta_group::2, 256 x 256 tiles, tc_gemm2.cu):
 // half the per-SM operand traffic; false if unsupported (caller falls back).
 bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const float* a_hi,
                        const float* a_lo, long long lda, const float* b_hi, const float* b_lo,
-                       long long ldb, float beta, float* c, long long ldc, cudaStream_t st);
+                       long long ldb, float beta, float* c, long long ldc, cudaStream_t st,
+                       bool pdl = false);
+// pdl: launched as a programmatic dependent of the previous kernel on st (the
+// kernel's setup overlaps that kernel's tail; its loads wait in griddepcontrol)
 // Dispatch: T = float -> tcgen05 3xTF32 (when a workspace is set and the
 // problem is big enough to fill tiles), else SIMT.
 template <typename T>

@@ -378,19 +378,14 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
   const long long j = j0 + cj;
   const bool col_ok = j < m;
 
-  // ---- row order (one row per thread) and this thread's acc rows, in flight together
-  float r[kRpt];  // slot s = row rg + 8s (acc = earlier super-blocks)
-#pragma unroll
-  for (int k = 0; k < kRpt; ++k) {
-    const int li = rg + 8 * k;
-    r[k] = (use_acc && col_ok && li < bsz) ? acc[(ib + li) * m + j] : 0.f;
-  }
-  // ---- async: late G rows (never overlapped by the lookahead buffers), lookahead chunk 0
+  // Up to the table, the prologue reads only what the sweep never writes (order,
+  // W, grids, G): as a programmatic dependent it runs beside the previous
+  // kernel's tail; acc and the lookahead D (previous kernels' outputs) follow
+  // griddepcontrol.wait.
+  // ---- async: late G rows (never overlapped by the lookahead buffers)
   const long long kprev = ib - bprev;
   stage_gt(sm, gpb, ib, bsz, bprev > 0 ? kGtEarly : 0, kB, tid);
   if (tid < 8) reinterpret_cast<float4*>(&sm.u.gt[kB * kB])[tid] = make_float4(0.f, 0.f, 0.f, 0.f);
-  cp_async_commit();
-  if (bprev > 0) stage_la(sm, 0, gpl, dprev, n, m, ib, bsz, kprev, bprev, 0, j0, ldd, tid);
   cp_async_commit();
   sm.og[tid] = og;
   sm.orow[tid] = (long long)og * ldo;
@@ -444,6 +439,16 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
     }
   }
   stamp(trace, 7);
+  pdl_wait();
+  // ---- this thread's acc rows (earlier super-blocks) and lookahead chunk 0
+  float r[kRpt];  // slot s = row rg + 8s
+#pragma unroll
+  for (int k = 0; k < kRpt; ++k) {
+    const int li = rg + 8 * k;
+    r[k] = (use_acc && col_ok && li < bsz) ? acc[(ib + li) * m + j] : 0.f;
+  }
+  if (bprev > 0) stage_la(sm, 0, gpl, dprev, n, m, ib, bsz, kprev, bprev, 0, j0, ldd, tid);
+  cp_async_commit();
   stamp(trace, 1);
 
   // ---- lookahead: G[blk, sb0:ib] D[sb0:ib] on the tensor cores (3xTF32,
@@ -572,6 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
     chain(std::true_type{});
   else
     chain(std::false_type{});
+  pdl_trigger();  // the next kernel's setup may start as these CTAs drain
   __syncthreads();
   stamp(trace, 4);
   // ---- D (K-major, the trailing GEMM's B operand), then codes / W_hat in
@@ -625,7 +631,7 @@ void launch_inblock4(const float* w, long long ldw, const int32_t* order, const 
                      float* dcur, float* dch, float* dcl, const QCfg& c, const float* scales,
                      const int32_t* zeros, long long n, long long m, long long ib, int bsz,
                      int16_t* codes, float* w_hat, long long ldo, long long ldd, int trace,
-                     cudaStream_t st) {
+                     bool pdl, cudaStream_t st) {
   static const bool attr = [] {
     cudaFuncSetAttribute(l4::inblock4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(sizeof(l4::Smem)));
@@ -637,10 +643,19 @@ void launch_inblock4(const float* w, long long ldw, const int32_t* order, const 
   trace = (trace ? 1 : 0) | (ex && std::atoi(ex) ? 2 : 0);
   const unsigned ctas = unsigned((m + l4::kCols4 - 1) / l4::kCols4);
   count_launches(1);
-  l4::inblock4_kernel<<<ctas, l4::kThreads, sizeof(l4::Smem), st>>>(w, ldw, order, acc, use_acc, gpl, gtt,
-                                                          dprev, bprev, dcur, dch, dcl, c, scales,
-                                                          zeros, n, m, ib, bsz, codes, w_hat, ldo,
-                                                          ldd, trace);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(l4::kThreads);
+  cfg.dynamicSmemBytes = sizeof(l4::Smem);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, l4::inblock4_kernel, w, ldw, order, acc, use_acc, gpl, gtt, dprev, bprev,
+                     dcur, dch, dcl, c, scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, ldd,
+                     trace);
 }
 
 template <typename T, int RPT>
@@ -699,6 +714,12 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
     const char* e = getenv("OCWG_SWEEP_TRACE_IB");
     return e ? atoll(e) : -1LL;
   }();
+  // programmatic dependent launches between the sweep's own kernels (not the
+  // first: it follows the factorisation and the grids' event); OCWG_SWEEP_PDL=0 off
+  static const bool pdl_on = [] {
+    const char* e = getenv("OCWG_SWEEP_PDL");
+    return !(e && e[0] == '0');
+  }();
   static const int skip = [] {
     const char* e = getenv("OCWG_SWEEP_SKIP");
     return !e ? 0 : (e[0] == 'i' ? 1 : (e[0] == 'g' ? 2 : 0));
@@ -726,7 +747,7 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
                         reinterpret_cast<const float*>(gpl), gtt,
                         reinterpret_cast<const float*>(dpl[p]), bprev,
                         reinterpret_cast<float*>(dcur), dch, dcl, c, scales, zeros, n, m, ib, bsz,
-                        codes, w_hat, ldo, kSuperRows, ib == trace_ib, st);
+                        codes, w_hat, ldo, kSuperRows, ib == trace_ib, pdl_on && ib > 0, st);
       else
         launch_inblock<T, 16>(w, ldw, order, acc, use_acc, gpl, dpl[p], bprev, dcur, dch, dcl, c,
                               scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, kSuperRows, st);
@@ -749,12 +770,12 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
           done = tc_gemm2_presplit(n - se, m, kk, 1.0f,
                                    reinterpret_cast<const float*>(ghi) + se * n + s0,
                                    glo + se * n + s0, n, dhi[p], dlo[p], kSuperRows, float(beta),
-                                   reinterpret_cast<float*>(acc) + se * m, m, st);
+                                   reinterpret_cast<float*>(acc) + se * m, m, st, pdl_on);
         if (split && !done)
           done = tc_gemm_presplit(n - se, m, kk, 1.0f,
                                   reinterpret_cast<const float*>(ghi) + se * n + s0,
                                   glo + se * n + s0, n, dhi[p], dlo[p], kSuperRows, float(beta),
-                                  reinterpret_cast<float*>(acc) + se * m, m, st);
+                                  reinterpret_cast<float*>(acc) + se * m, m, st, 0, pdl_on);
       }
       if (!done)
         gemm<T, T, T>(n - se, m, kk, 1.0, gpl + se * n + s0, n, false, dpl[p], kSuperRows, true,

@@ -147,6 +147,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_holder;
+  // programmatic dependent launch (no-op otherwise): setup above overlaps the
+  // previous kernel, whose outputs may be B and C
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // t -> (batch, tm, tn); the operand rows of batch b start at b*m (A) / b*n (B)
   const int per_batch = tiles_m * tiles_n;
@@ -448,7 +452,7 @@ bool tc_gemm_tf32x3(int batch, long long m, long long n, long long k, float alph
 bool tc_gemm_presplit(long long m, long long n, long long k, float alpha, const float* a_hi,
                       const float* a_lo, long long lda, const float* b_hi, const float* b_lo,
                       long long ldb, float beta, float* c, long long ldc, cudaStream_t st,
-                      int max_ctas) {
+                      int max_ctas, bool pdl) {
   if (m <= 0 || n <= 0) return true;
   if (!encoder() || k <= 0 || m >= (1LL << 31) || n >= (1LL << 31)) return false;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -464,6 +468,20 @@ bool tc_gemm_presplit(long long m, long long n, long long k, float alpha, const 
   const int cap = max_ctas > 0 ? std::min(max_ctas, num_sms_tc()) : num_sms_tc();
   const int grid = std::min(ntiles, cap);
   count_launches(1);
+  if (pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel, mah, mal, mbh, mbl, 0, 0, m, n, k, alpha, beta,
+                              c, ldc, 0LL, 0, tiles_m, tiles_n, ntiles) == cudaSuccess;
+  }
   tc_gemm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(mah, mal, mbh, mbl, 0, 0, m, n, k, alpha, beta,
                                                     c, ldc, 0, 0, tiles_m, tiles_n, ntiles);
   return cudaGetLastError() == cudaSuccess;

@@ -157,6 +157,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_holder;
+  // programmatic dependent launch: setup above overlaps the previous kernel;
+  // B (D) and C (acc) are its outputs.  Dependents may start their own setup.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ====================== TMA producer (both CTAs, own halves) ======================
@@ -343,7 +347,8 @@ int num_sms3() {
 
 bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const float* a_hi,
                        const float* a_lo, long long lda, const float* b_hi, const float* b_lo,
-                       long long ldb, float beta, float* c, long long ldc, cudaStream_t st) {
+                       long long ldb, float beta, float* c, long long ldc, cudaStream_t st,
+                       bool pdl) {
   if (m <= 0 || n <= 0) return true;
   if (!encoder3() || k <= 0 || m >= (1LL << 31) || n >= (1LL << 31)) return false;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -366,13 +371,15 @@ bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   count_launches(1);
   return cudaLaunchKernelEx(&cfg, tc_gemm2_kernel, mah, mal, mbh, mbl, m, n, k, alpha, beta, c,
                             ldc, tiles_n, ntiles) == cudaSuccess;
