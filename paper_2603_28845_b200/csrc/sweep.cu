@@ -536,12 +536,13 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
     // of row li then never waits on shared memory (this row's stores precede
     // the read in program order, so the compiler cannot hoist it itself)
     float4 tvn = sm.tab[0][cj];
-#pragma unroll 1
-    for (int T = 0; T < kRpt / 2; ++T) {
-      if (16 * T >= bsz) break;
-      int off[8];
+    // 16 rows; LIVE slots: from T = 4 on, slots 8..15 hold rows past the block
+    // (16T + 8s + rg >= 128), so half the coefficient loads and FMAs drop out
+    auto rows16 = [&](int T, auto live_c) {
+      constexpr int LIVE = decltype(live_c)::value;
+      int off[LIVE / 2];
 #pragma unroll
-      for (int mm = 0; mm < 8; ++mm)
+      for (int mm = 0; mm < LIVE / 2; ++mm)
         off[mm] = 16 * T * kB + rg * 16 + 2 * ((T + mm + 2 * (rg >> 1)) & 7);
 #pragma unroll
       for (int tt = 0; tt < 2; ++tt) {
@@ -550,27 +551,41 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
           const int lj = 8 * tt + o, li = 16 * T + lj;
           const float4 tv = tvn;  // (w, s, 1/s, z) of row li
           tvn = sm.tab[li + 1][cj];
-          float g[kRpt];
+          float g[LIVE];
 #pragma unroll
-          for (int mm = 0; mm < 8; ++mm) {
+          for (int mm = 0; mm < LIVE / 2; ++mm) {
             const float2 g2 = *reinterpret_cast<const float2*>(&sm.u.gt[off[mm] + lj * kB]);
             g[2 * mm] = g2.x, g[2 * mm + 1] = g2.y;
           }
           const float x = __fadd_rn(tv.x, r[tt]);  // w_cur = w + sum G D (owner lanes)
           const float qv = kExact ? __fdiv_rn(x, tv.y) : div_rn_residual(x, tv.y, tv.z);
-          const float cf = quantize_code_f(qv, tv.w, qminf, qmaxf);
-          const float wh = __fmul_rn(tv.y, __fsub_rn(cf, tv.w));  // quant.cpp:33-35
+          // code - z = clamp(rint(q), qmin - z, qmax - z) (quantize_code_f,
+          // shifted by z so W_hat = s (code - z) needs no subtraction on the chain)
+          const float loz = __fsub_rn(qminf, tv.w), hiz = __fsub_rn(qmaxf, tv.w);
+          const float u = __fsub_rn(__fadd_rn(qv, kRoundShifter), kRoundShifter);
+          const float cl = fminf(fmaxf(u, loz), qv < 2147483648.0f ? hiz : loz);
+          const float wh = __fmul_rn(tv.y, cl);  // quant.cpp:33-35
           const float d = __shfl_sync(0xffffffffu, __fsub_rn(tv.x, wh), cc + 4 * o);
           if (rg == o) {  // the owner's own d; stores leave with the epilogue
             sm.ds[cj][li] = d;
-            sm.cs[cj][li] = code_bits(cf);
+            sm.cs[cj][li] = code_bits(__fadd_rn(cl, tv.w));
           }
 #pragma unroll
-          for (int k = 0; k < kRpt; ++k) r[k] = fmaf(g[k], d, r[k]);
+          for (int k = 0; k < LIVE; ++k) r[k] = fmaf(g[k], d, r[k]);
         }
       }
 #pragma unroll
-      for (int k = 0; k < kRpt; ++k) r[k] = k + 2 < kRpt ? r[k + 2] : 0.f;
+      for (int k = 0; k < LIVE; ++k) r[k] = k + 2 < LIVE ? r[k + 2] : 0.f;
+    };
+#pragma unroll 1
+    for (int T = 0; T < 4; ++T) {
+      if (16 * T >= bsz) return;
+      rows16(T, std::integral_constant<int, kRpt>{});
+    }
+#pragma unroll 1
+    for (int T = 4; T < kRpt / 2; ++T) {
+      if (16 * T >= bsz) return;
+      rows16(T, std::integral_constant<int, kRpt / 2>{});
     }
   };
   if (exact_div)
