@@ -20,7 +20,9 @@
 // beta = 0 and the first super-block never reads it.
 //
 // fp32 path (l4::inblock4_kernel, B = 128): 16 columns per 4-warp CTA, 8
-// lanes per column, 16 rotating register slots per lane; see the kernel.
+// lanes per column, 16 rotating register slots per lane; a branch-free
+// quantise chain (residual division, shifter rounding); the sweep's kernels
+// are chained by programmatic dependent launch.  See the kernel.
 // Generic path (inblock_g_kernel: fp64, or B != 128): a CTA owns 32 columns
 // (8 warps x 4); lane = cc + 4*rg keeps rows rg, rg+8, ... of its column in
 // registers, rotating by one slot per 8-row group; D is broadcast with one
