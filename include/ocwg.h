@@ -83,7 +83,8 @@ int ocwg_version(void);
 /* Context on one CUDA device: stream, workspace pool, device status word. */
 int ocwg_create(int device, ocwg_ctx** out);
 int ocwg_destroy(ocwg_ctx* ctx);
-/* OCWG_FP32 (default, fast) or OCWG_FP64 (reference arithmetic class). */
+/* OCWG_FP32 (default, fast: tensor-core statistics, fp32 factorisation +
+ * 3xTF32 sweep) or OCWG_FP64 (the reference's arithmetic class throughout). */
 int ocwg_set_precision(ocwg_ctx* ctx, int precision);
 /* Run subsequent work on an external cudaStream_t (NULL = the CUDA legacy
  * default stream).  A new context uses its own non-blocking stream. */
@@ -138,7 +139,11 @@ int ocwg_unpack_uniform(ocwg_ctx* ctx, const uint8_t* payload, uint64_t len, uin
 /* ---- stats.hpp --------------------------------------------------------- */
 /* accumulate_stats (stats.cpp:10-19): gram += Xp^T Xp; cross += Xp^T (X - Xp),
  * fp64 n x n row-major, updated in place; cross may be NULL when
- * x_fp == x_pert (then cross is identically 0, test_core.cpp:273-279). */
+ * x_fp == x_pert (then cross is identically 0, test_core.cpp:273-279).
+ * OCWG_FP32 precision (default): tcgen05 tensor cores on bf16 parts of the
+ * inputs (Xp = P1 + P2, X - Xp = D1 + D2; gram = P1'P1 + P1'P2 + P2'P1,
+ * cross = P1'D1 + P1'D2 + P2'D1; fp32 accumulation per 2048 tokens, fp64
+ * across), |dH_ij| <~ 1e-5 sqrt(H_ii H_jj).  OCWG_FP64: fp64 SIMT GEMMs. */
 int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert, uint64_t rows,
                           uint64_t dim, double* gram, double* cross, uint64_t* token_count);
 /* Hessian of bf16 calibration tokens on the tensor cores: H (+)= X^T X.
@@ -164,13 +169,20 @@ int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, do
  * N x N fp64 (CalibStats), W / out: N x M fp32 (out may alias W). */
 int ocwg_qep_target(ocwg_ctx* ctx, const float* w, const double* gram, const double* cross,
                     uint64_t n, uint64_t m, double alpha, double eta, float* out);
-/* quantize_layer (layerwise.cpp:120-126) over fp64 stats (gram N x N);
- * method: 0 rtn, 1 gptq.  qep must be 0 here: the QEP-corrected target comes
- * from ocwg_qep_target first (as quantize_layer does, layerwise.cpp:121). */
-int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, uint64_t n, uint64_t m,
-                        int method, const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
-                        int scale_mode, int qep, int16_t* codes, float* scales, int32_t* zeros,
-                        float* w_hat);
+/* QepOptions (layerwise.hpp:33-36) */
+typedef struct ocwg_qep_options {
+  double alpha; /* [0, 1] */
+  double eta;   /* > 0 */
+} ocwg_qep_options;
+/* quantize_layer (layerwise.cpp:120-126) over fp64 CalibStats (gram, cross:
+ * N x N), in one device round trip: [qep_target when qep != NULL] -> RTN
+ * (method 0) or GPTQ (method 1) on fp32(gram).  cross may be NULL without
+ * QEP.  w_hat (N x M dequantized) may be NULL. */
+int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, const double* cross,
+                        uint64_t n, uint64_t m, int method, const ocwg_quant_config* cfg,
+                        const ocwg_gptq_options* opts, int scale_mode,
+                        const ocwg_qep_options* qep, int16_t* codes, float* scales,
+                        int32_t* zeros, float* w_hat);
 
 /* ---- end-to-end layer quantize from calibration tokens (north_star call) --
  * W (N x M fp32) + X (T x N bf16) -> codes, grids, dequantized W and the

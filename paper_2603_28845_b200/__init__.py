@@ -207,8 +207,8 @@ _SIGS = {
     "ocwg_gptq_quantize": (C.c_int, [_P, _P, _P, _U64, _U64, C.POINTER(_QCfg), C.POINTER(_GOpt),
                                      C.c_int, _P, _P, _P, _P]),
     "ocwg_gptq_factor": (C.c_int, [_P, _P, _U64, C.c_int, C.c_double, _P, _P, _P, _P]),
-    "ocwg_quantize_layer": (C.c_int, [_P, _P, _P, _U64, _U64, C.c_int, C.POINTER(_QCfg),
-                                      C.POINTER(_GOpt), C.c_int, C.c_int, _P, _P, _P, _P]),
+    "ocwg_quantize_layer": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.c_int, C.POINTER(_QCfg),
+                                      C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P]),
     "ocwg_quantize_layer_x": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, C.POINTER(_QCfg),
                                         C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P, _U64, _P]),
     "ocwg_candidate_grid": (C.c_int, [_P, _P, _U64, _U64, C.c_int, _P, _P, _P]),
@@ -487,14 +487,40 @@ def base_method_from_name(name: str) -> str:
     raise InvalidInput(f"unknown quantization method: {name}")
 
 
-def quantize_layer(w, stats: CalibStats, opts: LayerQuantOptions, device: int = 0) -> QuantizedMatrix:
-    """layerwise.cpp:120-126: [qep_target] -> RTN or GPTQ on stats.gram_matrix()."""
-    target = qep_target(w, stats, opts.qep, device) if opts.qep is not None else _f32(w)
+class _QepOpt(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("eta", C.c_double)]
+
+
+def quantize_layer(w, stats: CalibStats, opts: LayerQuantOptions, device: int = 0,
+                   want_w_hat: bool = False) -> QuantizedMatrix:
+    """layerwise.cpp:120-126: [qep_target] -> RTN or GPTQ on stats.gram_matrix(),
+    in one device round trip (ocwg_quantize_layer)."""
+    w = _f32(w)
     method = base_method_from_name(opts.method)
-    if method == "rtn":
-        return quantize_matrix(target, opts.config, opts.scale_mode, device)
-    return gptq_quantize(target, stats.gram_matrix(), opts.config, opts.gptq, opts.scale_mode,
-                         device=device)
+    n, m = w.shape
+    if method == "rtn" and opts.qep is None:  # quantize_matrix ignores the statistics
+        q = quantize_matrix(w, opts.config, opts.scale_mode, device)
+        if want_w_hat:
+            q.w_hat = dequantize(q, device)
+        return q
+    if stats.dim() != n:
+        raise InvalidInput("qep_target: stats dimension does not match W rows" if opts.qep is not None
+                           else "gptq_quantize: H must be N x N with N = rows of W")
+    gram = np.ascontiguousarray(stats.gram, np.float64)
+    cross = np.ascontiguousarray(stats.cross, np.float64) if opts.qep is not None else None
+    qep = _QepOpt(float(opts.qep.alpha), float(opts.qep.eta)) if opts.qep is not None else None
+    cfg = opts.config
+    ng = quant_group_count(cfg, n, m)
+    codes = np.zeros((n, m), np.int16)
+    scales = np.zeros(ng, np.float32)
+    zeros = np.zeros(ng, np.int32)
+    w_hat = np.zeros((n, m), np.float32) if want_w_hat else None
+    c, o = cfg._c(), opts.gptq._c()
+    _check(lib().ocwg_quantize_layer(context(device).handle, _ptr(w), _ptr(gram), _ptr(cross), n, m,
+                                     1 if method == "gptq" else 0, C.byref(c), C.byref(o),
+                                     int(opts.scale_mode), C.byref(qep) if qep is not None else None,
+                                     _ptr(codes), _ptr(scales), _ptr(zeros), _ptr(w_hat)))
+    return QuantizedMatrix(n, m, cfg, codes, scales, zeros, w_hat)
 
 
 class LayerOutputs:

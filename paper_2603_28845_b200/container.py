@@ -125,10 +125,13 @@ def deserialize_ocw(data: bytes, decode: bool = True):
         raise IoError(f"container: bad header ({e})") from None
     body = data[12 + hlen:]
     out = []
+    expected = 0
     for t in header.get("tensors", []):
         off, nb = int(t["offset"]), int(t["bytes"])
+        if off != expected:  # container.cpp:404
+            raise IoError("container: tensor offsets must be ascending and packed")
         if off + nb > len(body):
-            raise IoError(f"container: payload out of range for {t['name']}")
+            raise IoError("container: tensor exceeds payload")
         r = Record(t["name"], t["encoding"], tuple(int(v) for v in t["shape"]),
                    t.get("params", {}), body[off:off + nb])
         if r.encoding not in ("f32", "uniform-quant"):
@@ -142,6 +145,9 @@ def deserialize_ocw(data: bytes, decode: bool = True):
             else:
                 r.value = unpack_uniform(r.payload, rows, cols, _config(r.params))
         out.append(r)
+        expected = off + nb
+    if expected != len(body):  # container.cpp:411
+        raise IoError("container: payload length does not match tensor sizes")
     return header.get("meta", {}), out
 
 

@@ -26,13 +26,21 @@
 namespace ocw {
 namespace {
 
-ocwg_ctx* ctx() {  // one context per host thread (concurrent calls)
+// One context per host thread (concurrent calls).
+// Arithmetic: OCWG_FP32 by default -- tensor-core statistics (bf16 parts, fp32
+// per 2048-token window, fp64 across), fp32 Cholesky and 3xTF32 sweep: codes
+// >= 99.9 % identical to the reference's fp64 path, H within 1e-5 of it.
+// OCW_GPU_PRECISION=fp64 selects the reference's arithmetic class (fp64
+// factorisation, sweep and statistics) for bit-level comparisons.
+ocwg_ctx* ctx() {
   thread_local struct Holder {
     ocwg_ctx* c = nullptr;
     Holder() {
       const char* d = std::getenv("OCWG_DEVICE");
       if (ocwg_create(d ? std::atoi(d) : 0, &c) != OCWG_OK)
         throw std::runtime_error(std::string("ocwg_create: ") + ocwg_last_error());
+      const char* p = std::getenv("OCW_GPU_PRECISION");
+      if (p && std::strcmp(p, "fp64") == 0) ocwg_set_precision(c, OCWG_FP64);
     }
     ~Holder() { ocwg_destroy(c); }
   } h;
@@ -288,12 +296,34 @@ BaseQuantMethod base_method_from_name(const std::string& name) {
   throw invalid_input("unknown quantization method: " + name);
 }
 
+// [qep_target] -> RTN / GPTQ on stats.gram_matrix() (layerwise.cpp:120-126) in
+// one device round trip: W and the fp64 statistics go in once, the QEP target
+// and fp32(gram) stay on the device.
 QuantizedMatrix quantize_layer(const Matrix& w, const CalibStats& stats,
                                const LayerQuantOptions& opts) {
-  const Matrix target = opts.qep ? qep_target(w, stats, *opts.qep) : w;
-  if (opts.method == BaseQuantMethod::rtn)
-    return quantize_matrix(target, opts.config, opts.scale_mode);
-  return gptq_quantize(target, stats.gram_matrix(), opts.config, opts.gptq, opts.scale_mode);
+  if (opts.method == BaseQuantMethod::rtn && !opts.qep)
+    return quantize_matrix(w, opts.config, opts.scale_mode);
+  if (stats.dim() != w.rows)
+    throw invalid_input(opts.qep ? "qep_target: stats dimension does not match W rows"
+                                 : "gptq_quantize: H must be N x N with N = rows of W");
+  const QuantConfig& cfg = opts.config;
+  const ocwg_quant_config c = cc(cfg);
+  const ocwg_gptq_options o{opts.gptq.actorder ? 1 : 0, 0, opts.gptq.percdamp,
+                            uint64_t(opts.gptq.block_cols)};
+  ocwg_qep_options qo{};
+  if (opts.qep) qo = ocwg_qep_options{opts.qep->alpha, opts.qep->eta};
+  const std::vector<double> g = row_major(stats.gram);
+  const std::vector<double> cr = opts.qep ? row_major(stats.cross) : std::vector<double>{};
+  const size_t ng = quant_group_count(cfg, w.rows, w.cols);
+  std::vector<float> s(ng);
+  std::vector<int32_t> z(ng);
+  QuantizedMatrix q{w.rows, w.cols, cfg, std::vector<int16_t>(w.rows * w.cols), {}};
+  check(ocwg_quantize_layer(ctx(), w.data.data(), g.data(), opts.qep ? cr.data() : nullptr, w.rows,
+                            w.cols, opts.method == BaseQuantMethod::gptq ? 1 : 0, &c, &o,
+                            mode_of(opts.scale_mode), opts.qep ? &qo : nullptr, q.codes.data(),
+                            s.data(), z.data(), nullptr));
+  q.grids = grids_of(s, z, cfg);
+  return q;
 }
 
 }  // namespace ocw

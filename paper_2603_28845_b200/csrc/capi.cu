@@ -20,6 +20,20 @@ static std::atomic<unsigned long long> g_launches{0};
 void count_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 unsigned long long launches_issued() { return g_launches.load(std::memory_order_relaxed); }
 
+int device_sms() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 }  // namespace ocwg
 
 using namespace ocwg;
@@ -353,6 +367,37 @@ void check_gptq_args(const ocwg_quant_config* cfg, const ocwg_gptq_options* opts
     fail(OCWG_INVALID_INPUT, "gptq_quantize: percdamp must be in (0, 1]");
   (void)n;
   (void)m;
+}
+
+// H (+)= X^T X of bf16 X (device, tokens x n) on the tensor cores, any n:
+// rows are re-strided to a multiple of 8 elements (TMA's 16-byte row pitch)
+// into `pad` (hessian_pad_bytes) when n % 8 != 0.
+size_t hessian_pad_bytes(uint64_t tokens, uint64_t n) {
+  return n % 8 ? size_t(tokens) * size_t((n + 7) / 8 * 8) * 2 : 0;
+}
+void run_hessian(const uint16_t* x, uint64_t tokens, uint64_t n, float* h, bool accumulate,
+                 void* gws, size_t gws_bytes, uint16_t* pad, cudaStream_t st) {
+  if (tokens == 0) {
+    if (!accumulate) ck(cudaMemsetAsync(h, 0, n * n * 4, st), "memset");
+    return;
+  }
+  GramSpec s;
+  s.tokens = (long long)tokens;
+  s.dim = (long long)n;
+  s.ld = (long long)n;
+  s.ops[0] = x;
+  if (n % 8) {
+    s.ld = (long long)((n + 7) / 8 * 8);
+    launch_pad_bf16(x, (long long)tokens, (long long)n, s.ld, pad, st);
+    s.ops[0] = pad;
+  }
+  s.nops = 1;
+  s.gseg = 1;
+  s.gram = h;
+  s.accumulate = accumulate;
+  const int r = gram_tc(s, gws, gws_bytes, st);
+  if (r == -1) fail(OCWG_INVALID_INPUT, "hessian: shape outside the tensor-core kernel's range");
+  if (r != 0) fail(OCWG_CUDA_ERROR, "hessian: tensor-core kernel launch failed");
 }
 
 }  // namespace
@@ -739,24 +784,80 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
     if (!gram) fail(OCWG_INVALID_INPUT, "accumulate_stats: null gram");
     std::lock_guard<std::mutex> lk(ctx->mu);
     begin(ctx);
-    const bool same = (x_fp == x_pert);
-    Arena ar(ctx);
-    const size_t of = ar.reserve(rows * dim * 4), op = ar.reserve(rows * dim * 4),
-                 og = ar.reserve(dim * dim * 8), oc = ar.reserve(dim * dim * 8),
-                 od = ar.reserve(rows * dim * 8);
-    ar.commit();
-    h2d(ar.at<float>(op), x_pert, rows * dim * 4, ctx);
-    if (!same) h2d(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
-    h2d(ar.at<double>(og), gram, dim * dim * 8, ctx);
-    if (cross) h2d(ar.at<double>(oc), cross, dim * dim * 8, ctx);
-    const float* xf = same ? ar.at<float>(op) : ar.at<float>(of);
-    // cross += Xp^T (X - Xp) is identically zero when X == Xp: skip the GEMM
-    accumulate_stats_f64(xf, ar.at<float>(op), (long long)rows, (long long)dim, ar.at<double>(og),
-                         (cross && !same) ? ar.at<double>(oc) : nullptr, ar.at<double>(od),
-                         ctx->stream);
-    d2h(gram, ar.at<double>(og), dim * dim * 8, ctx);
-    if (cross && !same) d2h(cross, ar.at<double>(oc), dim * dim * 8, ctx);
-    finish(ctx);
+    // cross += Xp^T (X - Xp) is identically zero when X == Xp: skip it
+    const bool same = (x_fp == x_pert), want_cross = cross && !same;
+    if (rows == 0 || dim == 0) {
+      if (token_count) *token_count += rows;
+      return;
+    }
+    cudaStream_t st = ctx->stream;
+    if (ctx->precision == OCWG_FP64) {  // the reference's arithmetic class: fp64 SIMT GEMMs
+      Arena ar(ctx);
+      const size_t of = ar.reserve(rows * dim * 4), op = ar.reserve(rows * dim * 4),
+                   og = ar.reserve(dim * dim * 8), oc = ar.reserve(dim * dim * 8),
+                   od = ar.reserve(want_cross ? rows * dim * 8 : 8);
+      ar.commit();
+      h2d(ar.at<float>(op), x_pert, rows * dim * 4, ctx);
+      if (!same) h2d(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
+      h2d(ar.at<double>(og), gram, dim * dim * 8, ctx);
+      if (want_cross) h2d(ar.at<double>(oc), cross, dim * dim * 8, ctx);
+      const float* xf = same ? ar.at<float>(op) : ar.at<float>(of);
+      accumulate_stats_f64(xf, ar.at<float>(op), (long long)rows, (long long)dim, ar.at<double>(og),
+                           want_cross ? ar.at<double>(oc) : nullptr, ar.at<double>(od), st);
+      d2h(gram, ar.at<double>(og), dim * dim * 8, ctx);
+      if (want_cross) d2h(cross, ar.at<double>(oc), dim * dim * 8, ctx);
+      finish(ctx);
+    } else {
+      // tensor cores: X_hat = P1 + P2, X - X_hat = D1 + D2 (bf16 parts), fp64 outputs
+      const uint64_t ld = (dim + 7) / 8 * 8;
+      Arena ar(ctx);
+      const size_t op = ar.reserve(rows * dim * 4), of = ar.reserve(want_cross ? rows * dim * 4 : 4),
+                   o1 = ar.reserve(rows * ld * 2), o2 = ar.reserve(rows * ld * 2),
+                   o3 = ar.reserve(want_cross ? rows * ld * 2 : 16),
+                   o4 = ar.reserve(want_cross ? rows * ld * 2 : 16), og = ar.reserve(dim * dim * 8),
+                   oc = ar.reserve(want_cross ? dim * dim * 8 : 8), ofl = ar.reserve(16),
+                   ows = ar.reserve(gram_tc_workspace_bytes((long long)dim));
+      ar.commit();
+      h2d(ar.at<float>(op), x_pert, rows * dim * 4, ctx);
+      if (want_cross) h2d(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
+      h2d(ar.at<double>(og), gram, dim * dim * 8, ctx);
+      if (want_cross) h2d(ar.at<double>(oc), cross, dim * dim * 8, ctx);
+      unsigned* fl = ar.at<unsigned>(ofl);
+      ck(cudaMemsetAsync(fl, 0, 4, st), "memset");
+      uint16_t *p1 = ar.at<uint16_t>(o1), *p2 = ar.at<uint16_t>(o2), *d1 = ar.at<uint16_t>(o3),
+               *d2 = ar.at<uint16_t>(o4);
+      launch_split_bf16(ar.at<float>(op), want_cross ? ar.at<float>(of) : nullptr, (long long)rows,
+                        (long long)dim, (long long)ld, p1, p2, d1, d2, fl, st);
+      unsigned f = 0;
+      d2h(&f, fl, 4, ctx);
+      ck(cudaStreamSynchronize(st), "sync");
+      GramSpec s;
+      s.tokens = (long long)rows;
+      s.dim = (long long)dim;
+      s.ld = (long long)ld;
+      s.ops[0] = p1;
+      s.ops[1] = p2;
+      s.ops[2] = d1;
+      s.ops[3] = d2;
+      s.nops = 4;
+      // gram = P1'P1 (+ P1'P2 + P2'P1 when X_hat is not bf16-exact)
+      s.gseg = (f & 1u) ? 3 : 1;
+      const int ga[3] = {0, 0, 1}, gb[3] = {0, 1, 0};
+      // cross = P1'D1 + P1'D2 + P2'D1
+      s.cseg = (want_cross && (f & 2u)) ? 3 : 0;
+      const int ca[3] = {0, 0, 1}, cb[3] = {2, 3, 2};
+      for (int k = 0; k < 3; ++k) s.gA[k] = ga[k], s.gB[k] = gb[k], s.cA[k] = ca[k], s.cB[k] = cb[k];
+      s.gram = ar.at<double>(og);
+      s.cross = ar.at<double>(oc);
+      s.f64 = true;
+      s.accumulate = true;
+      s.window_tokens = 2048;  // short TMEM accumulations, fp64 across windows
+      const int r = gram_tc(s, ar.at<void>(ows), gram_tc_workspace_bytes((long long)dim), st);
+      if (r != 0) fail(OCWG_CUDA_ERROR, "accumulate_stats: tensor-core kernel launch failed");
+      d2h(gram, ar.at<double>(og), dim * dim * 8, ctx);
+      if (want_cross) d2h(cross, ar.at<double>(oc), dim * dim * 8, ctx);
+      finish(ctx);
+    }
     if (token_count) *token_count += rows;
   });
 }
@@ -777,14 +878,11 @@ int ocwg_debug_hessian_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, ui
       hessian_simt(x, (long long)tokens, (long long)dim, h, accumulate, ctx->stream);
     } else {
       Arena ar(ctx);
-      const size_t bytes = hessian_tc_workspace_bytes((long long)tokens, (long long)dim);
-      const size_t o = ar.reserve(bytes);
+      const size_t gb = gram_tc_workspace_bytes((long long)dim);
+      const size_t o = ar.reserve(gb), op = ar.reserve(hessian_pad_bytes(tokens, dim));
       ar.commit();
-      const int r = hessian_tc(x, (long long)tokens, (long long)dim, h, accumulate, ar.at<void>(o),
-                               bytes, ctx->stream);
-      if (r == -1)
-        fail(OCWG_UNSUPPORTED, "hessian: dim must be a multiple of 8 for the tensor-core path");
-      if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
+      run_hessian(x, tokens, dim, h, accumulate != 0, ar.at<void>(o), gb, ar.at<uint16_t>(op),
+                  ctx->stream);
     }
     finish_dev(ctx);
   });
@@ -945,27 +1043,79 @@ int ocwg_gptq_quantize(ocwg_ctx* ctx, const float* w, const float* h, uint64_t n
   });
 }
 
-int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, uint64_t n, uint64_t m,
-                        int method, const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
-                        int mode, int qep, int16_t* codes, float* scales, int32_t* zeros,
-                        float* w_hat) {
+int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, const double* cross,
+                        uint64_t n, uint64_t m, int method, const ocwg_quant_config* cfg,
+                        const ocwg_gptq_options* opts, int mode, const ocwg_qep_options* qep,
+                        int16_t* codes, float* scales, int32_t* zeros, float* w_hat) {
   return guard([&] {
-    if (qep) fail(OCWG_UNSUPPORTED, "quantize_layer: QEP target correction not built yet");
-    if (method == 0) {
-      const int r = ocwg_quantize_matrix(ctx, w, n, m, cfg, mode, codes, scales, zeros);
-      if (r != OCWG_OK) fail(r, g_err);
-      if (w_hat) {
-        const int r2 = ocwg_dequantize(ctx, codes, scales, zeros, n, m, cfg, w_hat);
-        if (r2 != OCWG_OK) fail(r2, g_err);
-      }
-      return;
+    if (method != 0 && method != 1) fail(OCWG_INVALID_INPUT, "unknown quantization method");
+    if (qep) {  // qep_target's checks come first (layerwise.cpp:96-101, 121)
+      if (!(qep->alpha >= 0.0 && qep->alpha <= 1.0))
+        fail(OCWG_INVALID_INPUT, "qep_target: alpha must be in [0,1]");
+      if (!(qep->eta > 0.0)) fail(OCWG_INVALID_INPUT, "qep_target: eta must be positive");
+      if (!cross) fail(OCWG_INVALID_INPUT, "qep_target: null cross statistics");
     }
-    // stats.gram_matrix(): fp64 -> fp32 (stats.cpp:7)
-    std::vector<float> hf(n * n);
-    for (uint64_t i = 0; i < n * n; ++i) hf[i] = float(gram[i]);
-    const int r = ocwg_gptq_quantize(ctx, w, hf.data(), n, m, cfg, opts, mode, codes, scales, zeros,
-                                     w_hat);
-    if (r != OCWG_OK) fail(r, g_err);
+    const bool corr = qep && qep->alpha != 0.0 && n > 0;
+    if (method == 1)
+      check_gptq_args(cfg, opts, n, m);
+    else
+      validate(cfg);
+    if (n == 0 || m == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    cudaStream_t st = ctx->stream;
+    const uint64_t ng = group_count(cfg, n, m);
+    const QCfg c = qcfg(cfg, m);
+    Arena ar(ctx);
+    size_t o[11];
+    if (method == 1) gptq_reserve(ar, ctx, n, m, o);
+    const size_t ow = ar.reserve(n * m * 4), og = ar.reserve(n * n * 8),
+                 oc = ar.reserve(corr ? n * n * 8 : 8), oh = ar.reserve(method == 1 ? n * n * 4 : 4),
+                 ot = ar.reserve(corr ? n * m * 4 : 4),
+                 oqf = ar.reserve(corr ? cholesky_flag_ints((long long)n) * sizeof(int) : 4),
+                 oqw = ar.reserve(corr ? qep_workspace_doubles((long long)n, (long long)m) * 8 : 8),
+                 ocd = ar.reserve(n * m * 2), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4),
+                 owh = ar.reserve(w_hat ? n * m * 4 : 4), om = ar.reserve(4096 * 4);
+    ar.commit();
+    float* wd = ar.at<float>(ow);
+    h2d(wd, w, n * m * 4, ctx);
+    if (corr || method == 1) h2d(ar.at<double>(og), gram, n * n * 8, ctx);
+    const float* target = wd;
+    if (corr) {  // W* = W + alpha (gram + lambda I)^-1 (cross W)   (layerwise.cpp:103-111)
+      h2d(ar.at<double>(oc), cross, n * n * 8, ctx);
+      set_tc_workspace(nullptr, 0);
+      qep_target_f64(wd, ar.at<double>(og), ar.at<double>(oc), (long long)n, (long long)m,
+                     qep->alpha, qep->eta, ar.at<float>(ot), ar.at<double>(oqw), ar.at<int>(oqf),
+                     ctx->flag, st);
+      try {
+        finish(ctx);
+      } catch (const Error& e) {
+        if (e.code == OCWG_NUMERIC_ERROR)
+          fail(OCWG_NUMERIC_ERROR, "qep_target: regularized Gram matrix is singular");
+        throw;
+      }
+      target = ar.at<float>(ot);
+    }
+    int16_t* cd = ar.at<int16_t>(ocd);
+    float* sd = ar.at<float>(os);
+    int32_t* zd = ar.at<int32_t>(oz);
+    float* whd = w_hat ? ar.at<float>(owh) : nullptr;
+    if (method == 0) {  // RTN quantize_matrix (quant.cpp:198-210)
+      launch_calibrate_grids(target, (long long)n, (long long)m, (long long)m, c, mode, sd, zd,
+                             ctx->flag, ar.at<float>(om), st);
+      launch_quantize_rtn(target, (long long)n, (long long)m, (long long)m, c, sd, zd, cd, whd, st);
+    } else {  // gptq_quantize(target, stats.gram_matrix(), ...): fp64 -> fp32 H (stats.cpp:7)
+      float* hd = ar.at<float>(oh);
+      launch_f64_to_f32(ar.at<double>(og), (long long)(n * n), hd, st);
+      run_gptq(ctx, target, m, hd, n, m, cfg, opts, mode, cd, sd, zd, whd, gptq_bufs(ar, ctx, o, n, m),
+               ar.at<float>(om));
+    }
+    finish(ctx);
+    d2h(codes, cd, n * m * 2, ctx);
+    d2h(scales, sd, ng * 4, ctx);
+    d2h(zeros, zd, ng * 4, ctx);
+    if (w_hat) d2h(w_hat, whd, n * m * 4, ctx);
+    ck(cudaStreamSynchronize(st), "sync");
   });
 }
 
@@ -1023,22 +1173,15 @@ int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, 
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const size_t oh = ar.reserve(n * n * 4);
-    const size_t hws = hessian_tc_workspace_bytes((long long)tokens, (long long)n);
-    const size_t ohw = ar.reserve(hws);
+    const size_t hws = gram_tc_workspace_bytes((long long)n);
+    const size_t ohw = ar.reserve(hws), opad = ar.reserve(hessian_pad_bytes(tokens, n));
     const size_t oc = ar.reserve(n * m * 2), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4);
     ar.commit();
     float* h = h_out ? h_out : ar.at<float>(oh);
     int16_t* cd = codes ? codes : ar.at<int16_t>(oc);
     float* sd = scales ? scales : ar.at<float>(os);
     int32_t* zd = zeros ? zeros : ar.at<int32_t>(oz);
-    if (tokens == 0) {
-      ck(cudaMemsetAsync(h, 0, n * n * 4, ctx->stream), "memset");
-    } else {
-      const int r = hessian_tc(x, (long long)tokens, (long long)n, h, 0, ar.at<void>(ohw), hws,
-                               ctx->stream);
-      if (r == -1) hessian_simt(x, (long long)tokens, (long long)n, h, 0, ctx->stream);
-      else if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
-    }
+    run_hessian(x, tokens, n, h, false, ar.at<void>(ohw), hws, ar.at<uint16_t>(opad), ctx->stream);
     run_gptq(ctx, w, m, h, n, m, cfg, opts, mode, cd, sd, zd, w_hat, gptq_bufs(ar, ctx, o, n, m),
              ar.at<float>(om));
     if (payload) launch_pack(cd, (long long)(n * m), (long long)ng, qcfg(cfg, m), sd, zd, payload,
@@ -1098,9 +1241,9 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const long long chunk = 32768;  // tokens per H2D chunk (a multiple of the 16384 split)
-    const size_t hws = hessian_tc_workspace_bytes(std::min<long long>(chunk, (long long)tokens),
-                                                  (long long)n);
-    const size_t ohw = ar.reserve(hws);
+    const size_t hws = gram_tc_workspace_bytes((long long)n);
+    const size_t ohw = ar.reserve(hws),
+                 opad = ar.reserve(hessian_pad_bytes(std::min<uint64_t>(chunk, tokens), n));
     ar.commit();
     // ---- pipeline: W and X chunks on the copy stream, H chunk by chunk on st
     const long long nchunks = tokens ? ((long long)tokens + chunk - 1) / chunk : 0;
@@ -1119,10 +1262,8 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
          "H2D(X)");
       ck(cudaEventRecord(ctx->cev[2 + k], ctx->cpy), "event");
       ck(cudaStreamWaitEvent(st, ctx->cev[2 + k], 0), "event");
-      const int r = hessian_tc(xd + t0 * n, tc, (long long)n, hd, k > 0 ? 1 : 0, ar.at<void>(ohw),
-                               hws, st);
-      if (r == -1) hessian_simt(xd + t0 * n, tc, (long long)n, hd, k > 0 ? 1 : 0, st);
-      else if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
+      run_hessian(xd + t0 * n, uint64_t(tc), n, hd, k > 0, ar.at<void>(ohw), hws,
+                  ar.at<uint16_t>(opad), st);
     }
     // W goes over PCIe after X: it is needed only by the grids and the sweep, so
     // its copy overlaps the factorisation instead of delaying the first X chunk
@@ -1192,9 +1333,9 @@ int ocwg_quantize_layers_x(ocwg_ctx* ctx, int count, const float* const* w, cons
     gptq_reserve(ar, ctx, n, mmax, o);
     const size_t om = ar.reserve(4096 * 4);
     const long long chunk = 32768;
-    const size_t hws = hessian_tc_workspace_bytes(std::min<long long>(chunk, (long long)tokens),
-                                                  (long long)n);
-    const size_t ohw = ar.reserve(hws);
+    const size_t hws = gram_tc_workspace_bytes((long long)n);
+    const size_t ohw = ar.reserve(hws),
+                 opad = ar.reserve(hessian_pad_bytes(std::min<uint64_t>(chunk, tokens), n));
     ar.commit();
     const GptqBufs b = gptq_bufs(ar, ctx, o, n, mmax);
     // ---- H = X^T X, X streamed chunk by chunk under the Hessian (as quantize_layer_x)
@@ -1214,10 +1355,8 @@ int ocwg_quantize_layers_x(ocwg_ctx* ctx, int count, const float* const* w, cons
          "H2D(X)");
       ck(cudaEventRecord(ctx->cev[2 + k], ctx->cpy), "event");
       ck(cudaStreamWaitEvent(st, ctx->cev[2 + k], 0), "event");
-      const int r = hessian_tc(xd + t0 * n, tc, (long long)n, hd, k > 0 ? 1 : 0, ar.at<void>(ohw),
-                               hws, st);
-      if (r == -1) hessian_simt(xd + t0 * n, tc, (long long)n, hd, k > 0 ? 1 : 0, st);
-      else if (r != 0) fail(OCWG_CUDA_ERROR, "hessian_tc launch failed");
+      run_hessian(xd + t0 * n, uint64_t(tc), n, hd, k > 0, ar.at<void>(ohw), hws,
+                  ar.at<uint16_t>(opad), st);
     }
     // ---- one order + factorisation for every layer
     run_factor(ctx, hd, n, opts->actorder, opts->percdamp, b);

@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
 
   unsigned smid;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-  int* owner_sm = counter + 32;  // (zeroed with the flags)
+  int* owner_sm = counter + nt;  // panel ci's owner slot (counters: nt item counters, then nt owner slots)
   if (blockIdx.x == 0) {
     if (tid == 0) st_release(owner_sm, int(smid) + 1);
     // ================= owner: the critical path diag(c) -> sub(c+1, c) -> diag(c+1)
@@ -1103,15 +1103,7 @@ inline int blocks_for(long long n) {
   return int(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
 }
 
-int num_sms_f() {
-  static int v = [] {
-    int dev = 0, s = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-    return s;
-  }();
-  return v;
-}
+int num_sms_f() { return device_sms(); }
 
 // Micro-benchmark (debug): one CTA factors a well-conditioned 64 x 64 tile
 // `iters` times; cycles[0] = total clocks, cycles[1] = clocks of the last
@@ -1152,7 +1144,8 @@ void debug_factor_bench(int iters, long long* cycles, float* out, cudaStream_t s
 
 size_t cholesky_flag_ints(long long n) {
   const long long nt = (n + TB - 1) / TB;
-  return size_t(nt * nt + 2 * nt + 64);  // tile flags, partial flags, launch counters
+  // tile flags, partial flags, per-panel item counters + owner slots (<= nt panels)
+  return size_t(nt * nt + 2 * nt + 2 * nt + 8);
 }
 
 template <typename T>
@@ -1162,12 +1155,8 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
   damp_kernel<<<1, 1024, 0, st>>>(h, n, percdamp, damp);
   const size_t row_bytes = size_t(n) * sizeof(float);
   if (row_bytes <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(build_input_rows_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           200 * 1024);
-      attr = true;
-    }
+    cudaFuncSetAttribute(build_input_rows_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     build_input_rows_kernel<T><<<unsigned(n), 256, row_bytes, st>>>(h, n, order, damp, a);
   } else {
     build_input_kernel<T><<<blocks_for(n * n), 256, 0, st>>>(h, n, order, damp, a);
@@ -1177,12 +1166,8 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
 template <typename T>
 void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, float* gtt, int* flags,
                 unsigned* status, long long macro_cols, cudaStream_t st) {
-  static const bool attr = [] {
-    cudaFuncSetAttribute(chol_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(CholSmem<T>)));
-    return true;
-  }();
-  (void)attr;
+  cudaFuncSetAttribute(chol_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(CholSmem<T>)));  // (per device: set on every call)
   const int nt = int((n + TB - 1) / TB);
   int* pflags = flags + (long long)nt * nt;
   int* counters = pflags + 2LL * nt;

@@ -11,6 +11,9 @@
 
 namespace ocwg {
 
+// SM count of the CURRENT device (cached per device ordinal).
+int device_sms();
+
 // Kernel launches issued by this library (for the bench's gpu_launches claim).
 void count_launches(unsigned long long n);
 unsigned long long launches_issued();
@@ -136,26 +139,49 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
                   float* w_hat, long long ldo, T* acc, T* const dpl[2], float* const dhi[2],
                   float* const dlo[2], cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev);
 
-// ---- statistics (stats.cu, hessian_tc.cu) -------------------------------
-// fp64 accumulate_stats for fp32 inputs (stats.cpp:10-19): gram += Xp^T Xp,
-// cross += Xp^T (Xf - Xp).  diff_ws: rows*dim doubles.
-void accumulate_stats_f64(const float* x_fp, const float* x_pert, long long rows, long long dim,
-                          double* gram, double* cross, double* diff_ws, cudaStream_t st);
-// bf16 X (tokens x dim, row-major) -> H (dim x dim fp32, symmetric, full).
-// accumulate: H += X^T X else H = X^T X.  tcgen05/TMEM/TMA kernel.
+// ---- statistics (gram_tc.cu, stats.cu) ------------------------------------
+// Tensor-core statistics: gram (+)= sum_s ops[gA[s]]^T ops[gB[s]] (symmetric
+// operand set; upper tiles computed, mirrored) and cross (+)= sum_s
+// ops[cA[s]]^T ops[cB[s]] (full).  Operands: tokens x dim bf16, row stride ld
+// (ld % 8 == 0, >= dim).  Outputs dim x dim row-major, fp32 or (f64) fp64.
+struct GramSpec {
+  long long tokens = 0, dim = 0, ld = 0;
+  const uint16_t* ops[4] = {};
+  int nops = 0;
+  int gseg = 0, gA[3] = {}, gB[3] = {};
+  int cseg = 0, cA[3] = {}, cB[3] = {};
+  void* gram = nullptr;
+  void* cross = nullptr;
+  bool f64 = false, accumulate = false;
+  long long window_tokens = 0;  // max tokens per TMEM accumulation (0: 16384)
+};
+size_t gram_tc_workspace_bytes(long long dim);
+// 0 ok, -1 unsupported shape, -2 workspace too small, > 0 CUDA error
+int gram_tc(const GramSpec& s, void* ws, size_t ws_bytes, cudaStream_t st);
+// bf16 X (tokens x dim, row-major, dim % 8 == 0) -> H (dim x dim fp32,
+// symmetric, full); accumulate: H += X^T X else H = X^T X.
 size_t hessian_tc_workspace_bytes(long long tokens, long long dim);
-// CTA-pair variant (hessian_tc2.cu), used by hessian_tc unless OCWG_HESSIAN_2CTA=0
-size_t hessian_tc2_workspace_bytes(long long tokens, long long dim);
-int hessian_tc2(const uint16_t* x, long long tokens, long long dim, float* h, int accumulate,
-                void* ws, size_t ws_bytes, cudaStream_t st);
 int hessian_tc(const uint16_t* x, long long tokens, long long dim, float* h, int accumulate,
                void* ws, size_t ws_bytes, cudaStream_t st);
-// SIMT cross-check kernel (same contract), used by tests to validate hessian_tc.
+// SIMT cross-check kernel (same contract as hessian_tc), used by tests only.
 void hessian_simt(const uint16_t* x, long long tokens, long long dim, float* h, int accumulate,
                   cudaStream_t st);
-// fp32 -> bf16 (RNE) conversion, and "all values bf16-exact" check
-void launch_f32_to_bf16(const float* x, long long n, uint16_t* out, unsigned* inexact,
-                        cudaStream_t st);
+// bf16 rows (rows x dim) -> rows x ld with zero pad columns (TMA needs ld % 8 == 0)
+void launch_pad_bf16(const uint16_t* x, long long rows, long long dim, long long ld, uint16_t* out,
+                     cudaStream_t st);
+// fp32 -> bf16 parts for the tensor-core statistics (rows x ld, pad columns 0):
+//   p1 = bf16(xp), p2 = bf16(xp - p1);  (xf != null) d = fp64(xf) - fp64(xp),
+//   d1 = bf16(d), d2 = bf16(d - d1).  *flags |= 1 when some p2 != 0 (xp not
+//   bf16-exact), 2 when some d != 0.
+void launch_split_bf16(const float* xp, const float* xf, long long rows, long long dim, long long ld,
+                       uint16_t* p1, uint16_t* p2, uint16_t* d1, uint16_t* d2, unsigned* flags,
+                       cudaStream_t st);
+// fp64 accumulate_stats for fp32 inputs on the FP64 pipe (OCWG_FP64 precision):
+// gram += Xp^T Xp, cross += Xp^T (Xf - Xp).  diff_ws: rows*dim doubles.
+void accumulate_stats_f64(const float* x_fp, const float* x_pert, long long rows, long long dim,
+                          double* gram, double* cross, double* diff_ws, cudaStream_t st);
+// out[i] += in[i] (fp32 -> fp64), n elements
+void launch_add_f32_to_f64(const float* in, long long n, double* out, cudaStream_t st);
 
 // ---- QEP target correction (qep.cu), fp64 -----------------------------------
 size_t qep_workspace_doubles(long long n, long long m);

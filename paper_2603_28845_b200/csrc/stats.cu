@@ -1,9 +1,14 @@
-// Calibration statistics for the general (fp32-input) API, plus small
-// conversion / metric kernels.
-//   accumulate_stats_f64: stats.cpp:10-19 in fp64 (gram += Xp^T Xp,
-//                         cross += Xp^T (X - Xp)), on the FP64 pipe.
-//   hessian_simt:         fp64-accumulated X^T X of bf16 X, a test-only
-//                         cross-check for the tcgen05 kernel (hessian_tc.cu).
+// Operand preparation for the tensor-core statistics (gram_tc.cu), plus
+// small conversion / metric kernels.
+//   split_bf16:   fp32 calibration inputs of the reference API
+//                 (accumulate_stats, stats.cpp:10-19) -> bf16 parts
+//                 X_hat = P1 + P2, X - X_hat = D1 + D2 for gram / cross;
+//   pad_bf16:     bf16 rows to a TMA-legal row stride (multiple of 8);
+//   accumulate_stats_f64: stats.cpp:10-19 in fp64 SIMT GEMMs (OCWG_FP64);
+//   hessian_simt: fp64-accumulated X^T X of bf16 X, a test-only cross-check
+//                 for the tcgen05 kernel.
+#include <cuda_bf16.h>
+
 #include "kernels.h"
 
 namespace ocwg {
@@ -53,18 +58,56 @@ __global__ void hessian_simt_kernel(const uint16_t* __restrict__ x, long long t,
   }
 }
 
-__global__ void f32_to_bf16_kernel(const float* __restrict__ x, long long n, uint16_t* out,
-                                   unsigned* inexact) {
-  bool bad = false;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+__device__ __forceinline__ uint16_t bf16_bits(float v) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+__device__ __forceinline__ float bf16_val(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
+
+__global__ void split_bf16_kernel(const float* __restrict__ xp, const float* __restrict__ xf,
+                                  long long rows, long long dim, long long ld, uint16_t* __restrict__ p1,
+                                  uint16_t* __restrict__ p2, uint16_t* __restrict__ d1,
+                                  uint16_t* __restrict__ d2, unsigned* flags) {
+  bool inexact = false, dnz = false;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < rows * ld;
        e += (long long)gridDim.x * blockDim.x) {
-    const uint32_t u = __float_as_uint(x[e]);
-    const uint32_t lsb = (u >> 16) & 1u;
-    const uint32_t r = u + 0x7fffu + lsb;  // RNE (finite inputs)
-    out[e] = uint16_t(r >> 16);
-    bad |= (u & 0xffffu) != 0 || !isfinite(x[e]);
+    const long long r = e / ld, c = e % ld;
+    uint16_t a = 0, b = 0, u = 0, v = 0;
+    if (c < dim) {
+      const float x = xp[r * dim + c];
+      a = bf16_bits(x);
+      b = bf16_bits(__fsub_rn(x, bf16_val(a)));  // exact: x - bf16(x) fits fp32
+      inexact |= b != 0;
+      if (xf) {
+        const double d = double(xf[r * dim + c]) - double(x);
+        u = bf16_bits(float(d));
+        v = bf16_bits(float(d - double(bf16_val(u))));
+        dnz |= d != 0.0;
+      }
+    }
+    p1[e] = a;
+    p2[e] = b;
+    if (xf) {
+      d1[e] = u;
+      d2[e] = v;
+    }
   }
-  if (inexact && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(inexact, 1u);
+  const unsigned f = (__any_sync(0xffffffffu, inexact) ? 1u : 0u) | (__any_sync(0xffffffffu, dnz) ? 2u : 0u);
+  if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+}
+
+__global__ void pad_bf16_kernel(const uint16_t* __restrict__ x, long long rows, long long dim,
+                                long long ld, uint16_t* __restrict__ out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < rows * ld;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / ld, c = e % ld;
+    out[e] = c < dim ? x[r * dim + c] : uint16_t(0);
+  }
+}
+
+__global__ void add_f32_to_f64_kernel(const float* __restrict__ in, long long n, double* out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] += double(in[e]);
 }
 
 __global__ void f64_to_f32_kernel(const double* __restrict__ in, long long n, float* out) {
@@ -103,15 +146,16 @@ __global__ void dot_kernel(const double* __restrict__ a, const double* __restric
 
 }  // namespace
 
+// OCWG_FP64 precision: the reference's arithmetic class (fp64 SIMT GEMMs)
 void accumulate_stats_f64(const float* x_fp, const float* x_pert, long long rows, long long dim,
                           double* gram, double* cross, double* diff_ws, cudaStream_t st) {
-  gemm<double, float, float>(dim, dim, rows, 1.0, x_pert, dim, true, x_pert, dim, false, 1.0, gram, dim,
-                      false, st);
+  gemm<double, float, float>(dim, dim, rows, 1.0, x_pert, dim, true, x_pert, dim, false, 1.0, gram,
+                             dim, false, st);
   if (cross) {
     count_launches(1);
     diff_kernel<<<blocks_for(rows * dim), 256, 0, st>>>(x_fp, x_pert, rows * dim, diff_ws);
-    gemm<double, float, double>(dim, dim, rows, 1.0, x_pert, dim, true, diff_ws, dim, false, 1.0, cross,
-                         dim, false, st);
+    gemm<double, float, double>(dim, dim, rows, 1.0, x_pert, dim, true, diff_ws, dim, false, 1.0,
+                                cross, dim, false, st);
   }
 }
 
@@ -122,10 +166,21 @@ void hessian_simt(const uint16_t* x, long long tokens, long long dim, float* h, 
   hessian_simt_kernel<<<grid, 256, 0, st>>>(x, tokens, dim, h, accumulate);
 }
 
-void launch_f32_to_bf16(const float* x, long long n, uint16_t* out, unsigned* inexact,
-                        cudaStream_t st) {
+void launch_split_bf16(const float* xp, const float* xf, long long rows, long long dim, long long ld,
+                       uint16_t* p1, uint16_t* p2, uint16_t* d1, uint16_t* d2, unsigned* flags,
+                       cudaStream_t st) {
   count_launches(1);
-  f32_to_bf16_kernel<<<blocks_for(n), 256, 0, st>>>(x, n, out, inexact);
+  split_bf16_kernel<<<blocks_for(rows * ld), 256, 0, st>>>(xp, xf, rows, dim, ld, p1, p2, d1, d2,
+                                                           flags);
+}
+void launch_pad_bf16(const uint16_t* x, long long rows, long long dim, long long ld, uint16_t* out,
+                     cudaStream_t st) {
+  count_launches(1);
+  pad_bf16_kernel<<<blocks_for(rows * ld), 256, 0, st>>>(x, rows, dim, ld, out);
+}
+void launch_add_f32_to_f64(const float* in, long long n, double* out, cudaStream_t st) {
+  count_launches(1);
+  add_f32_to_f64_kernel<<<blocks_for(n), 256, 0, st>>>(in, n, out);
 }
 void launch_f64_to_f32(const double* in, long long n, float* out, cudaStream_t st) {
   count_launches(1);

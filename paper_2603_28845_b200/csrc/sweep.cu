@@ -649,12 +649,9 @@ void launch_inblock4(const float* w, long long ldw, const int32_t* order, const 
                      const int32_t* zeros, long long n, long long m, long long ib, int bsz,
                      int16_t* codes, float* w_hat, long long ldo, long long ldd, int trace,
                      bool pdl, cudaStream_t st) {
-  static const bool attr = [] {
-    cudaFuncSetAttribute(l4::inblock4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(l4::Smem)));
-    return true;
-  }();
-  (void)attr;
+  // function attributes are per device: set on every launch (cheap)
+  cudaFuncSetAttribute(l4::inblock4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(l4::Smem)));
   // OCWG_SWEEP_EXACT_DIV=1 (tests): the IEEE-division chain even with safe scales
   const char* ex = std::getenv("OCWG_SWEEP_EXACT_DIV");
   trace = (trace ? 1 : 0) | (ex && std::atoi(ex) ? 2 : 0);
@@ -681,12 +678,8 @@ void launch_inblock(const float* w, long long ldw, const int32_t* order, const T
                     const QCfg& c, const float* scales, const int32_t* zeros, long long n,
                     long long m, long long ib, int bsz, int16_t* codes, float* w_hat, long long ldo,
                     long long ldd, cudaStream_t st) {
-  static const bool attr = [] {
-    cudaFuncSetAttribute(inblock_g_kernel<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(InblockSmem<T>)));
-    return true;
-  }();
-  (void)attr;
+  cudaFuncSetAttribute(inblock_g_kernel<T, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(InblockSmem<T>)));
   const unsigned ctas = unsigned((m + kCols - 1) / kCols);
   count_launches(1);
   inblock_g_kernel<T, RPT><<<ctas, 256, sizeof(InblockSmem<T>), st>>>(
@@ -715,9 +708,12 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
                   cudaEvent_t* ev) {
   (void)aux;
   (void)ev;
-  // block size is a pure re-association of the trailing update (SURVEY §0
-  // item 11); blocks above 128 rows run as 128-row blocks.
-  const long long B = block < 1 ? 1 : (block > kB ? kB : block);
+  // Block size is a pure re-association of the trailing update (SURVEY §0
+  // item 11): the fp32 path always runs the tuned 128-row kernel (so the
+  // reference default block_cols = 32, layerwise.hpp:14, is fast too); the
+  // fp64 path honours block_cols (blocks above 128 rows run as 128-row blocks).
+  const bool fast128 = sizeof(T) == 4 && gtt != nullptr;
+  const long long B = fast128 ? kB : (block < 1 ? 1 : (block > kB ? kB : block));
   static const long long super_rows = [] {  // tuning switch: OCWG_SWEEP_SUPER=128..512
     const char* e = getenv("OCWG_SWEEP_SUPER");
     const long long v = e ? atoll(e) : kSuperRows;
@@ -726,7 +722,6 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
   const long long SB = std::max<long long>(1, super_rows / B);  // blocks per super-block
   const long long SBK = SB * B;
   const bool split = glo != nullptr;
-  // debug timing switch (results invalid): OCWG_SWEEP_SKIP=inblock|gemm
   static const long long trace_ib = [] {
     const char* e = getenv("OCWG_SWEEP_TRACE_IB");
     return e ? atoll(e) : -1LL;
@@ -736,10 +731,6 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
   static const bool pdl_on = [] {
     const char* e = getenv("OCWG_SWEEP_PDL");
     return !(e && e[0] == '0');
-  }();
-  static const int skip = [] {
-    const char* e = getenv("OCWG_SWEEP_SKIP");
-    return !e ? 0 : (e[0] == 'i' ? 1 : (e[0] == 'g' ? 2 : 0));
   }();
   for (long long s0 = 0, si = 0; s0 < n; s0 += SBK, ++si) {
     const long long se = std::min(n, s0 + SBK);
@@ -751,15 +742,13 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
       T* dcur = dpl[p] + bprev;
       float* dch = split ? dhi[p] + bprev : nullptr;
       float* dcl = split ? dlo[p] + bprev : nullptr;
-      if (skip == 1)
-        ;
-      else if (B <= 32)
+      if (B <= 32)
         launch_inblock<T, 4>(w, ldw, order, acc, use_acc, gpl, dpl[p], bprev, dcur, dch, dcl, c,
                              scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, kSuperRows, st);
       else if (B <= 64)
         launch_inblock<T, 8>(w, ldw, order, acc, use_acc, gpl, dpl[p], bprev, dcur, dch, dcl, c,
                              scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, kSuperRows, st);
-      else if (sizeof(T) == 4 && gtt && B == kB)
+      else if (fast128)
         launch_inblock4(w, ldw, order, reinterpret_cast<const float*>(acc), use_acc,
                         reinterpret_cast<const float*>(gpl), gtt,
                         reinterpret_cast<const float*>(dpl[p]), bprev,
@@ -770,7 +759,7 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
                               scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, kSuperRows, st);
     }
     // trailing update of this super-block: acc[se:, :] (+)= G[se:, s0:se] D[s0:se, :]
-    if (se < n && skip != 2) {
+    if (se < n) {
       const double beta = si == 0 ? 0.0 : 1.0;
       const long long kk = se - s0;
       bool done = false;

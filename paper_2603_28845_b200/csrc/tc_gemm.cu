@@ -384,24 +384,12 @@ bool make_map(CUtensorMap* map, const float* base, long long rows, long long col
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int num_sms_tc() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
+int num_sms_tc() { return device_sms(); }
 
 inline long long pad4(long long x) { return (x + 3) & ~3LL; }
 
-void ensure_attr() {
-  static const bool attr = [] {
-    cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    return true;
-  }();
-  (void)attr;
+void ensure_attr() {  // function attributes are per device: set on every call
+  cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
 }
 
 }  // namespace

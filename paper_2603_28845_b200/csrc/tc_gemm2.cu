@@ -333,15 +333,7 @@ bool kmap(CUtensorMap* map, const float* base, long long rows, long long cols, l
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int num_sms3() {
-  static int v = [] {
-    int dev = 0, s = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-    return s;
-  }();
-  return v;
-}
+int num_sms3() { return device_sms(); }
 
 }  // namespace
 
@@ -358,11 +350,7 @@ bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const
   if (!kmap(&mah, a_hi, m, k, lda) || !kmap(&mal, a_lo, m, k, lda) || !kmap(&mbh, b_hi, n, k, ldb) ||
       !kmap(&mbl, b_lo, n, k, ldb))
     return false;
-  static const bool attr = [] {
-    cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    return true;
-  }();
-  (void)attr;
+  cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   const int tiles_m = int((m + 255) / 256), tiles_n = int((n + 255) / 256);
   const int ntiles = tiles_m * tiles_n;
   const int npairs = std::min(ntiles, num_sms3() / 2);

@@ -57,18 +57,16 @@ def hessian(x_bf16: torch.Tensor, h: torch.Tensor, accumulate: bool = False) -> 
 
 
 def gptq(w: torch.Tensor, h: torch.Tensor, cfg: QuantConfig, opts: GptqOptions, out: LayerBuffers,
-         mode: ScaleMode = ScaleMode.minmax, col0: int = 0, ncols: int | None = None) -> None:
-    """GPTQ on (a group-aligned column slab of) a device-resident W."""
+         mode: ScaleMode = ScaleMode.minmax) -> None:
+    """GPTQ of a device-resident W (N x M, contiguous) into `out` (N x M)."""
     n, m = w.shape
-    ncols = m - col0 if ncols is None else ncols
+    if not w.is_contiguous() or tuple(out.codes.shape) != (n, m):
+        raise ValueError("gptq: W must be contiguous and match the output buffers")
     ctx = _bind_stream(w.device.index)
     c, o = cfg._c(), opts._c()
-    esz = 4
-    w_ptr = C.c_void_p(w.data_ptr() + col0 * esz)
-    codes_ptr = C.c_void_p(out.codes.data_ptr() + col0 * 2)
-    wh_ptr = None if out.w_hat is None else C.c_void_p(out.w_hat.data_ptr() + col0 * 4)
-    _check(lib().ocwg_gptq_quantize_dev(ctx.handle, w_ptr, m, _p(h), n, ncols, C.byref(c), C.byref(o),
-                                        int(mode), codes_ptr, _p(out.scales), _p(out.zeros), wh_ptr))
+    _check(lib().ocwg_gptq_quantize_dev(ctx.handle, _p(w), m, _p(h), n, m, C.byref(c), C.byref(o),
+                                        int(mode), _p(out.codes), _p(out.scales), _p(out.zeros),
+                                        _p(out.w_hat)))
 
 
 def pack(out: LayerBuffers, cfg: QuantConfig) -> None:

@@ -83,6 +83,18 @@ def test_parse_structure_and_errors(orc):
     bad = ct.Record("x", "uniform-quant", (4, 4), recs[0].params, b"\x00")
     with pytest.raises(g.IoError):
         ct.serialize_ocw([bad])
+    # payload longer than the tensors account for (container.cpp:411)
+    with pytest.raises(g.IoError, match="payload length"):
+        ct.deserialize_ocw(data + b"\x00", decode=False)
+    # offsets not ascending-and-packed (container.cpp:404): swap two entries' offsets
+    import struct
+    hlen = struct.unpack("<Q", data[4:12])[0]
+    header = json.loads(data[12:12 + hlen])
+    t = header["tensors"]
+    t[0]["offset"], t[1]["offset"] = t[1]["offset"], t[0]["offset"]
+    h2 = json.dumps(header, separators=(",", ":"), sort_keys=True).encode()
+    with pytest.raises(g.IoError, match="ascending and packed"):
+        ct.deserialize_ocw(b"OCW1" + struct.pack("<Q", len(h2)) + h2 + data[12 + hlen:], decode=False)
 
 
 @pytest.mark.gpu
