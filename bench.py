@@ -194,6 +194,74 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------- C4 model sweep
+def run_model_mode(args):
+    """BASELINE.json configs[3]: the whole 7B-shaped model (32 blocks x 7
+    linears, W4 g128, act-order, 262144 tokens per tap), the 128 distinct-input
+    units spread over the ranks by LPT; each step is one full sweep (synthetic
+    X and W generated on the device, then Hessian / factor / sweeps / pack);
+    wall-clock = max over ranks of the device time of the step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_28845_b200 import dev
+    from paper_2603_28845_b200 import model_sweep as MS
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    units = MS.model_units(args.blocks)
+    plan = MS.lpt(units, world)
+    mine = plan[rank]
+    for _ in range(args.warmup):  # warm: one unit of each shape
+        seen, warm = set(), []
+        for u in mine:
+            if (u.n, u.linears) not in seen:
+                seen.add((u.n, u.linears))
+                warm.append(u)
+        MS.run_rank(warm, local, keep_payload=False)
+    clocks = ClockSampler(local)
+    l0 = dev.launch_count()
+    walls, stats = [], None
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks.start() if not walls else None
+        payloads, stats = MS.run_rank(mine, local, keep_payload=True)
+        ms = torch.tensor([stats["ms"]], device=device)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        walls.append(float(ms.item()))
+        del payloads
+    ck = clocks.stop()
+    launches = dev.launch_count() - l0
+    total_w = sum(u.n * m for u in units for _, m in u.linears)
+    loads = [sum(MS.unit_cost(u) for u in p) for p in plan]
+    if rank == 0:
+        wall = statistics.mean(walls)
+        line = {
+            "metric": "C4 whole-model sweep throughput (weights/s), 32 x 7 Llama-2-7B linears W4 g128",
+            "value": total_w / (wall / 1e3), "unit": "weights/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall,
+            "wall_clock_s": wall / 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16 (Hessian); fp32 factor/sweep", "data": "synthetic",
+            "config": {"workload": f"C4: {args.blocks} blocks x 7 linears (q/k/v/o 4096x4096, gate/up "
+                                   f"4096x11008, down 11008x4096, reference orientation), "
+                                   f"{TOKENS} tokens per tap, 4 distinct taps per block",
+                       "parallelism": f"{len(units)} units by LPT over {world} ranks",
+                       "lpt_balance": max(loads) / (sum(loads) / world)},
+            "rank0": stats, "gpu_launches": launches, "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -205,9 +273,12 @@ def main():
     ap.add_argument("--cpu-baseline-only", type=int, default=0, metavar="THREADS",
                     help="(internal) run the CPU baseline leg with THREADS threads, print JSON")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--mode", default="layers", choices=["layers", "sharded"],
+    ap.add_argument("--mode", default="layers", choices=["layers", "sharded", "model"],
                     help="N>1: layers = one layer per rank (weak); sharded = one layer split "
-                         "over ranks: token-sharded Hessian + NCCL all-reduce + column slabs (strong)")
+                         "over ranks: token-sharded Hessian + NCCL all-reduce + column slabs + "
+                         "gather to rank 0 (strong); model = BASELINE configs[3] (C4): the whole "
+                         "7B-shaped model sweep, units spread over the ranks by LPT (strong)")
+    ap.add_argument("--blocks", type=int, default=32, help="--mode model: decoder blocks")
     args = ap.parse_args()
     if args.cpu_baseline_only:
         cb = cpu_reference(steps=args.steps, warmup=0, chunk=1024, threads=args.cpu_baseline_only)
@@ -215,6 +286,8 @@ def main():
         return
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.mode == "model":
+        return run_model_mode(args)
 
     import torch
     import torch.distributed as dist
@@ -234,17 +307,14 @@ def main():
     opts = g.GptqOptions(actorder=True, percdamp=0.01, block_cols=128)
     w, x = make_inputs(device, torch)
     sharded = args.mode == "sharded"
-    if sharded:  # this rank's token shard and column slab (paper_2603_28845_b200/dist.py)
+    out = dev.LayerBuffers(N_IN, M_OUT, cfg, local, w_hat=not sharded, payload=not sharded)
+    stream = torch.cuda.current_stream(device)
+    if sharded:  # this rank's token shard; slabs + gather in paper_2603_28845_b200/dist.py
         from paper_2603_28845_b200 import dist as D
         t0, t1 = D.token_range(TOKENS, rank, world)
-        x = x[t0:t1]  # (synthetic: every rank draws the same stream, keeps its shard)
-        j0, j1 = D.column_slabs(M_OUT, GROUP, BITS, world)[rank]
-        w_slab = w[:, j0:j1].contiguous()
-        out = dev.LayerBuffers(N_IN, j1 - j0, cfg, local)
-    else:
-        w_slab = w
-        out = dev.LayerBuffers(N_IN, M_OUT, cfg, local)
-    stream = torch.cuda.current_stream(device)
+        x = x[t0:t1].contiguous()  # (synthetic: every rank draws the same stream, keeps its shard)
+        j0, j1 = D.column_slabs(M_OUT, GROUP, BITS, world)[rank] if world > 1 else (0, M_OUT)
+        ops = D.gpu_ops(local, w_hat=True)
 
     def step(ev=None):
         if ev is not None:
@@ -254,10 +324,16 @@ def main():
             dist.all_reduce(out.h, op=dist.ReduceOp.SUM)  # the one exchange step (NCCL)
         if ev is not None:
             ev[1].record(stream)
-        dev.gptq(w_slab, out.h, cfg, opts, out)
-        if ev is not None:
-            ev[2].record(stream)
-        dev.pack(out, cfg)
+        if sharded:
+            res = ops.gptq_slab(w, j0, j1, out.h, cfg, opts)  # grids + sweep + pack of the slab
+            if ev is not None:
+                ev[2].record(stream)
+            D.gather_slabs(res, N_IN, M_OUT, GROUP, BITS, True)  # to rank 0 + per-row assembly
+        else:
+            dev.gptq(w, out.h, cfg, opts, out)
+            if ev is not None:
+                ev[2].record(stream)
+            dev.pack(out, cfg)
         if ev is not None:
             ev[3].record(stream)
 
@@ -373,7 +449,8 @@ def main():
                    "parallelism": (f"one layer over {world} ranks: token-sharded Hessian + NCCL "
                                    f"all-reduce, {GROUP}-aligned column slabs" if sharded else
                                    f"{world} independent layers" if world > 1 else "single GPU")},
-        "breakdown_ms": {"hessian": t_h, "gptq": t_q, "pack": t_p, "gptq_phases": phases},
+        "breakdown_ms": {"hessian": t_h, "gptq": t_q, ("gather" if sharded else "pack"): t_p,
+                         "gptq_phases": phases},
         "hessian_tflops": achieved,
         "roofline": {"bound": "tensor", "kernel": "gram_tc_kernel<float>", "achieved": achieved,
                      "peak": peak_burst, "unit": "TFLOP/s", "frac": achieved / peak_burst,

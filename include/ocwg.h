@@ -207,6 +207,22 @@ int ocwg_quantize_layers_x(ocwg_ctx* ctx, int count, const float* const* w, cons
                            int scale_mode, int16_t* const* codes, float* const* scales,
                            int32_t* const* zeros, uint8_t* const* payload,
                            const uint64_t* payload_len);
+/* ocwg_quantize_layers_x with every pointer in device memory (w, m and the
+ * output pointer arrays themselves are host arrays of device pointers);
+ * codes / scales / zeros required, payload[i] optional.  Async-capable. */
+int ocwg_quantize_layers_x_dev(ocwg_ctx* ctx, int count, const float* const* w, const uint64_t* m,
+                               const uint16_t* x, uint64_t tokens, uint64_t n,
+                               const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
+                               int scale_mode, int16_t* const* codes, float* const* scales,
+                               int32_t* const* zeros, uint8_t* const* payload);
+/* Seeded synthetic inputs on the device (counter-based
+ * Philox4x32-10 + Box-Muller normals g, independent of launch shape):
+ *   kind 0: out (bf16 bits, rows x cols) = bf16(g * col_scale[c]) (col_scale
+ *           device fp32[cols], NULL = 1) -- calibration X with outlier channels;
+ *   kind 1: out (bf16 bits) = bf16(silu(a) * b) -- down_proj calibration X;
+ *   kind 2: out (fp32) = float(bf16(g * stddev)) -- bf16-valued W. */
+int ocwg_synth_dev(ocwg_ctx* ctx, int kind, uint64_t seed, uint64_t rows, uint64_t cols,
+                   double stddev, const float* col_scale, void* out);
 /* Same with every pointer in device memory (inputs resident in HBM). */
 int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint64_t tokens,
                               uint64_t n, uint64_t m, const ocwg_quant_config* cfg,
@@ -232,6 +248,19 @@ int ocwg_pack_uniform_dev(ocwg_ctx* ctx, const int16_t* codes, const float* scal
 /* impl: 0 = tcgen05 kernel (product), 1 = SIMT fp64-accumulate cross-check */
 int ocwg_debug_hessian_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, uint64_t dim,
                            float* h, int accumulate, int impl);
+/* bf16 parts of fp32 statistics inputs (stats.cu split_bf16), device pointers */
+int ocwg_debug_split_dev(ocwg_ctx* ctx, const float* xp, const float* xf, uint64_t rows,
+                         uint64_t dim, uint64_t ld, uint16_t* p1, uint16_t* p2, uint16_t* d1,
+                         uint16_t* d2, unsigned* flags);
+/* The general tensor-core statistics kernel (gram_tc.cu), device pointers:
+ * gram (+)= sum_s ops[ga[s]]^T ops[gb[s]] (s < gseg; symmetric operand set)
+ * and cross (+)= sum_s ops[ca[s]]^T ops[cb[s]] (s < cseg); ops: tokens x dim
+ * bf16 with row stride ld (% 8 == 0); outputs dim x dim fp32 (f64 = 0) or
+ * fp64; window: tokens per TMEM accumulation (0 = default). */
+int ocwg_debug_gram_dev(ocwg_ctx* ctx, const uint16_t* const* ops, int nops, uint64_t tokens,
+                        uint64_t dim, uint64_t ld, int gseg, const int* ga, const int* gb, int cseg,
+                        const int* ca, const int* cb, void* gram, void* cross, int f64,
+                        int accumulate, int64_t window);
 /* Phase timing of gptq (CUDA events): on != 0 enables recording; phase_ms
  * (may be NULL) receives the last run's [order+damp+permute-H, Cholesky,
  * triangular inverse, grids, sweep] in milliseconds. */

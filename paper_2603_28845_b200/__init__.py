@@ -217,10 +217,16 @@ _SIGS = {
     "ocwg_quantize_layer_x_dev": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, C.POINTER(_QCfg),
                                             C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P, _P, _P]),
     "ocwg_hessian_bf16_dev": (C.c_int, [_P, _P, _U64, _U64, _P, C.c_int]),
+    "ocwg_quantize_layers_x_dev": (C.c_int, [_P, C.c_int, _P, _P, _P, _U64, _U64, C.POINTER(_QCfg),
+                                             C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P]),
+    "ocwg_synth_dev": (C.c_int, [_P, C.c_int, _U64, _U64, _U64, C.c_double, _P, _P]),
     "ocwg_gptq_quantize_dev": (C.c_int, [_P, _P, _U64, _P, _U64, _U64, C.POINTER(_QCfg),
                                          C.POINTER(_GOpt), C.c_int, _P, _P, _P, _P]),
     "ocwg_pack_uniform_dev": (C.c_int, [_P, _P, _P, _P, _U64, _U64, C.POINTER(_QCfg), _P]),
     "ocwg_debug_hessian_dev": (C.c_int, [_P, _P, _U64, _U64, _P, C.c_int, C.c_int]),
+    "ocwg_debug_split_dev": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, _P, _P, _P, _P, _P]),
+    "ocwg_debug_gram_dev": (C.c_int, [_P, _P, C.c_int, _U64, _U64, _U64, C.c_int, _P, _P, C.c_int, _P,
+                                      _P, _P, _P, C.c_int, C.c_int, C.c_int64]),
     "ocwg_launch_count": (_U64, [_P]),
     "ocwg_debug_profile": (C.c_int, [_P, C.c_int, _P]),
     "ocwg_debug_gemm": (C.c_int, [_P, C.c_int, _U64, _U64, _U64, C.c_double, _P, _U64, C.c_int, _P,

@@ -831,6 +831,7 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
       unsigned f = 0;
       d2h(&f, fl, 4, ctx);
       ck(cudaStreamSynchronize(st), "sync");
+      if (getenv("OCWG_DEBUG_STATS")) fprintf(stderr, "accumulate_stats: split flags %u\n", f);
       GramSpec s;
       s.tokens = (long long)rows;
       s.dim = (long long)dim;
@@ -884,6 +885,55 @@ int ocwg_debug_hessian_dev(ocwg_ctx* ctx, const uint16_t* x, uint64_t tokens, ui
       run_hessian(x, tokens, dim, h, accumulate != 0, ar.at<void>(o), gb, ar.at<uint16_t>(op),
                   ctx->stream);
     }
+    finish_dev(ctx);
+  });
+}
+
+int ocwg_debug_split_dev(ocwg_ctx* ctx, const float* xp, const float* xf, uint64_t rows,
+                         uint64_t dim, uint64_t ld, uint16_t* p1, uint16_t* p2, uint16_t* d1,
+                         uint16_t* d2, unsigned* flags) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx, true);
+    launch_split_bf16(xp, xf, (long long)rows, (long long)dim, (long long)ld, p1, p2, d1, d2, flags,
+                      ctx->stream);
+    finish_dev(ctx);
+  });
+}
+
+int ocwg_debug_gram_dev(ocwg_ctx* ctx, const uint16_t* const* ops, int nops, uint64_t tokens,
+                        uint64_t dim, uint64_t ld, int gseg, const int* ga, const int* gb, int cseg,
+                        const int* ca, const int* cb, void* gram, void* cross, int f64,
+                        int accumulate, int64_t window) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx, true);
+    GramSpec s;
+    s.tokens = (long long)tokens;
+    s.dim = (long long)dim;
+    s.ld = (long long)ld;
+    s.nops = nops;
+    for (int k = 0; k < nops && k < 4; ++k) s.ops[k] = ops[k];
+    s.gseg = gseg;
+    s.cseg = cseg;
+    for (int k = 0; k < 3; ++k) {
+      s.gA[k] = k < gseg ? ga[k] : 0;
+      s.gB[k] = k < gseg ? gb[k] : 0;
+      s.cA[k] = k < cseg ? ca[k] : 0;
+      s.cB[k] = k < cseg ? cb[k] : 0;
+    }
+    s.gram = gram;
+    s.cross = cross;
+    s.f64 = f64 != 0;
+    s.accumulate = accumulate != 0;
+    s.window_tokens = window;
+    Arena ar(ctx);
+    const size_t gbytes = gram_tc_workspace_bytes((long long)dim);
+    const size_t o = ar.reserve(gbytes);
+    ar.commit();
+    const int r = gram_tc(s, ar.at<void>(o), gbytes, ctx->stream);
+    if (r == -1) fail(OCWG_INVALID_INPUT, "gram_tc: unsupported shape / segment set");
+    if (r != 0) fail(OCWG_CUDA_ERROR, "gram_tc launch failed");
     finish_dev(ctx);
   });
 }
@@ -1280,6 +1330,66 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
     if (payload) d2h(payload, pd, pb, ctx);
     if (h_out) d2h(h_out, hd, n * n * 4, ctx);
     finish(ctx);
+  });
+}
+
+int ocwg_synth_dev(ocwg_ctx* ctx, int kind, uint64_t seed, uint64_t rows, uint64_t cols,
+                   double stddev, const float* col_scale, void* out) {
+  return guard([&] {
+    if (kind < 0 || kind > 2) fail(OCWG_INVALID_INPUT, "synth: unknown kind");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx, true);
+    if (rows > 0 && cols > 0)
+      launch_synth(kind, (unsigned long long)seed, (long long)rows, (long long)cols, float(stddev),
+                   col_scale, out, 0, ctx->stream);
+    finish_dev(ctx);
+  });
+}
+
+int ocwg_quantize_layers_x_dev(ocwg_ctx* ctx, int count, const float* const* w, const uint64_t* m,
+                               const uint16_t* x, uint64_t tokens, uint64_t n,
+                               const ocwg_quant_config* cfg, const ocwg_gptq_options* opts,
+                               int mode, int16_t* const* codes, float* const* scales,
+                               int32_t* const* zeros, uint8_t* const* payload) {
+  return guard([&] {
+    if (count < 1 || !w || !m) fail(OCWG_INVALID_INPUT, "quantize_layers_x: no layers");
+    uint64_t mmax = 0;
+    for (int i = 0; i < count; ++i) {
+      check_gptq_args(cfg, opts, n, m[i]);
+      if (n == 0 || m[i] == 0) fail(OCWG_INVALID_INPUT, "calibrate_grids: empty matrix");
+      if (!codes || !codes[i] || !scales || !scales[i] || !zeros || !zeros[i])
+        fail(OCWG_INVALID_INPUT, "quantize_layers_x_dev: codes / scales / zeros are required");
+      mmax = std::max(mmax, m[i]);
+    }
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx, true);
+    cudaStream_t st = ctx->stream;
+    Arena ar(ctx);
+    size_t o[11];
+    gptq_reserve(ar, ctx, n, mmax, o);
+    const size_t om = ar.reserve(4096 * 4), oh = ar.reserve(n * n * 4);
+    const size_t hws = gram_tc_workspace_bytes((long long)n);
+    const size_t ohw = ar.reserve(hws), opad = ar.reserve(hessian_pad_bytes(tokens, n));
+    ar.commit();
+    const GptqBufs b = gptq_bufs(ar, ctx, o, n, mmax);
+    float* hd = ar.at<float>(oh);
+    // one Hessian + order + factorisation for every layer that reads X
+    run_hessian(x, tokens, n, hd, false, ar.at<void>(ohw), hws, ar.at<uint16_t>(opad), st);
+    run_factor(ctx, hd, n, opts->actorder, opts->percdamp, b);
+    for (int i = 0; i < count; ++i) {
+      const uint64_t mi = m[i];
+      const QCfg c = qcfg(cfg, mi);
+      launch_calibrate_grids(w[i], (long long)n, (long long)mi, (long long)mi, c, mode, scales[i],
+                             zeros[i], ctx->flag, ar.at<float>(om), st);
+      if (ctx->precision == OCWG_FP64)
+        run_sweep_t<double>(ctx, w[i], mi, n, mi, c, opts, codes[i], scales[i], zeros[i], nullptr, b);
+      else
+        run_sweep_t<float>(ctx, w[i], mi, n, mi, c, opts, codes[i], scales[i], zeros[i], nullptr, b);
+      if (payload && payload[i])
+        launch_pack(codes[i], (long long)(n * mi), (long long)group_count(cfg, n, mi), c, scales[i],
+                    zeros[i], payload[i], st);
+    }
+    finish_dev(ctx);
   });
 }
 

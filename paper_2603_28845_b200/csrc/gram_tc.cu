@@ -186,11 +186,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (u < 0) break;
         const Unit x = decode(p, u);
         const int arow = x.bi * 256 + int(rank) * TM, bcol = x.bj * 256 + int(rank) * TNH;
+        int seg = int(x.kb0 / p.kb_seg);
+        long long kk = x.kb0 - seg * p.kb_seg;  // k-block within the segment
         for (long long kb = x.kb0; kb < x.kb1; ++kb) {
-          const int seg = int(kb / p.kb_seg);
-          const int t0 = int((kb - seg * p.kb_seg) * TK);
+          const int t0 = int(kk * TK);
           const CUtensorMap* ma = &p.maps[p.seg_a[x.kind][seg]];
           const CUtensorMap* mb = &p.maps[p.seg_b[x.kind][seg]];
+          if (++kk == p.kb_seg) {
+            kk = 0;
+            ++seg;
+          }
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
           const uint32_t fb = smem_u32(&full_bar[stage]);
           if (rank == 0) mbar_expect_tx(fb, 2 * STAGE_BYTES);
@@ -275,57 +280,78 @@ __global__ void __launch_bounds__(THREADS, 1)
       const long long row = row_base + q * 32 + lane;
       const bool first = x.split == 0 && !p.accumulate, last = x.split == p.splits - 1;
       const bool vec_ok = (dim & 3) == 0;  // 16-byte aligned rows
-#pragma unroll 1
-      for (int c0 = 0; c0 < 256; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * 256 + c0, r);
-        const long long col0 = (long long)x.bj * 256 + c0;
-        if (gram && col0 + 31 < row_base) continue;  // chunk entirely below the diagonal
-        if (row >= dim) continue;
-        OutT* orow = out + row * dim + col0;
-        float v[32];
+      const long long colt = (long long)x.bj * 256;
+      if constexpr (sizeof(OutT) == 4) {
+        // fp32 output (the hot path's H): the chunk's old values are loaded one
+        // chunk ahead, so their L2 latency overlaps the TMEM load and the adds
+        auto load_old = [&](int c0, float (&o)[32]) {
+          const long long col0 = colt + c0;
+          const float* src = out + row * dim + col0;
+          if (first || row >= dim || (gram && col0 + 31 < row_base)) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
-        const bool full = vec_ok && col0 + 32 <= dim && (!gram || col0 >= row);
-        if (full) {
-          if constexpr (sizeof(OutT) == 4) {
-            if (!first) {
+            for (int e = 0; e < 32; ++e) o[e] = 0.f;
+          } else if (vec_ok && col0 + 32 <= dim) {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const float4 o = __ldcg(reinterpret_cast<const float4*>(orow) + e);
-                v[4 * e] += o.x, v[4 * e + 1] += o.y, v[4 * e + 2] += o.z, v[4 * e + 3] += o.w;
-              }
+            for (int e = 0; e < 8; ++e) {
+              const float4 f = __ldcg(reinterpret_cast<const float4*>(src) + e);
+              o[4 * e] = f.x, o[4 * e + 1] = f.y, o[4 * e + 2] = f.z, o[4 * e + 3] = f.w;
             }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = col0 + e < dim ? __ldcg(src + e) : 0.f;
+          }
+        };
+        float v[32], nv[32];
+        load_old(0, nv);
+#pragma unroll 1
+        for (int c0 = 0; c0 < 256; c0 += 32) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = nv[e];
+          if (c0 + 32 < 256) load_old(c0 + 32, nv);
+          uint32_t r[32];
+          tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * 256 + c0, r);
+          const long long col0 = colt + c0;
+          if (gram && col0 + 31 < row_base) continue;  // chunk entirely below the diagonal
+          if (row >= dim) continue;
+          float* orow = out + row * dim + col0;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] += __uint_as_float(r[e]);
+          if (vec_ok && col0 + 32 <= dim && (!gram || col0 >= row)) {
 #pragma unroll
             for (int e = 0; e < 8; ++e)
               reinterpret_cast<float4*>(orow)[e] =
                   make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
           } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              double2 o = first ? make_double2(0.0, 0.0) : __ldcg(reinterpret_cast<const double2*>(orow) + e);
-              o.x += double(v[2 * e]);
-              o.y += double(v[2 * e + 1]);
-              reinterpret_cast<double2*>(orow)[e] = o;
-            }
+            for (int e = 0; e < 32; ++e)
+              if (col0 + e < dim && (!gram || col0 + e >= row)) orow[e] = v[e];
           }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const long long col = col0 + e;
-            if (col < dim && (!gram || col >= row)) {
-              if constexpr (sizeof(OutT) == 4)
-                orow[e] = first ? v[e] : __ldcg(orow + e) + v[e];
-              else
-                orow[e] = first ? double(v[e]) : __ldcg(orow + e) + double(v[e]);
+          if (gram && last) {  // mirror into the lower triangle (coalesced over lanes)
+#pragma unroll 4
+            for (int e = 0; e < 32; ++e) {
+              const long long col = col0 + e;
+              if (col < dim && col > row) out[col * dim + row] = v[e];
             }
           }
         }
-        if (gram && last) {  // mirror into the lower triangle (coalesced over lanes)
+      } else {
+        // fp64 output (the reference API's CalibStats): plain read-modify-write
+#pragma unroll 1
+        for (int c0 = 0; c0 < 256; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * 256 + c0, r);
+          const long long col0 = colt + c0;
+          if (gram && col0 + 31 < row_base) continue;
+          if (row >= dim) continue;
+          double* orow = out + row * dim + col0;
 #pragma unroll 4
           for (int e = 0; e < 32; ++e) {
             const long long col = col0 + e;
-            if (col < dim && col > row) out[col * dim + row] = orow[e];
+            if (col < dim && (!gram || col >= row)) {
+              const double nvv = (first ? 0.0 : __ldcg(orow + e)) + double(__uint_as_float(r[e]));
+              orow[e] = nvv;
+              if (gram && last && col > row) out[col * dim + row] = nvv;
+            }
           }
         }
       }

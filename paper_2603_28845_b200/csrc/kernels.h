@@ -190,6 +190,12 @@ void qep_target_f64(const float* w, const double* gram, const double* cross, lon
                     long long m, double alpha, double eta, float* out, double* ws, int* flags,
                     unsigned* status, cudaStream_t st);
 
+// ---- seeded synthetic inputs (synth.cu) ------------------------
+// kind 0: bf16(g * col_scale[c]) (col_scale may be null: 1); kind 1: bf16(silu(a) * b);
+// kind 2: fp32 value of bf16(g * stddev).  g: Philox4x32-10 + Box-Muller normals.
+void launch_synth(int kind, unsigned long long seed, long long rows, long long cols, float stddev,
+                  const float* col_scale, void* out, int max_ctas, cudaStream_t st);
+
 // ---- debug micro-benchmarks -------------------------------------------------
 void debug_factor_bench(int iters, long long* cycles, float* out, cudaStream_t st);
 int debug_sweep_trace(unsigned long long* out, int cap);

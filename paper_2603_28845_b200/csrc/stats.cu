@@ -91,7 +91,9 @@ __global__ void split_bf16_kernel(const float* __restrict__ xp, const float* __r
       d2[e] = v;
     }
   }
-  const unsigned f = (__any_sync(0xffffffffu, inexact) ? 1u : 0u) | (__any_sync(0xffffffffu, dnz) ? 2u : 0u);
+  // (an integer OR-reduction: nvcc 12.9 miscompiled the two-__any_sync form
+  // of this epilogue into votes on the negated predicates)
+  const unsigned f = __reduce_or_sync(0xffffffffu, (inexact ? 1u : 0u) | (dnz ? 2u : 0u));
   if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
 }
 

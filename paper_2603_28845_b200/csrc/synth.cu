@@ -1,0 +1,111 @@
+// Seeded synthetic inputs on the device (SURVEY §8(d) generator): the
+// BASELINE configs' calibration activations and weights, so the model-sweep
+// driver (C4) can stream 128 calibration taps of 1-6 GB each through one GPU
+// without host traffic, and the CPU oracle can consume identical bytes (D2H).
+//
+// Counter-based: element e of stream s draws Philox4x32-10 at counter
+// (e / 4, s, 0, 0) with the 64-bit seed as key, and Box-Muller turns the four
+// 32-bit words into four fp32 normals (pairs (0,1), (2,3)).  The value of
+// an element is independent of the grid shape.
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+
+namespace ocwg {
+namespace {
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = c.x * 0xD2511F53u, hi0 = __umulhi(c.x, 0xD2511F53u);
+    const uint32_t lo1 = c.z * 0xCD9E8D57u, hi1 = __umulhi(c.z, 0xCD9E8D57u);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ void normals4(unsigned long long seed, unsigned long long q, uint32_t s,
+                                         float (&z)[4]) {
+  const uint4 r = philox4x32_10(make_uint4(uint32_t(q), uint32_t(q >> 32), s, 0u),
+                                make_uint2(uint32_t(seed), uint32_t(seed >> 32)));
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    // u1 in (0, 1] (log finite), u2 in [0, 1)
+    const float u1 = (float(w[2 * p] >> 8) + 1.0f) * (1.0f / 16777216.0f);
+    const float u2 = float(w[2 * p + 1] >> 8) * (1.0f / 16777216.0f);
+    const float rad = sqrtf(-2.0f * logf(u1));
+    float sn, cs;
+    sincospif(2.0f * u2, &sn, &cs);
+    z[2 * p] = rad * cs;
+    z[2 * p + 1] = rad * sn;
+  }
+}
+
+__device__ __forceinline__ uint16_t bf16_bits(float v) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+__device__ __forceinline__ float bf16_val(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
+
+// kind 0: bf16(g * col_scale[c]); kind 1: bf16(silu(a) * b); kind 2: fp32 value of bf16(g * stddev)
+__global__ void synth_kernel(int kind, unsigned long long seed, long long rows, long long cols,
+                             float stddev, const float* __restrict__ col_scale, void* out) {
+  const long long total = rows * cols;
+  const long long nq = (total + 3) / 4;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (long long)gridDim.x * blockDim.x) {
+    float z[4];
+    normals4(seed, (unsigned long long)q, 0u, z);
+    float v[4];
+    if (kind == 1) {
+      float b[4];
+      normals4(seed, (unsigned long long)q, 1u, b);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = (z[i] / (1.0f + __expf(-z[i]))) * b[i];  // silu(a) * b
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const long long e = 4 * q + i;
+        const float sc = kind == 2 ? stddev : (col_scale ? col_scale[e % cols] : 1.0f);
+        v[i] = z[i] * sc;
+      }
+    }
+    const long long e0 = 4 * q;
+    if (kind == 2) {
+      float* o = static_cast<float*>(out);
+      if (e0 + 4 <= total && (reinterpret_cast<uintptr_t>(o + e0) & 15) == 0) {
+        *reinterpret_cast<float4*>(o + e0) = make_float4(bf16_val(bf16_bits(v[0])), bf16_val(bf16_bits(v[1])),
+                                                         bf16_val(bf16_bits(v[2])), bf16_val(bf16_bits(v[3])));
+      } else {
+        for (int i = 0; i < 4 && e0 + i < total; ++i) o[e0 + i] = bf16_val(bf16_bits(v[i]));
+      }
+    } else {
+      uint16_t* o = static_cast<uint16_t*>(out);
+      if (e0 + 4 <= total && (reinterpret_cast<uintptr_t>(o + e0) & 7) == 0) {
+        uint2 pk;
+        pk.x = uint32_t(bf16_bits(v[0])) | (uint32_t(bf16_bits(v[1])) << 16);
+        pk.y = uint32_t(bf16_bits(v[2])) | (uint32_t(bf16_bits(v[3])) << 16);
+        *reinterpret_cast<uint2*>(o + e0) = pk;
+      } else {
+        for (int i = 0; i < 4 && e0 + i < total; ++i) o[e0 + i] = bf16_bits(v[i]);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void launch_synth(int kind, unsigned long long seed, long long rows, long long cols, float stddev,
+                  const float* col_scale, void* out, int max_ctas, cudaStream_t st) {
+  const long long nq = (rows * cols + 3) / 4;
+  long long g = (nq + 255) / 256;
+  const long long cap = max_ctas > 0 ? max_ctas : (long long)device_sms() * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  count_launches(1);
+  synth_kernel<<<unsigned(g), 256, 0, st>>>(kind, seed, rows, cols, stddev, col_scale, out);
+}
+
+}  // namespace ocwg

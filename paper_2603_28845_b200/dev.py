@@ -33,7 +33,7 @@ class LayerBuffers:
     """Output buffers of one layer quantize, allocated once (N x M)."""
 
     def __init__(self, n: int, m: int, cfg: QuantConfig, device: int, w_hat: bool = True,
-                 payload: bool = True):
+                 payload: bool = True, h: bool = True):
         dev = torch.device("cuda", device)
         ng = quant_group_count(cfg, n, m)
         self.codes = torch.empty((n, m), dtype=torch.int16, device=dev)
@@ -42,7 +42,7 @@ class LayerBuffers:
         self.w_hat = torch.empty((n, m), dtype=torch.float32, device=dev) if w_hat else None
         self.payload_bytes = uniform_storage_bytes(cfg, n, m)
         self.payload = torch.empty(self.payload_bytes, dtype=torch.uint8, device=dev) if payload else None
-        self.h = torch.empty((n, n), dtype=torch.float32, device=dev)
+        self.h = torch.empty((n, n), dtype=torch.float32, device=dev) if h else None
 
 
 def _p(t):
@@ -87,6 +87,37 @@ def quantize_layer_x(w: torch.Tensor, x_bf16: torch.Tensor, cfg: QuantConfig, op
                                            C.byref(c), C.byref(o), int(mode), _p(out.codes),
                                            _p(out.scales), _p(out.zeros), _p(out.w_hat),
                                            _p(out.payload), _p(out.h)))
+
+
+def quantize_layers(ws: list, x_bf16: torch.Tensor, cfg: QuantConfig, opts: GptqOptions,
+                    outs: list, mode: ScaleMode = ScaleMode.minmax) -> None:
+    """Layers sharing one calibration input (q/k/v, gate/up): one Hessian and
+    one factorisation on the device, then grids + sweep + pack per W."""
+    k = len(ws)
+    n = ws[0].shape[0]
+    ctx = _bind_stream(x_bf16.device.index)
+    arr = lambda vals, t: (t * k)(*vals)  # noqa: E731
+    wp = arr([w.data_ptr() for w in ws], C.c_void_p)
+    mp = arr([w.shape[1] for w in ws], C.c_uint64)
+    cp = arr([o.codes.data_ptr() for o in outs], C.c_void_p)
+    sp = arr([o.scales.data_ptr() for o in outs], C.c_void_p)
+    zp = arr([o.zeros.data_ptr() for o in outs], C.c_void_p)
+    pp = arr([o.payload.data_ptr() if o.payload is not None else 0 for o in outs], C.c_void_p)
+    c, o = cfg._c(), opts._c()
+    _check(lib().ocwg_quantize_layers_x_dev(ctx.handle, k, C.cast(wp, C.c_void_p), C.cast(mp, C.c_void_p),
+                                            _p(x_bf16), x_bf16.shape[0], n, C.byref(c), C.byref(o),
+                                            int(mode), C.cast(cp, C.c_void_p), C.cast(sp, C.c_void_p),
+                                            C.cast(zp, C.c_void_p), C.cast(pp, C.c_void_p)))
+
+
+def synth(kind: int, seed: int, out: torch.Tensor, stddev: float = 1.0,
+          col_scale: torch.Tensor | None = None) -> None:
+    """Seeded synthetic inputs on the device (ocwg_synth_dev): kind 0 bf16
+    X = g * col_scale, 1 bf16 X = silu(a) * b, 2 fp32 bf16-valued W = g * stddev."""
+    rows, cols = out.shape
+    ctx = _bind_stream(out.device.index)
+    _check(lib().ocwg_synth_dev(ctx.handle, int(kind), int(seed) & ((1 << 64) - 1), rows, cols,
+                                float(stddev), _p(col_scale), _p(out)))
 
 
 def profile(on: bool, device: int = 0):

@@ -37,19 +37,19 @@ class OracleOps:
         self.orc = orc
 
     def gram(self, x_local):
-        return x_local.astype(np.float64).T @ x_local.astype(np.float64)
-
-    def as_tensor(self, h):
         import torch
-        return torch.from_numpy(h)
+        return torch.from_numpy(x_local.astype(np.float64).T @ x_local.astype(np.float64))
 
     def gptq_slab(self, w, j0, j1, h, cfg, opts):
+        import torch
         orc = self.orc
         hf = h.numpy().astype(np.float32)
         q = orc.gptq_quantize(w[:, j0:j1], hf, cfg, opts)
         wh = orc.dequantize(q)
-        return D.SlabResult(j0, j1, q.codes, q.grids.scale, q.grids.zero, wh,
-                            orc.pack_uniform(q.codes, q.grids, cfg))
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dt))  # noqa: E731
+        payload = torch.frombuffer(bytearray(orc.pack_uniform(q.codes, q.grids, cfg)), dtype=torch.uint8)
+        return D.SlabResult(j0, j1, t(q.codes, np.int16), t(q.grids.scale, np.float32),
+                            t(q.grids.zero, np.int32), t(wh, np.float32), payload)
 
 
 def _problem(orc):
@@ -73,7 +73,11 @@ def _worker(rank, world, port, q):
         t0, t1 = D.token_range(x.shape[0], rank, world)
         out = D.quantize_layer_sharded(w, x[t0:t1], x.shape[0], cfg, opts, ops=OracleOps(orc))
         if rank == 0:
-            q.put(out)
+            codes, scales, zeros, w_hat, payload = out
+            q.put((codes.numpy(), scales.numpy(), zeros.numpy(), w_hat.numpy(),
+                   payload.numpy().tobytes()))
+        else:
+            assert out is None
     finally:
         dist.destroy_process_group()
 
@@ -84,11 +88,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_sharded_layer_matches_single_process(orc):
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_layer_matches_single_process(orc, world):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    world, port = 2, _free_port()
+    port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()

@@ -372,3 +372,72 @@ def test_quantize_layer_x_unaligned_dim(g, ref, orc, n, m, t):
     np.testing.assert_array_equal(q.scales, rs)
     np.testing.assert_array_equal(q.zeros, rz)
     assert len(payload) == g.storage_bytes(q)
+
+
+@pytest.mark.parametrize("t,n,ld,gsegs,csegs,f64,window", [
+    (300, 64, 64, [(0, 0)], [], False, 0),
+    (300, 64, 64, [(0, 0), (0, 1), (1, 0)], [], False, 0),
+    (300, 64, 64, [(0, 0)], [(0, 2)], False, 0),
+    (300, 64, 64, [(0, 0), (0, 1), (1, 0)], [(0, 2), (0, 3), (1, 2)], True, 0),
+    (5000, 131, 136, [(0, 0), (0, 1), (1, 0)], [(0, 2), (0, 3), (1, 2)], True, 2048),
+    (2000, 520, 520, [(1, 1)], [(3, 2)], False, 512),
+])
+def test_gram_kernel_segments(g, t, n, ld, gsegs, csegs, f64, window):
+    """The general statistics kernel (gram_tc.cu) on random bf16 operands:
+    every segment set against an fp64 numpy restatement of the same sum of
+    products (stats.cpp:16-17 shape)."""
+    import ctypes as C
+    import torch
+    rng = np.random.default_rng(t + n)
+    ops = [torch.from_numpy((rng.standard_normal((t, ld)) * (1.0 if k < 2 else 0.05)).astype(np.float32))
+           .to(torch.bfloat16).cuda() for k in range(4)]
+    for o in ops:
+        o[:, n:] = 0
+    host = [o.float().cpu().numpy().astype(np.float64)[:, :n] for o in ops]
+    want_g = sum(host[a].T @ host[b] for a, b in gsegs)
+    want_c = sum(host[a].T @ host[b] for a, b in csegs) if csegs else None
+    dt = torch.float64 if f64 else torch.float32
+    gram = torch.zeros(n, n, dtype=dt, device="cuda")
+    cross = torch.zeros(n, n, dtype=dt, device="cuda")
+    arr = lambda v, t_: (t_ * max(1, len(v)))(*(v or [0]))  # noqa: E731
+    opp = (C.c_void_p * 4)(*[o.data_ptr() for o in ops])
+    lib = g.lib()
+    g._check(lib.ocwg_debug_gram_dev(g.context().handle, C.cast(opp, C.c_void_p), 4, t, n, ld,
+                                     len(gsegs), C.cast(arr([a for a, _ in gsegs], C.c_int), C.c_void_p),
+                                     C.cast(arr([b for _, b in gsegs], C.c_int), C.c_void_p),
+                                     len(csegs), C.cast(arr([a for a, _ in csegs], C.c_int), C.c_void_p),
+                                     C.cast(arr([b for _, b in csegs], C.c_int), C.c_void_p),
+                                     gram.data_ptr(), cross.data_ptr(), int(f64), 0, window))
+    torch.cuda.synchronize()
+    scale = np.sqrt(np.outer(np.abs(np.diagonal(host[0].T @ host[0])), np.abs(np.diagonal(host[0].T @ host[0]))))
+    eg = float(np.max(np.abs(gram.double().cpu().numpy() - want_g) / scale))
+    assert eg <= 2e-5, eg
+    if want_c is not None:
+        ec = float(np.max(np.abs(cross.double().cpu().numpy() - want_c) / scale))
+        assert ec <= 2e-5, ec
+
+
+def test_split_bf16_parts(g, orc):
+    """fp32 statistics inputs -> bf16 parts (stats.cu): P1 = bf16(xp),
+    P2 = bf16(xp - P1), D = fp64(xf) - fp64(xp), D1 = bf16(D), D2 = bf16(D - D1),
+    pad columns zero, flags (1: xp not bf16-exact, 2: D != 0)."""
+    import torch
+    rng = np.random.default_rng(5)
+    t, n, ld = 37, 13, 16
+    xf = rng.standard_normal((t, n)).astype(np.float32)
+    xp = (xf + 0.05 * rng.standard_normal((t, n))).astype(np.float32)
+    dxp, dxf = torch.from_numpy(xp).cuda(), torch.from_numpy(xf).cuda()
+    outs = [torch.zeros((t, ld), dtype=torch.int16, device="cuda") for _ in range(4)]
+    fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+    g._check(g.lib().ocwg_debug_split_dev(g.context().handle, dxp.data_ptr(), dxf.data_ptr(), t, n, ld,
+                                          *[o.data_ptr() for o in outs], fl.data_ptr()))
+    torch.cuda.synchronize()
+    p1, p2, d1, d2 = [o.cpu().numpy().view(np.uint16) for o in outs]
+    val = lambda b: (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
+    np.testing.assert_array_equal(p1[:, :n], orc.bf16_bits(xp))
+    np.testing.assert_array_equal(p1[:, n:], 0)
+    r = xp.astype(np.float64) - val(p1[:, :n])
+    np.testing.assert_array_equal(p2[:, :n], orc.bf16_bits(r.astype(np.float32)))
+    d = xf.astype(np.float64) - xp.astype(np.float64)
+    np.testing.assert_array_equal(d1[:, :n], orc.bf16_bits(d.astype(np.float32)))
+    assert int(fl.item()) == 3
