@@ -395,6 +395,11 @@ void run_hessian(const uint16_t* x, uint64_t tokens, uint64_t n, float* h, bool 
   s.gseg = 1;
   s.gram = h;
   s.accumulate = accumulate;
+  static const long long window = [] {  // tuning switch: OCWG_HESSIAN_WINDOW tokens
+    const char* e = getenv("OCWG_HESSIAN_WINDOW");
+    return e ? atoll(e) : 0LL;
+  }();
+  s.window_tokens = window;
   const int r = gram_tc(s, gws, gws_bytes, st);
   if (r == -1) fail(OCWG_INVALID_INPUT, "hessian: shape outside the tensor-core kernel's range");
   if (r != 0) fail(OCWG_CUDA_ERROR, "hessian: tensor-core kernel launch failed");
