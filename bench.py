@@ -231,7 +231,8 @@ def run_model_mode(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        clocks.start() if not walls else None
+        if not walls:
+            clocks.start()
         payloads, stats = MS.run_rank(mine, local, keep_payload=True)
         ms = torch.tensor([stats["ms"]], device=device)
         if world > 1:
@@ -273,6 +274,9 @@ def main():
     ap.add_argument("--cpu-baseline-only", type=int, default=0, metavar="THREADS",
                     help="(internal) run the CPU baseline leg with THREADS threads, print JSON")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-dropin", action="store_true",
+                    help="skip the reference-API leg (lib/dropin_bench: ocw::accumulate_stats + "
+                         "ocw::quantize_layer on fp32 host matrices)")
     ap.add_argument("--mode", default="layers", choices=["layers", "sharded", "model"],
                     help="N>1: layers = one layer per rank (weak); sharded = one layer split "
                          "over ranks: token-sharded Hessian + NCCL all-reduce + column slabs + "
@@ -413,6 +417,27 @@ def main():
                       "OCW1 payload; X streamed in 32768-token "
                       "chunks under the Hessian)"}
 
+    # ---- the reference's own API path through the C++ drop-in (fp32 host matrices,
+    # X_hat != X; what run_layerwise_sweep calls per layer, pipeline.cpp:215-226)
+    dropin = None
+    exe = ROOT / "paper_2603_28845_b200" / "lib" / "dropin_bench"
+    if world == 1 and not args.no_dropin and not sharded and exe.exists():
+        try:
+            torch.cuda.synchronize()
+            r = subprocess.run([str(exe), str(TOKENS), str(N_IN), str(M_OUT)], capture_output=True,
+                               text=True, timeout=900,
+                               env=dict(os.environ, OCWG_DEVICE=str(local)))
+            js = [l for l in r.stdout.splitlines() if l.startswith("{")]
+            dropin = json.loads(js[-1]) if r.returncode == 0 and js else {"error": r.stderr[-300:]}
+            if "layer_ms" in dropin:
+                dropin["value"] = N_IN * M_OUT / (dropin["layer_ms"] / 1e3)
+                dropin["unit"] = "weights/s"
+                dropin["api"] = ("ocw::accumulate_stats(stats, x_fp, x_hat) + ocw::quantize_layer(w, stats, "
+                                 "gptq W4 g128 act-order, block_cols 32) through cpp/ocw_dropin.cpp "
+                                 "(fp32 host matrices in and out; layer_qep_ms adds QEP alpha 1 eta 0.01)")
+        except Exception as e:  # report, never fake
+            dropin = {"error": str(e)[:300]}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -465,6 +490,7 @@ def main():
         "gpu_launches": launches,
         "clocks": ck,
         "e2e": e2e,
+        "dropin": dropin,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)

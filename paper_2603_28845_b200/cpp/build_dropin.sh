@@ -25,4 +25,6 @@ for t in test_core test_layerwise; do
   $CXX $FLAGS -o "$LIB/dropin_$t" "$REF/tests/test_main.cpp" "$REF/tests/$t.cpp" \
     -L"$LIB" -locw_dropin -locwg -Wl,-rpath,'$ORIGIN' -ldl
 done
-echo "build_dropin: built $LIB/{libocw_dropin.so,dropin_test_core,dropin_test_layerwise}"
+$CXX $FLAGS -O3 -pthread -o "$LIB/dropin_bench" "$HERE/dropin_bench.cpp" \
+  -L"$LIB" -locw_dropin -locwg -Wl,-rpath,'$ORIGIN' -ldl
+echo "build_dropin: built $LIB/{libocw_dropin.so,dropin_test_core,dropin_test_layerwise,dropin_bench}"

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ocw/errors.hpp"
@@ -226,15 +227,36 @@ Matrix CalibStats::cross_matrix() const {
 }
 
 namespace {
+// Eigen::MatrixXd (column-major) <-> row-major buffers of the C ABI: a blocked
+// transpose over row bands on a few host threads (the N x N statistics are
+// 128 MiB each at N = 4096)
+template <typename F>
+void bands(Eigen::Index rows, F&& f) {
+  const unsigned nt = rows >= 512 ? 8u : 1u;
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] { f(rows * t / nt, rows * (t + 1) / nt); });
+  for (auto& x : th) x.join();
+}
 std::vector<double> row_major(const Eigen::MatrixXd& a) {
   std::vector<double> v(size_t(a.rows()) * size_t(a.cols()));
-  for (Eigen::Index i = 0; i < a.rows(); ++i)
-    for (Eigen::Index j = 0; j < a.cols(); ++j) v[size_t(i) * size_t(a.cols()) + size_t(j)] = a(i, j);
+  const double* src = a.data();
+  const size_t R = size_t(a.rows()), Cc = size_t(a.cols());
+  bands(a.rows(), [&](Eigen::Index i0, Eigen::Index i1) {
+    for (size_t jb = 0; jb < Cc; jb += 64)
+      for (size_t i = size_t(i0); i < size_t(i1); ++i)
+        for (size_t j = jb; j < std::min(Cc, jb + 64); ++j) v[i * Cc + j] = src[j * R + i];
+  });
   return v;
 }
 void from_row_major(const std::vector<double>& v, Eigen::MatrixXd& a) {
-  for (Eigen::Index i = 0; i < a.rows(); ++i)
-    for (Eigen::Index j = 0; j < a.cols(); ++j) a(i, j) = v[size_t(i) * size_t(a.cols()) + size_t(j)];
+  double* dst = a.data();
+  const size_t R = size_t(a.rows()), Cc = size_t(a.cols());
+  bands(a.rows(), [&](Eigen::Index i0, Eigen::Index i1) {
+    for (size_t jb = 0; jb < Cc; jb += 64)
+      for (size_t i = size_t(i0); i < size_t(i1); ++i)
+        for (size_t j = jb; j < std::min(Cc, jb + 64); ++j) dst[j * R + i] = v[i * Cc + j];
+  });
 }
 }  // namespace
 

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ocwg.h"
@@ -58,6 +59,8 @@ struct ocwg_ctx {
   void* io = nullptr;              // grow-only device buffers of the host-pointer calls
   size_t io_bytes = 0;
   std::vector<cudaEvent_t> cev;    // per-chunk copy events
+  void* stage[2] = {nullptr, nullptr};  // pinned staging for large pageable host copies
+  cudaEvent_t stage_ev[2] = {};
   std::mutex mu;
 };
 
@@ -196,6 +199,93 @@ void h2d(void* d, const void* h, size_t bytes, ocwg_ctx* ctx) {
 }
 void d2h(void* h, const void* d, size_t bytes, ocwg_ctx* ctx) {
   if (bytes && h) ck(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+}
+
+// Large copies between PAGEABLE host memory (e.g. the std::vector inside an
+// ocw::Matrix) and the device: through two pinned staging buffers, the host
+// side memcpy of one chunk (several CPU threads) overlapping the DMA of the
+// other, instead of the driver's synchronous pageable path.
+constexpr size_t kStageBytes = size_t(64) << 20;
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const unsigned nt = bytes < (size_t(4) << 20) ? 1u : 8u;
+  if (nt == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t) {
+    const size_t a = bytes * t / nt, b = bytes * (t + 1) / nt;
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
+  }
+  for (auto& x : th) x.join();
+}
+void ensure_stage(ocwg_ctx* ctx) {
+  for (int b = 0; b < 2; ++b) {
+    if (!ctx->stage[b]) {
+      ck(cudaMallocHost(&ctx->stage[b], kStageBytes), "cudaMallocHost(stage)");
+      ck(cudaEventCreateWithFlags(&ctx->stage_ev[b], cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventRecord(ctx->stage_ev[b], ctx->cpy), "event");
+    }
+  }
+}
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+// H2D of a large host buffer, ordered before later work on ctx->stream
+void h2d_big(void* d, const void* h, size_t bytes, ocwg_ctx* ctx) {
+  if (bytes < kStageBytes || is_pinned(h)) return h2d(d, h, bytes, ctx);
+  ensure_stage(ctx);
+  ck(cudaEventRecord(ctx->stage_ev[0], ctx->stream), "event");  // after prior work on the stream
+  ck(cudaStreamWaitEvent(ctx->cpy, ctx->stage_ev[0], 0), "event");
+  ck(cudaEventRecord(ctx->stage_ev[0], ctx->cpy), "event");
+  ck(cudaEventRecord(ctx->stage_ev[1], ctx->cpy), "event");
+  for (size_t off = 0, k = 0; off < bytes; off += kStageBytes, ++k) {
+    const int b = int(k & 1);
+    const size_t len = std::min(kStageBytes, bytes - off);
+    ck(cudaEventSynchronize(ctx->stage_ev[b]), "event sync");  // its previous DMA is done
+    par_memcpy(ctx->stage[b], static_cast<const char*>(h) + off, len);
+    ck(cudaMemcpyAsync(static_cast<char*>(d) + off, ctx->stage[b], len, cudaMemcpyHostToDevice,
+                       ctx->cpy),
+       "H2D(staged)");
+    ck(cudaEventRecord(ctx->stage_ev[b], ctx->cpy), "event");
+  }
+  ck(cudaStreamWaitEvent(ctx->stream, ctx->stage_ev[0], 0), "event");
+  ck(cudaStreamWaitEvent(ctx->stream, ctx->stage_ev[1], 0), "event");
+}
+// D2H of a large device buffer after the work on ctx->stream; synchronous
+void d2h_big(void* h, const void* d, size_t bytes, ocwg_ctx* ctx) {
+  if (!h || !bytes) return;
+  if (bytes < kStageBytes || is_pinned(h)) {
+    d2h(h, d, bytes, ctx);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    return;
+  }
+  ensure_stage(ctx);
+  size_t pend_off[2] = {0, 0}, pend_len[2] = {0, 0};
+  for (size_t off = 0, k = 0; off < bytes; off += kStageBytes, ++k) {
+    const int b = int(k & 1);
+    const size_t len = std::min(kStageBytes, bytes - off);
+    if (pend_len[b]) {  // drain what this buffer holds
+      ck(cudaEventSynchronize(ctx->stage_ev[b]), "event sync");
+      par_memcpy(static_cast<char*>(h) + pend_off[b], ctx->stage[b], pend_len[b]);
+    }
+    ck(cudaMemcpyAsync(ctx->stage[b], static_cast<const char*>(d) + off, len,
+                       cudaMemcpyDeviceToHost, ctx->stream),
+       "D2H(staged)");
+    ck(cudaEventRecord(ctx->stage_ev[b], ctx->stream), "event");
+    pend_off[b] = off;
+    pend_len[b] = len;
+  }
+  for (int b = 0; b < 2; ++b)
+    if (pend_len[b]) {
+      ck(cudaEventSynchronize(ctx->stage_ev[b]), "event sync");
+      par_memcpy(static_cast<char*>(h) + pend_off[b], ctx->stage[b], pend_len[b]);
+    }
 }
 
 // ---------------------------------------------------------------- GPTQ core (device pointers)
@@ -447,6 +537,10 @@ int ocwg_destroy(ocwg_ctx* ctx) {
     cudaStreamSynchronize(ctx->cpy);
     for (auto& e : ctx->cev) cudaEventDestroy(e);
     if (ctx->io) cudaFree(ctx->io);
+    for (int b = 0; b < 2; ++b) {
+      if (ctx->stage[b]) cudaFreeHost(ctx->stage[b]);
+      if (ctx->stage_ev[b]) cudaEventDestroy(ctx->stage_ev[b]);
+    }
     cudaStreamDestroy(ctx->cpy);
     cudaStreamDestroy(ctx->aux);
     cudaStreamDestroy(ctx->own);
@@ -823,10 +917,10 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
                    oc = ar.reserve(want_cross ? dim * dim * 8 : 8), ofl = ar.reserve(16),
                    ows = ar.reserve(gram_tc_workspace_bytes((long long)dim));
       ar.commit();
-      h2d(ar.at<float>(op), x_pert, rows * dim * 4, ctx);
-      if (want_cross) h2d(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
-      h2d(ar.at<double>(og), gram, dim * dim * 8, ctx);
-      if (want_cross) h2d(ar.at<double>(oc), cross, dim * dim * 8, ctx);
+      h2d_big(ar.at<float>(op), x_pert, rows * dim * 4, ctx);
+      if (want_cross) h2d_big(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
+      h2d_big(ar.at<double>(og), gram, dim * dim * 8, ctx);
+      if (want_cross) h2d_big(ar.at<double>(oc), cross, dim * dim * 8, ctx);
       unsigned* fl = ar.at<unsigned>(ofl);
       ck(cudaMemsetAsync(fl, 0, 4, st), "memset");
       uint16_t *p1 = ar.at<uint16_t>(o1), *p2 = ar.at<uint16_t>(o2), *d1 = ar.at<uint16_t>(o3),
@@ -860,9 +954,9 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
       s.window_tokens = 2048;  // short TMEM accumulations, fp64 across windows
       const int r = gram_tc(s, ar.at<void>(ows), gram_tc_workspace_bytes((long long)dim), st);
       if (r != 0) fail(OCWG_CUDA_ERROR, "accumulate_stats: tensor-core kernel launch failed");
-      d2h(gram, ar.at<double>(og), dim * dim * 8, ctx);
-      if (want_cross) d2h(cross, ar.at<double>(oc), dim * dim * 8, ctx);
       finish(ctx);
+      d2h_big(gram, ar.at<double>(og), dim * dim * 8, ctx);
+      if (want_cross) d2h_big(cross, ar.at<double>(oc), dim * dim * 8, ctx);
     }
     if (token_count) *token_count += rows;
   });
@@ -1133,11 +1227,11 @@ int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, const
                  owh = ar.reserve(w_hat ? n * m * 4 : 4), om = ar.reserve(4096 * 4);
     ar.commit();
     float* wd = ar.at<float>(ow);
-    h2d(wd, w, n * m * 4, ctx);
-    if (corr || method == 1) h2d(ar.at<double>(og), gram, n * n * 8, ctx);
+    h2d_big(wd, w, n * m * 4, ctx);
+    if (corr || method == 1) h2d_big(ar.at<double>(og), gram, n * n * 8, ctx);
     const float* target = wd;
     if (corr) {  // W* = W + alpha (gram + lambda I)^-1 (cross W)   (layerwise.cpp:103-111)
-      h2d(ar.at<double>(oc), cross, n * n * 8, ctx);
+      h2d_big(ar.at<double>(oc), cross, n * n * 8, ctx);
       set_tc_workspace(nullptr, 0);
       qep_target_f64(wd, ar.at<double>(og), ar.at<double>(oc), (long long)n, (long long)m,
                      qep->alpha, qep->eta, ar.at<float>(ot), ar.at<double>(oqw), ar.at<int>(oqf),

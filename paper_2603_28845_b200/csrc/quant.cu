@@ -224,69 +224,59 @@ __global__ void dequantize_kernel(const int16_t* __restrict__ codes, long long r
   }
 }
 
-// Pack: thread t owns codes [32t, 32t+32) = exactly 4*bits bytes of the
-// LSB-first stream (container.cpp:15-35 BitWriter); emitted as `bits`
-// 32-bit words.  The stream's final partial byte is zero-padded (flush()).
-__global__ void pack_codes_kernel(const int16_t* __restrict__ codes, long long n_codes, int bits,
-                                  int qmin, uint8_t* out) {
+// Pack: thread t owns codes [128t, 128t+128) = exactly 16*bits bytes of the
+// LSB-first stream (container.cpp:15-35 BitWriter), assembled 32 codes
+// (= `bits` 32-bit words) at a time and written as `bits` 16-byte stores.
+// The stream's final partial byte is zero-padded (flush()).
+constexpr int kPackCodes = 128;
+template <int B>
+__global__ void pack_codes_kernel(const int16_t* __restrict__ codes, long long n_codes, int qmin,
+                                  uint8_t* out) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long c0 = t * 32;
+  const long long c0 = t * kPackCodes;
   if (c0 >= n_codes) return;
-  const uint32_t mask = (1u << bits) - 1u;
-  uint32_t words[8];
+  constexpr uint32_t mask = (1u << B) - 1u;
+  uint32_t words[4 * B];  // 4 sub-blocks of 32 codes, B words each
 #pragma unroll
-  for (int i = 0; i < 8; ++i) words[i] = 0;
-  const int cnt = int(min(32LL, n_codes - c0));
-  int16_t cv[32];
-  if (cnt == 32 && (reinterpret_cast<uintptr_t>(codes) & 15) == 0) {  // 4 x 16-byte loads
+  for (int i = 0; i < 4 * B; ++i) words[i] = 0;
+  const int cnt_all = int(min((long long)kPackCodes, n_codes - c0));
+  const bool vec = cnt_all == kPackCodes && (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int4 v4 = __ldg(reinterpret_cast<const int4*>(codes + c0) + q);
-      const int16_t* p = reinterpret_cast<const int16_t*>(&v4);
+  for (int sb = 0; sb < 4; ++sb) {
+    const int cnt = min(32, max(0, cnt_all - 32 * sb));
+    int16_t cv[32];
+    if (vec) {  // 4 x 16-byte loads
 #pragma unroll
-      for (int e = 0; e < 8; ++e) cv[8 * q + e] = p[e];
-    }
-  } else {
+      for (int q = 0; q < 4; ++q) {
+        const int4 v4 = __ldg(reinterpret_cast<const int4*>(codes + c0 + 32 * sb) + q);
+        const int16_t* p = reinterpret_cast<const int16_t*>(&v4);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) cv[k] = k < cnt ? codes[c0 + k] : int16_t(qmin);
-  }
-  // (codes past the end contribute zero bits: they are never written out)
-  auto dense = [&](auto bc) {  // bits dividing 32: whole codes per word
-    constexpr int B = decltype(bc)::value, PER = 32 / B;
-#pragma unroll
-    for (int i = 0; i < B; ++i)
-#pragma unroll
-      for (int e = 0; e < PER; ++e) {
-        const int k = i * PER + e;
-        const uint32_t v = k < cnt ? (uint32_t(int(cv[k]) - qmin) & mask) : 0u;
-        words[i] |= v << (e * B);
+        for (int e = 0; e < 8; ++e) cv[8 * q + e] = p[e];
       }
-  };
-  if (bits == 4) dense(std::integral_constant<int, 4>());
-  else if (bits == 2) dense(std::integral_constant<int, 2>());
-  else if (bits == 8) dense(std::integral_constant<int, 8>());
-  else
+    } else {
 #pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const uint32_t v = k < cnt ? (uint32_t(int(cv[k]) - qmin) & mask) : 0u;
-    const int bit = k * bits;
-    const int wi = bit >> 5, sh = bit & 31;
+      for (int k = 0; k < 32; ++k) cv[k] = k < cnt ? codes[c0 + 32 * sb + k] : int16_t(qmin);
+    }
+    // (codes past the end contribute zero bits: they are never written out)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (i == wi) words[i] |= v << sh;
-      if (i == wi + 1 && sh + bits > 32) words[i] |= v >> (32 - sh);
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t v = k < cnt ? (uint32_t(int(cv[k]) - qmin) & mask) : 0u;
+      const int bit = k * B, wi = bit >> 5, sh = bit & 31;  // static after unrolling
+      words[sb * B + wi] |= v << sh;
+      if (sh + B > 32) words[sb * B + wi + 1] |= v >> (32 - sh);
     }
   }
-  const long long byte0 = t * 4LL * bits;
-  const long long nbytes_total = (n_codes * bits + 7) / 8;
-  if (cnt == 32 && ((byte0 & 3) == 0)) {
-    uint32_t* o = reinterpret_cast<uint32_t*>(out + byte0);
+  const long long byte0 = t * 16LL * B;
+  if (cnt_all == kPackCodes && ((reinterpret_cast<uintptr_t>(out + byte0) & 15) == 0)) {
+    uint4* o = reinterpret_cast<uint4*>(out + byte0);
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < bits) o[i] = words[i];
+    for (int q = 0; q < B; ++q)
+      o[q] = make_uint4(words[4 * q], words[4 * q + 1], words[4 * q + 2], words[4 * q + 3]);
   } else {
-    const long long nb = min(4LL * bits, nbytes_total - byte0);
-    for (long long b = 0; b < nb; ++b) out[byte0 + b] = uint8_t(words[b >> 2] >> (8 * (b & 3)));
+    const long long nb = min(16LL * B, (n_codes * B + 7) / 8 - byte0);
+#pragma unroll
+    for (int b = 0; b < 16 * B; ++b)
+      if (b < nb) out[byte0 + b] = uint8_t(words[b >> 2] >> (8 * (b & 3)));
   }
 }
 
@@ -401,10 +391,17 @@ void launch_dequantize(const int16_t* codes, long long rows, long long cols, con
 void launch_pack(const int16_t* codes, long long n_codes, long long n_groups, const QCfg& c,
                  const float* scales, const int32_t* zeros, uint8_t* out, cudaStream_t st) {
   count_launches(2);
-  const long long threads = (n_codes + 31) / 32;
-  if (threads > 0)
-    pack_codes_kernel<<<int((threads + 255) / 256), 256, 0, st>>>(codes, n_codes, c.bits, c.qmin,
-                                                                  out);
+  const long long threads = (n_codes + kPackCodes - 1) / kPackCodes;
+  if (threads > 0) {
+    const int g = int((threads + 127) / 128);
+    switch (c.bits) {
+#define OCWG_PACK(B) \
+  case B: pack_codes_kernel<B><<<g, 128, 0, st>>>(codes, n_codes, c.qmin, out); break;
+      OCWG_PACK(1) OCWG_PACK(2) OCWG_PACK(3) OCWG_PACK(4) OCWG_PACK(5) OCWG_PACK(6) OCWG_PACK(7)
+      OCWG_PACK(8)
+#undef OCWG_PACK
+    }
+  }
   const long long code_bytes = (n_codes * c.bits + 7) / 8;
   pack_meta_kernel<<<grid_for(n_groups, 256), 256, 0, st>>>(n_groups, c.scheme == 1, scales, zeros,
                                                              out + code_bytes);

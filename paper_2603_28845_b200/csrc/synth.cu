@@ -36,7 +36,7 @@ __device__ __forceinline__ void normals4(unsigned long long seed, unsigned long 
     // u1 in (0, 1] (log finite), u2 in [0, 1)
     const float u1 = (float(w[2 * p] >> 8) + 1.0f) * (1.0f / 16777216.0f);
     const float u2 = float(w[2 * p + 1] >> 8) * (1.0f / 16777216.0f);
-    const float rad = sqrtf(-2.0f * logf(u1));
+    const float rad = sqrtf(-2.0f * __logf(u1));
     float sn, cs;
     sincospif(2.0f * u2, &sn, &cs);
     z[2 * p] = rad * cs;
@@ -54,8 +54,12 @@ __global__ void synth_kernel(int kind, unsigned long long seed, long long rows, 
                              float stddev, const float* __restrict__ col_scale, void* out) {
   const long long total = rows * cols;
   const long long nq = (total + 3) / 4;
-  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
-       q += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // column of element 4q, advanced incrementally (no 64-bit modulo per element)
+  long long col = (4 * q) % cols;
+  const long long step = (4 * stride) % cols;
+  for (; q < nq; q += stride, col = (col + step >= cols ? col + step - cols : col + step)) {
     float z[4];
     normals4(seed, (unsigned long long)q, 0u, z);
     float v[4];
@@ -65,11 +69,12 @@ __global__ void synth_kernel(int kind, unsigned long long seed, long long rows, 
 #pragma unroll
       for (int i = 0; i < 4; ++i) v[i] = (z[i] / (1.0f + __expf(-z[i]))) * b[i];  // silu(a) * b
     } else {
+      long long ci = col;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const long long e = 4 * q + i;
-        const float sc = kind == 2 ? stddev : (col_scale ? col_scale[e % cols] : 1.0f);
+        const float sc = kind == 2 ? stddev : (col_scale ? col_scale[ci] : 1.0f);
         v[i] = z[i] * sc;
+        if (++ci == cols) ci = 0;
       }
     }
     const long long e0 = 4 * q;
@@ -99,9 +104,11 @@ __global__ void synth_kernel(int kind, unsigned long long seed, long long rows, 
 
 void launch_synth(int kind, unsigned long long seed, long long rows, long long cols, float stddev,
                   const float* col_scale, void* out, int max_ctas, cudaStream_t st) {
+  // one quad per thread by default: many short CTAs, so a generator running
+  // beside latency-bound kernels on a low-priority stream frees SMs quickly
   const long long nq = (rows * cols + 3) / 4;
   long long g = (nq + 255) / 256;
-  const long long cap = max_ctas > 0 ? max_ctas : (long long)device_sms() * 8;
+  const long long cap = max_ctas > 0 ? max_ctas : (1LL << 31) - 1;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   count_launches(1);

@@ -112,10 +112,16 @@ def outlier_scale(n: int, frac: float, seed: int, osc: float):
 
 
 def run_rank(units: list[Unit], device: int, tokens: int = TOKENS, bits: int = 4, group: int = 128,
-             keep_payload: bool = True, timing: bool = True):
+             keep_payload: bool = True, timing: bool = True, overlap: bool = True):
     """Quantize this rank's units on `device`.  Returns (payloads {layer name:
-    uint8 device tensor}, stats) -- stats has the device time of the loop
-    (CUDA events) and per-phase sums (synthetic generation vs quantization)."""
+    uint8 device tensor}, stats) -- stats has the device time of the whole
+    loop (CUDA events) and the unit count / weights.
+
+    The calibration X of unit k+1 is generated on a second stream into the
+    other half of a double buffer while unit k's Hessian / factorisation /
+    sweeps run (the generator stands in for the model forward that collects
+    layer inputs; it is HBM / ALU work that overlaps the latency-bound
+    factorisation and sweep)."""
     import torch
 
     from . import GptqOptions, Granularity, QuantConfig, Scheme, dev
@@ -124,27 +130,51 @@ def run_rank(units: list[Unit], device: int, tokens: int = TOKENS, bits: int = 4
     opts = GptqOptions(actorder=True, percdamp=0.01, block_cols=128)
     dv = torch.device("cuda", device)
     payloads = {}
-    stats = {"units": len(units), "weights": 0, "gen_ms": 0.0, "quant_ms": 0.0, "ms": 0.0}
+    stats = {"units": len(units), "weights": 0, "ms": 0.0, "overlap": overlap}
     if not units:
         return payloads, stats
     nmax = max(u.n for u in units)
-    x = torch.empty((tokens, nmax), dtype=torch.bfloat16, device=dv)
-    scale_cache = {}
-    st = torch.cuda.current_stream(dv)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * len(units))]
-    t_all = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    nbuf = 2 if overlap else 1
+    xbuf = [torch.empty(tokens * nmax, dtype=torch.bfloat16, device=dv) for _ in range(nbuf)]
+    scales = {}
+    for u in units:
+        if not u.silu and u.n not in scales:
+            scales[u.n] = torch.from_numpy(outlier_scale(u.n, 0.01, seeds(u)["pick"], 20.0)).to(dv)
+    # the quantization on a high-priority stream, the generator at default priority:
+    # pending factorisation / sweep CTAs are dispatched before further generator CTAs
+    main = torch.cuda.Stream(dv, priority=-5) if overlap else torch.cuda.current_stream(dv)
+    gen = torch.cuda.Stream(dv) if overlap else main
+    torch.cuda.synchronize(dv)
+    ready = [torch.cuda.Event() for _ in range(nbuf)]
+    free = [torch.cuda.Event() for _ in range(nbuf)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def xview(k):
+        u = units[k]
+        return xbuf[k % nbuf][:tokens * u.n].view(tokens, u.n)
+
+    def gen_x(k):
+        u = units[k]
+        with torch.cuda.stream(gen):
+            if k >= nbuf:
+                gen.wait_event(free[k % nbuf])
+            if u.silu:
+                dev.synth(1, seeds(u)["x"], xview(k))
+            else:
+                dev.synth(0, seeds(u)["x"], xview(k), col_scale=scales[u.n])
+            ready[k % nbuf].record(gen)
+
     dev.set_async(True, device)  # device calls only enqueue; errors surface at synchronize
-    t_all[0].record(st)
+    ctx_main = torch.cuda.stream(main)
+    ctx_main.__enter__()
+    t0.record(main)
+    if overlap:
+        gen.wait_event(t0)
+    for k in range(min(nbuf, len(units))):
+        gen_x(k)
     for k, u in enumerate(units):
         sd = seeds(u)
-        ev[3 * k].record(st)
-        xu = x[:, :u.n] if u.n == nmax else x.view(-1)[:tokens * u.n].view(tokens, u.n)
-        if u.silu:
-            dev.synth(1, sd["x"], xu)
-        else:
-            if u.n not in scale_cache:
-                scale_cache[u.n] = torch.from_numpy(outlier_scale(u.n, 0.01, sd["pick"], 20.0)).to(dv)
-            dev.synth(0, sd["x"], xu, col_scale=scale_cache[u.n])
+        main.wait_event(ready[k % nbuf])
         ws, outs = [], []
         for (name, m), wseed in zip(u.linears, sd["w"]):
             w = torch.empty((u.n, m), dtype=torch.float32, device=dv)
@@ -152,24 +182,23 @@ def run_rank(units: list[Unit], device: int, tokens: int = TOKENS, bits: int = 4
             ws.append(w)
             outs.append(dev.LayerBuffers(u.n, m, cfg, device, w_hat=False, payload=keep_payload, h=False))
             stats["weights"] += u.n * m
-        ev[3 * k + 1].record(st)
-        dev.quantize_layers(ws, xu, cfg, opts, outs)
-        ev[3 * k + 2].record(st)
+        dev.quantize_layers(ws, xview(k), cfg, opts, outs)
+        free[k % nbuf].record(main)
+        if k + nbuf < len(units):
+            gen_x(k + nbuf)
         for (name, m), o in zip(u.linears, outs):
             if keep_payload:
                 payloads[f"model.layers.{u.block}.{name}"] = o.payload
         del ws, outs
-    t_all[1].record(st)
+    t1.record(main)
+    ctx_main.__exit__(None, None, None)
     torch.cuda.synchronize(dv)
     try:
         dev.synchronize(device)
     finally:
         dev.set_async(False, device)
     if timing:
-        for k in range(len(units)):
-            stats["gen_ms"] += ev[3 * k].elapsed_time(ev[3 * k + 1])
-            stats["quant_ms"] += ev[3 * k + 1].elapsed_time(ev[3 * k + 2])
-        stats["ms"] = t_all[0].elapsed_time(t_all[1])
+        stats["ms"] = t0.elapsed_time(t1)
     return payloads, stats
 
 
