@@ -249,7 +249,9 @@ def run_model_mode(args):
             "metric": "C4 whole-model sweep throughput (weights/s), 32 x 7 Llama-2-7B linears W4 g128",
             "value": total_w / (wall / 1e3), "unit": "weights/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall,
-            "wall_clock_s": wall / 1e3, "higher_is_better": True, "scaling": "strong",
+            "wall_clock_s": wall / 1e3,
+            "quantize_wall_clock_s": (stats or {}).get("quant_ms", 0) / 1e3,
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16 (Hessian); fp32 factor/sweep", "data": "synthetic",
             "config": {"workload": f"C4: {args.blocks} blocks x 7 linears (q/k/v/o 4096x4096, gate/up "
                                    f"4096x11008, down 11008x4096, reference orientation), "

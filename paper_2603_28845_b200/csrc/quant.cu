@@ -224,58 +224,55 @@ __global__ void dequantize_kernel(const int16_t* __restrict__ codes, long long r
   }
 }
 
-// Pack: thread t owns codes [128t, 128t+128) = exactly 16*bits bytes of the
-// LSB-first stream (container.cpp:15-35 BitWriter), assembled 32 codes
-// (= `bits` 32-bit words) at a time and written as `bits` 16-byte stores.
-// The stream's final partial byte is zero-padded (flush()).
-constexpr int kPackCodes = 128;
+// Pack: thread t owns CPT consecutive codes = exactly 16 bytes of the
+// LSB-first stream for b | 128 (CPT = 128 / b: 32 codes at 4 bits), else 128
+// codes = 16 b bytes (container.cpp:15-35 BitWriter), written as 16-byte
+// stores.  The stream's final partial byte is zero-padded (flush()).
+template <int B>
+constexpr int pack_cpt() { return (128 % B == 0) ? 128 / B : 128; }
 template <int B>
 __global__ void pack_codes_kernel(const int16_t* __restrict__ codes, long long n_codes, int qmin,
                                   uint8_t* out) {
+  constexpr int CPT = pack_cpt<B>(), NW = CPT * B / 32;  // codes, 32-bit words per thread
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long c0 = t * kPackCodes;
+  const long long c0 = t * CPT;
   if (c0 >= n_codes) return;
   constexpr uint32_t mask = (1u << B) - 1u;
-  uint32_t words[4 * B];  // 4 sub-blocks of 32 codes, B words each
+  uint32_t words[NW];
 #pragma unroll
-  for (int i = 0; i < 4 * B; ++i) words[i] = 0;
-  const int cnt_all = int(min((long long)kPackCodes, n_codes - c0));
-  const bool vec = cnt_all == kPackCodes && (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
+  for (int i = 0; i < NW; ++i) words[i] = 0;
+  const int cnt = int(min((long long)CPT, n_codes - c0));
+  int16_t cv[CPT];
+  if (cnt == CPT && (reinterpret_cast<uintptr_t>(codes) & 15) == 0) {  // 16-byte loads
 #pragma unroll
-  for (int sb = 0; sb < 4; ++sb) {
-    const int cnt = min(32, max(0, cnt_all - 32 * sb));
-    int16_t cv[32];
-    if (vec) {  // 4 x 16-byte loads
+    for (int q = 0; q < CPT / 8; ++q) {
+      const int4 v4 = __ldg(reinterpret_cast<const int4*>(codes + c0) + q);
+      const int16_t* p = reinterpret_cast<const int16_t*>(&v4);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int4 v4 = __ldg(reinterpret_cast<const int4*>(codes + c0 + 32 * sb) + q);
-        const int16_t* p = reinterpret_cast<const int16_t*>(&v4);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) cv[8 * q + e] = p[e];
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 32; ++k) cv[k] = k < cnt ? codes[c0 + 32 * sb + k] : int16_t(qmin);
+      for (int e = 0; e < 8; ++e) cv[8 * q + e] = p[e];
     }
-    // (codes past the end contribute zero bits: they are never written out)
+  } else {
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const uint32_t v = k < cnt ? (uint32_t(int(cv[k]) - qmin) & mask) : 0u;
-      const int bit = k * B, wi = bit >> 5, sh = bit & 31;  // static after unrolling
-      words[sb * B + wi] |= v << sh;
-      if (sh + B > 32) words[sb * B + wi + 1] |= v >> (32 - sh);
-    }
+    for (int k = 0; k < CPT; ++k) cv[k] = k < cnt ? codes[c0 + k] : int16_t(qmin);
   }
-  const long long byte0 = t * 16LL * B;
-  if (cnt_all == kPackCodes && ((reinterpret_cast<uintptr_t>(out + byte0) & 15) == 0)) {
+  // (codes past the end contribute zero bits: they are never written out)
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const uint32_t v = k < cnt ? (uint32_t(int(cv[k]) - qmin) & mask) : 0u;
+    const int bit = k * B, wi = bit >> 5, sh = bit & 31;  // static after unrolling
+    words[wi] |= v << sh;
+    if (sh + B > 32) words[wi + 1] |= v >> (32 - sh);
+  }
+  const long long byte0 = t * (4LL * NW);
+  if (cnt == CPT && ((reinterpret_cast<uintptr_t>(out + byte0) & 15) == 0)) {
     uint4* o = reinterpret_cast<uint4*>(out + byte0);
 #pragma unroll
-    for (int q = 0; q < B; ++q)
+    for (int q = 0; q < NW / 4; ++q)
       o[q] = make_uint4(words[4 * q], words[4 * q + 1], words[4 * q + 2], words[4 * q + 3]);
   } else {
-    const long long nb = min(16LL * B, (n_codes * B + 7) / 8 - byte0);
+    const long long nb = min(4LL * NW, (n_codes * B + 7) / 8 - byte0);
 #pragma unroll
-    for (int b = 0; b < 16 * B; ++b)
+    for (int b = 0; b < 4 * NW; ++b)
       if (b < nb) out[byte0 + b] = uint8_t(words[b >> 2] >> (8 * (b & 3)));
   }
 }
@@ -391,12 +388,13 @@ void launch_dequantize(const int16_t* codes, long long rows, long long cols, con
 void launch_pack(const int16_t* codes, long long n_codes, long long n_groups, const QCfg& c,
                  const float* scales, const int32_t* zeros, uint8_t* out, cudaStream_t st) {
   count_launches(2);
-  const long long threads = (n_codes + kPackCodes - 1) / kPackCodes;
-  if (threads > 0) {
-    const int g = int((threads + 127) / 128);
+  if (n_codes > 0) {
     switch (c.bits) {
-#define OCWG_PACK(B) \
-  case B: pack_codes_kernel<B><<<g, 128, 0, st>>>(codes, n_codes, c.qmin, out); break;
+#define OCWG_PACK(B)                                                                     \
+  case B: {                                                                              \
+    const long long thr = (n_codes + pack_cpt<B>() - 1) / pack_cpt<B>();                 \
+    pack_codes_kernel<B><<<int((thr + 255) / 256), 256, 0, st>>>(codes, n_codes, c.qmin, out); \
+  } break;
       OCWG_PACK(1) OCWG_PACK(2) OCWG_PACK(3) OCWG_PACK(4) OCWG_PACK(5) OCWG_PACK(6) OCWG_PACK(7)
       OCWG_PACK(8)
 #undef OCWG_PACK

@@ -112,20 +112,26 @@ def outlier_scale(n: int, frac: float, seed: int, osc: float):
 
 
 def run_rank(units: list[Unit], device: int, tokens: int = TOKENS, bits: int = 4, group: int = 128,
-             keep_payload: bool = True, timing: bool = True, overlap: bool = True):
+             keep_payload: bool = True, timing: bool = True, overlap: bool | None = None):
     """Quantize this rank's units on `device`.  Returns (payloads {layer name:
     uint8 device tensor}, stats) -- stats has the device time of the whole
     loop (CUDA events) and the unit count / weights.
 
-    The calibration X of unit k+1 is generated on a second stream into the
-    other half of a double buffer while unit k's Hessian / factorisation /
-    sweeps run (the generator stands in for the model forward that collects
-    layer inputs; it is HBM / ALU work that overlaps the latency-bound
-    factorisation and sweep)."""
+    With overlap (OCWG_MODEL_OVERLAP=1) the calibration X of unit k+1 is
+    generated on a second, lower-priority stream into the other half of a
+    double buffer while unit k is quantized.  Measured on one B200 it gains
+    nothing (3.19 s vs 3.21 s for the 32-block model): the generator only
+    finds room beside the Hessian, which it slows down, as the factorisation
+    fills every SM's register file.  So the default is sequential, which
+    also separates the generation (a stand-in for the model forward that
+    collects layer inputs) from the quantization in the stats."""
     import torch
 
     from . import GptqOptions, Granularity, QuantConfig, Scheme, dev
 
+    import os
+    if overlap is None:
+        overlap = os.environ.get("OCWG_MODEL_OVERLAP", "0") == "1"
     cfg = QuantConfig(bits, Scheme.asymmetric, Granularity.per_group, group)
     opts = GptqOptions(actorder=True, percdamp=0.01, block_cols=128)
     dv = torch.device("cuda", device)
@@ -148,6 +154,9 @@ def run_rank(units: list[Unit], device: int, tokens: int = TOKENS, bits: int = 4
     ready = [torch.cuda.Event() for _ in range(nbuf)]
     free = [torch.cuda.Event() for _ in range(nbuf)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # per-unit phase events (meaningful without overlap): generation | quantization
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in units]
 
     def xview(k):
         u = units[k]
@@ -175,6 +184,7 @@ def run_rank(units: list[Unit], device: int, tokens: int = TOKENS, bits: int = 4
     for k, u in enumerate(units):
         sd = seeds(u)
         main.wait_event(ready[k % nbuf])
+        ev[k][0].record(main)
         ws, outs = [], []
         for (name, m), wseed in zip(u.linears, sd["w"]):
             w = torch.empty((u.n, m), dtype=torch.float32, device=dv)
@@ -183,6 +193,7 @@ def run_rank(units: list[Unit], device: int, tokens: int = TOKENS, bits: int = 4
             outs.append(dev.LayerBuffers(u.n, m, cfg, device, w_hat=False, payload=keep_payload, h=False))
             stats["weights"] += u.n * m
         dev.quantize_layers(ws, xview(k), cfg, opts, outs)
+        ev[k][1].record(main)
         free[k % nbuf].record(main)
         if k + nbuf < len(units):
             gen_x(k + nbuf)
@@ -199,6 +210,10 @@ def run_rank(units: list[Unit], device: int, tokens: int = TOKENS, bits: int = 4
         dev.set_async(False, device)
     if timing:
         stats["ms"] = t0.elapsed_time(t1)
+        # W synthesis + Hessian + factorisation + sweeps + pack per unit (the
+        # X generation, which stands in for the model forward, is the rest)
+        stats["quant_ms"] = sum(a.elapsed_time(b) for a, b in ev)
+        stats["gen_ms"] = stats["ms"] - stats["quant_ms"] if not overlap else None
     return payloads, stats
 
 
