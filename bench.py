@@ -234,23 +234,24 @@ def run_model_mode(args):
         if not walls:
             clocks.start()
         payloads, stats = MS.run_rank(mine, local, keep_payload=True)
-        ms = torch.tensor([stats["ms"]], device=device)
+        ms = torch.tensor([stats["ms"], stats["quant_ms"]], device=device)
         if world > 1:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        walls.append(float(ms.item()))
+        walls.append((float(ms[0].item()), float(ms[1].item())))
         del payloads
     ck = clocks.stop()
     launches = dev.launch_count() - l0
     total_w = sum(u.n * m for u in units for _, m in u.linears)
     loads = [sum(MS.unit_cost(u) for u in p) for p in plan]
     if rank == 0:
-        wall = statistics.mean(walls)
+        wall = statistics.mean(w for w, _ in walls)
+        qwall = statistics.mean(q for _, q in walls)
         line = {
             "metric": "C4 whole-model sweep throughput (weights/s), 32 x 7 Llama-2-7B linears W4 g128",
-            "value": total_w / (wall / 1e3), "unit": "weights/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall,
-            "wall_clock_s": wall / 1e3,
-            "quantize_wall_clock_s": (stats or {}).get("quant_ms", 0) / 1e3,
+            "value": total_w / (qwall / 1e3), "unit": "weights/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": qwall,
+            "quantize_wall_clock_s": qwall / 1e3,
+            "wall_clock_s_with_input_generation": wall / 1e3,
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16 (Hessian); fp32 factor/sweep", "data": "synthetic",
             "config": {"workload": f"C4: {args.blocks} blocks x 7 linears (q/k/v/o 4096x4096, gate/up "
