@@ -27,7 +27,9 @@
 // (8 warps x 4); lane = cc + 4*rg keeps rows rg, rg+8, ... of its column in
 // registers, rotating by one slot per 8-row group; D is broadcast with one
 // warp shuffle and staged for a coalesced K-major store.
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include <type_traits>
 
@@ -732,6 +734,23 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
     const char* e = getenv("OCWG_SWEEP_PDL");
     return !(e && e[0] == '0');
   }();
+  // OCWG_SWEEP_EVENTS=1 (debug): an event after every launch, per-launch times
+  // printed to stderr at the end (events between launches disable PDL overlap)
+  static const bool ev_on = [] {
+    const char* e = getenv("OCWG_SWEEP_EVENTS");
+    return e && e[0] == '1';
+  }();
+  std::vector<cudaEvent_t> tl;
+  std::vector<char> tl_kind;
+  auto mark = [&](char kind) {
+    if (!ev_on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tl.push_back(e);
+    tl_kind.push_back(kind);
+  };
+  mark('s');
   for (long long s0 = 0, si = 0; s0 < n; s0 += SBK, ++si) {
     const long long se = std::min(n, s0 + SBK);
     const int p = int(si & 1);
@@ -757,6 +776,7 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
       else
         launch_inblock<T, 16>(w, ldw, order, acc, use_acc, gpl, dpl[p], bprev, dcur, dch, dcl, c,
                               scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, kSuperRows, st);
+      mark('i');
     }
     // trailing update of this super-block: acc[se:, :] (+)= G[se:, s0:se] D[s0:se, :]
     if (se < n) {
@@ -786,7 +806,20 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
       if (!done)
         gemm<T, T, T>(n - se, m, kk, 1.0, gpl + se * n + s0, n, false, dpl[p], kSuperRows, true,
                       beta, acc + se * m, m, false, st);
+      mark('g');
     }
+  }
+  if (ev_on) {
+    cudaEventSynchronize(tl.back());
+    float tot = 0.f;
+    for (size_t i = 1; i < tl.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tl[i - 1], tl[i]);
+      tot += ms;
+      fprintf(stderr, "sweep-ev %c %zu %.2f us\n", tl_kind[i], i, ms * 1e3f);
+    }
+    fprintf(stderr, "sweep-ev total %.2f us\n", tot * 1e3f);
+    for (cudaEvent_t e : tl) cudaEventDestroy(e);
   }
 }
 
