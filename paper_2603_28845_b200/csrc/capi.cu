@@ -299,9 +299,10 @@ struct GptqBufs {
   float* gtt;  // n x 128 fp32: diagonal blocks of G^T in in-block lane order
   int* flags;  // Cholesky tile flags
   void* acc;   // n x m  T: sweep partial sums
-  void* dpl[2];   // D (m x 128 T), by block parity
-  float* dhi[2];  // D tf32 hi / lo (split only)
+  void* dpl[2];   // D, K-major: split -- dpl[0] m x n (every row); else m x 512 by parity
+  float* dhi[2];  // D tf32 hi / lo (split only: [0] m x n)
   float* dlo[2];
+  int* kflag;     // split-K tile flags of the left-looking sweep GEMMs (split only)
   float* tcws;
   size_t tcws_floats;
 };
@@ -335,10 +336,11 @@ void gptq_reserve(Arena& ar, const ocwg_ctx* ctx, uint64_t n, uint64_t m, size_t
   o[4] = ar.reserve(split ? 2 * n * n * 4 : 0);
   o[5] = ar.reserve(cholesky_flag_ints((long long)n) * sizeof(int));
   o[6] = ar.reserve(n * std::max<uint64_t>(m, 1) * es);
-  o[7] = ar.reserve(2 * de * es);
-  o[8] = ar.reserve(split ? 4 * de * 4 : 0);
+  o[7] = ar.reserve(split ? n * m * 4 : 2 * de * es);
+  o[8] = ar.reserve(split ? 2 * n * m * 4 : 0);
   o[9] = ar.reserve(tc_ws_floats(n) * sizeof(float));
   o[10] = ar.reserve(split ? n * 128 * 4 + 1024 : 0);
+  o[11] = ar.reserve(split ? sweep_kflag_ints((long long)n, (long long)m) * sizeof(int) : 0);
 }
 GptqBufs gptq_bufs(const Arena& ar, const ocwg_ctx* ctx, const size_t* o, uint64_t n, uint64_t m) {
   const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
@@ -354,11 +356,11 @@ GptqBufs gptq_bufs(const Arena& ar, const ocwg_ctx* ctx, const size_t* o, uint64
   b.flags = ar.at<int>(o[5]);
   b.acc = ar.at<void>(o[6]);
   b.dpl[0] = ar.at<char>(o[7]);
-  b.dpl[1] = ar.at<char>(o[7]) + de * es;
-  for (int k = 0; k < 2; ++k) {
-    b.dhi[k] = split ? ar.at<float>(o[8]) + (2 * k) * de : nullptr;
-    b.dlo[k] = split ? ar.at<float>(o[8]) + (2 * k + 1) * de : nullptr;
-  }
+  b.dpl[1] = split ? nullptr : ar.at<char>(o[7]) + de * es;
+  b.dhi[0] = split ? ar.at<float>(o[8]) : nullptr;
+  b.dlo[0] = split ? ar.at<float>(o[8]) + n * m : nullptr;
+  b.dhi[1] = b.dlo[1] = nullptr;
+  b.kflag = split ? ar.at<int>(o[11]) : nullptr;
   b.tcws = ar.at<float>(o[9]);
   b.tcws_floats = tc_ws_floats(n);
   b.gtt = split ? ar.at<float>(o[10]) : nullptr;
@@ -402,7 +404,7 @@ void run_sweep_t(ocwg_ctx* ctx, const float* w, uint64_t ldw, uint64_t n, uint64
   gptq_sweep_g<T>(w, (long long)ldw, (long long)n, (long long)m, static_cast<const T*>(b.gpl),
                   b.gtt, static_cast<const T*>(b.ghi), b.glo, b.order, c, scales, zeros,
                   (long long)opts->block_cols, codes, w_hat, (long long)ldw, static_cast<T*>(b.acc),
-                  dp, dh, dl, ctx->stream, ctx->aux, ctx->sev);
+                  dp, dh, dl, b.kflag, ctx->stream);
 }
 
 // gptq_quantize on device buffers (w row stride ldw; codes/w_hat stride ldw)
@@ -1091,7 +1093,7 @@ int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, do
     const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
     const uint64_t nblk = (n + 63) / 64;
     Arena ar(ctx);
-    size_t o[11];
+    size_t o[12];
     gptq_reserve(ar, ctx, n, 1, o);
     const size_t oh = ar.reserve(n * n * 4), ohi = ar.reserve(n * n * 8),
                  ou64 = ar.reserve(n * n * 8), ou = ar.reserve(n * n * es),
@@ -1134,7 +1136,7 @@ int ocwg_gptq_quantize_dev(ocwg_ctx* ctx, const float* w, uint64_t ldw, const fl
     std::lock_guard<std::mutex> lk(ctx->mu);
     begin(ctx, true);
     Arena ar(ctx);
-    size_t o[11];
+    size_t o[12];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     ar.commit();
@@ -1216,7 +1218,7 @@ int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, const
     const uint64_t ng = group_count(cfg, n, m);
     const QCfg c = qcfg(cfg, m);
     Arena ar(ctx);
-    size_t o[11];
+    size_t o[12];
     if (method == 1) gptq_reserve(ar, ctx, n, m, o);
     const size_t ow = ar.reserve(n * m * 4), og = ar.reserve(n * n * 8),
                  oc = ar.reserve(corr ? n * n * 8 : 8), oh = ar.reserve(method == 1 ? n * n * 4 : 4),
@@ -1318,7 +1320,7 @@ int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, 
     begin(ctx, true);
     const uint64_t ng = group_count(cfg, n, m);
     Arena ar(ctx);
-    size_t o[11];
+    size_t o[12];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const size_t oh = ar.reserve(n * n * 4);
@@ -1386,7 +1388,7 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
     float* hd = reinterpret_cast<float*>(io + oh);
     // ---- workspace
     Arena ar(ctx);
-    size_t o[11];
+    size_t o[12];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const long long chunk = 32768;  // tokens per H2D chunk (a multiple of the 16384 split)
@@ -1464,7 +1466,7 @@ int ocwg_quantize_layers_x_dev(ocwg_ctx* ctx, int count, const float* const* w, 
     begin(ctx, true);
     cudaStream_t st = ctx->stream;
     Arena ar(ctx);
-    size_t o[11];
+    size_t o[12];
     gptq_reserve(ar, ctx, n, mmax, o);
     const size_t om = ar.reserve(4096 * 4), oh = ar.reserve(n * n * 4);
     const size_t hws = gram_tc_workspace_bytes((long long)n);
@@ -1538,7 +1540,7 @@ int ocwg_quantize_layers_x(ocwg_ctx* ctx, int count, const float* const* w, cons
     uint8_t* pd = reinterpret_cast<uint8_t*>(io + opl);
     float* hd = reinterpret_cast<float*>(io + oh);
     Arena ar(ctx);
-    size_t o[11];
+    size_t o[12];
     gptq_reserve(ar, ctx, n, mmax, o);
     const size_t om = ar.reserve(4096 * 4);
     const long long chunk = 32768;

@@ -112,7 +112,10 @@ bool tc_gemm_presplit(long long m, long long n, long long k, float alpha, const 
 bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const float* a_hi,
                        const float* a_lo, long long lda, const float* b_hi, const float* b_lo,
                        long long ldb, float beta, float* c, long long ldc, cudaStream_t st,
-                       bool pdl = false);
+                       bool pdl = false, int ksplit = 1, int* kflag = nullptr, int epoch = 0);
+// (ksplit = 2: two K halves per tile on different pairs, the second adding to
+// the first's store; kflag: 2 ints per 256 x 256 tile, never equal to a fresh
+// epoch before the launch)
 // pdl: launched as a programmatic dependent of the previous kernel on st (the
 // kernel's setup overlaps that kernel's tail; its loads wait in griddepcontrol)
 // Dispatch: T = float -> tcgen05 3xTF32 (when a workspace is set and the
@@ -137,7 +140,10 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
                   const float* gtt, const T* ghi, const float* glo, const int32_t* order, const QCfg& c,
                   const float* scales, const int32_t* zeros, long long block, int16_t* codes,
                   float* w_hat, long long ldo, T* acc, T* const dpl[2], float* const dhi[2],
-                  float* const dlo[2], cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev);
+                  float* const dlo[2], int* kflag, cudaStream_t st);
+// fp32 pre-split path (kflag != null): left-looking sweep, D of every row kept:
+// dpl[0] / dhi[0] / dlo[0] are m x n K-major (ld n); kflag: sweep_kflag_ints.
+size_t sweep_kflag_ints(long long n, long long m);
 
 // ---- statistics (gram_tc.cu, stats.cu) ------------------------------------
 // Tensor-core statistics: gram (+)= sum_s ops[gA[s]]^T ops[gB[s]] (symmetric

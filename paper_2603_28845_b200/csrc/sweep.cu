@@ -694,6 +694,9 @@ void launch_inblock(const float* w, long long ldw, const int32_t* order, const T
 constexpr long long kSuperRows = 512;  // rows of G D applied per trailing GEMM (K)
 
 size_t sweep_delta_elems(long long m) { return size_t(m) * kSuperRows; }
+size_t sweep_kflag_ints(long long n, long long m) {
+  return size_t(2 * ((kSuperRows + 255) / 256) * ((m + 255) / 256)) + 8;
+}
 
 // Two-level blocking: super-blocks of kSuperRows rows (4 blocks of 128).
 // In-block kernel b applies, by lookahead, every earlier block of its own
@@ -706,10 +709,7 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
                   const float* gtt, const T* ghi, const float* glo, const int32_t* order,
                   const QCfg& c, const float* scales, const int32_t* zeros, long long block,
                   int16_t* codes, float* w_hat, long long ldo, T* acc, T* const dpl[2],
-                  float* const dhi[2], float* const dlo[2], cudaStream_t st, cudaStream_t aux,
-                  cudaEvent_t* ev) {
-  (void)aux;
-  (void)ev;
+                  float* const dhi[2], float* const dlo[2], int* kflag, cudaStream_t st) {
   // Block size is a pure re-association of the trailing update (SURVEY §0
   // item 11): the fp32 path always runs the tuned 128-row kernel (so the
   // reference default block_cols = 32, layerwise.hpp:14, is fast too); the
@@ -750,7 +750,62 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
     tl.push_back(e);
     tl_kind.push_back(kind);
   };
+  auto report = [&] {
+    if (!ev_on) return;
+    cudaEventSynchronize(tl.back());
+    float tot = 0.f;
+    for (size_t i = 1; i < tl.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tl[i - 1], tl[i]);
+      tot += ms;
+      fprintf(stderr, "sweep-ev %c %zu %.2f us\n", tl_kind[i], i, ms * 1e3f);
+    }
+    fprintf(stderr, "sweep-ev total %.2f us\n", tot * 1e3f);
+    for (cudaEvent_t e : tl) cudaEventDestroy(e);
+  };
   mark('s');
+  if constexpr (sizeof(T) == 4) {
+    if (fast128 && split && kflag) {
+      // Left-looking: before super-block s, ONE GEMM forms its rows' sum over
+      // every earlier row, acc[s0:se, :] = G[s0:se, 0:s0] D[0:s0, :] (K = s0,
+      // written once: no read-modify-write of the later rows' partial sums),
+      // on 2-SM pairs with the K range split in two so 2 x 16 tiles fill the
+      // GPU.  D of every row is kept (K-major, ld n: plain for the lookahead,
+      // tf32 hi / lo for the GEMM).
+      cudaMemsetAsync(kflag, 0, sweep_kflag_ints(n, m) * sizeof(int), st);
+      for (long long s0 = 0, si = 0; s0 < n; s0 += SBK, ++si) {
+        const long long se = std::min(n, s0 + SBK);
+        if (si > 0) {
+          bool done = tc_gemm2_presplit(se - s0, m, s0, 1.0f,
+                                        reinterpret_cast<const float*>(ghi) + s0 * n,
+                                        glo + s0 * n, n, dhi[0], dlo[0], n, 0.0f,
+                                        reinterpret_cast<float*>(acc) + s0 * m, m, st, pdl_on, 2,
+                                        kflag, int(si));
+          if (!done)
+            done = tc_gemm_presplit(se - s0, m, s0, 1.0f,
+                                    reinterpret_cast<const float*>(ghi) + s0 * n, glo + s0 * n, n,
+                                    dhi[0], dlo[0], n, 0.0f,
+                                    reinterpret_cast<float*>(acc) + s0 * m, m, st, 0, pdl_on);
+          if (!done)
+            gemm<T, T, T>(se - s0, m, s0, 1.0, gpl + s0 * n, n, false, dpl[0], n, true, 0.0,
+                          acc + s0 * m, m, false, st);
+          mark('g');
+        }
+        for (long long ib = s0; ib < se; ib += B) {
+          const int bsz = int(std::min(se, ib + B) - ib);
+          launch_inblock4(w, ldw, order, reinterpret_cast<const float*>(acc), si >= 1,
+                          reinterpret_cast<const float*>(gpl), gtt,
+                          reinterpret_cast<const float*>(dpl[0]) + s0, int(ib - s0),
+                          reinterpret_cast<float*>(dpl[0]) + ib, dhi[0] + ib, dlo[0] + ib, c,
+                          scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, n, ib == trace_ib,
+                          pdl_on && ib > 0, st);
+          mark('i');
+        }
+      }
+      report();
+      return;
+    }
+  }
   for (long long s0 = 0, si = 0; s0 < n; s0 += SBK, ++si) {
     const long long se = std::min(n, s0 + SBK);
     const int p = int(si & 1);
@@ -809,18 +864,7 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
       mark('g');
     }
   }
-  if (ev_on) {
-    cudaEventSynchronize(tl.back());
-    float tot = 0.f;
-    for (size_t i = 1; i < tl.size(); ++i) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, tl[i - 1], tl[i]);
-      tot += ms;
-      fprintf(stderr, "sweep-ev %c %zu %.2f us\n", tl_kind[i], i, ms * 1e3f);
-    }
-    fprintf(stderr, "sweep-ev total %.2f us\n", tot * 1e3f);
-    for (cudaEvent_t e : tl) cudaEventDestroy(e);
-  }
+  report();
 }
 
 int debug_sweep_trace(unsigned long long* out, int cap) {
@@ -834,11 +878,11 @@ template void gptq_sweep_g<float>(const float*, long long, long long, long long,
                                   const float*, const float*, const float*, const int32_t*, const QCfg&,
                                   const float*, const int32_t*, long long, int16_t*, float*,
                                   long long, float*, float* const[2], float* const[2],
-                                  float* const[2], cudaStream_t, cudaStream_t, cudaEvent_t*);
+                                  float* const[2], int*, cudaStream_t);
 template void gptq_sweep_g<double>(const float*, long long, long long, long long, const double*,
                                    const float*, const double*, const float*, const int32_t*, const QCfg&,
                                    const float*, const int32_t*, long long, int16_t*, float*,
                                    long long, double*, double* const[2], float* const[2],
-                                   float* const[2], cudaStream_t, cudaStream_t, cudaEvent_t*);
+                                   float* const[2], int*, cudaStream_t);
 
 }  // namespace ocwg

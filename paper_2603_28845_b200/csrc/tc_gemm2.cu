@@ -85,6 +85,14 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
       : "memory");
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -123,7 +131,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap ahi, const __grid_constant__ CUtensorMap alo,
                     const __grid_constant__ CUtensorMap bhi, const __grid_constant__ CUtensorMap blo,
                     long long m, long long n, long long k, float alpha, float beta,
-                    float* __restrict__ c, long long ldc, int tiles_n, int ntiles) {
+                    float* __restrict__ c, long long ldc, int tiles_n, int ntiles, int ksplit,
+                    int* __restrict__ kflag, int epoch) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
@@ -134,6 +143,18 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t rank = cta_rank();
   const int pair = int(blockIdx.x >> 1), npairs = int(gridDim.x >> 1);
   const int kb_total = int((k + TK - 1) / TK);
+  // units: (tile, K part), part-major; part q of a tile covers k-blocks
+  // [kb_total q / ksplit, kb_total (q+1) / ksplit).  With ksplit = 2 the second
+  // part adds into C after the first part's store (per-(tile, CTA) flag set to
+  // `epoch`): deterministic, no zero-fill.  A part-1 unit is assigned after its
+  // part-0 unit (round-robin over resident pairs), so it never waits on a unit
+  // that has not started.
+  const int nunits = ntiles * ksplit;
+  auto kb_range = [&](int t, int& kb0, int& kb1) {
+    const int q = t / ntiles;
+    kb0 = int((long long)kb_total * q / ksplit);
+    kb1 = int((long long)kb_total * (q + 1) / ksplit);
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -166,10 +187,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ====================== TMA producer (both CTAs, own halves) ======================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (int t = pair; t < ntiles; t += npairs) {
-        const int tm = t / tiles_n, tn = t % tiles_n;
+      for (int t = pair; t < nunits; t += npairs) {
+        const int tile = t % ntiles, tm = tile / tiles_n, tn = tile % tiles_n;
         const int arow = tm * 256 + int(rank) * TM, brow = tn * 256 + int(rank) * TNH;
-        for (int kb = 0; kb < kb_total; ++kb) {
+        int kb0, kb1;
+        kb_range(t, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1u);
           const uint32_t fb = smem_u32(&full_bar[stage]);
           if (rank == 0) mbar_expect_tx(fb, 2 * STAGE_BYTES);
@@ -192,12 +215,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (rank == 0) {
       uint32_t stage = 0, phase = 0;
       int local = 0;
-      for (int t = pair; t < ntiles; t += npairs, ++local) {
+      for (int t = pair; t < nunits; t += npairs, ++local) {
         const uint32_t acc = uint32_t(local & 1), use = uint32_t(local >> 1);
+        int kb0, kb1;
+        kb_range(t, kb0, kb1);
         mbar_wait(smem_u32(&tempty_bar[acc]), (use & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
-        for (int kb = 0; kb < kb_total; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(smem_u32(&full_bar[stage]), phase);
           tc_fence_after();
           if (lane == 0) {
@@ -206,12 +231,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int kk = 0; kk < TK / 8; ++kk) {
               const uint64_t ah = kdesc(s0, kk), al = kdesc(s0 + OPB, kk);
               const uint64_t bh = kdesc(s0 + 2 * OPB, kk), bl = kdesc(s0 + 3 * OPB, kk);
-              tc_mma_pair_tf32(d_tmem, al, bh, (kb > 0 || kk > 0) ? 1u : 0u);  // small terms first
+              tc_mma_pair_tf32(d_tmem, al, bh, (kb > kb0 || kk > 0) ? 1u : 0u);  // small terms first
               tc_mma_pair_tf32(d_tmem, ah, bl, 1u);
               tc_mma_pair_tf32(d_tmem, ah, bh, 1u);
             }
             tc_commit_pair(smem_u32(&empty_bar[stage]));
-            if (kb + 1 == kb_total) tc_commit_pair(smem_u32(&tfull_bar[acc]));
+            if (kb + 1 == kb1) tc_commit_pair(smem_u32(&tfull_bar[acc]));
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -227,15 +252,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3, cbeg = ((warp - 2) >> 2) * 128;
     const bool vec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(c) & 15) == 0;
     int local = 0;
-    for (int t = pair; t < ntiles; t += npairs, ++local) {
-      const int tm = t / tiles_n, tn = t % tiles_n;
+    for (int t = pair; t < nunits; t += npairs, ++local) {
+      const int tile = t % ntiles, tm = tile / tiles_n, tn = tile % tiles_n;
+      const int part = t / ntiles;
       const uint32_t acc = uint32_t(local & 1), use = uint32_t(local >> 1);
       const long long row = (long long)tm * 256 + rank * TM + q * 32 + lane;
       float* crow_base = c + row * ldc + (long long)tn * 256;
+      int* flag = kflag + tile * 2 + int(rank);
+      const float bt = part == 0 ? beta : 1.f;  // later parts add to the first
+      if (part > 0) {  // the first part of this tile has stored its rows
+        if (warp == 2 && lane == 0)
+          while (ld_acquire_gpu(flag) != epoch) __nanosleep(64);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
       auto load_c = [&](int c0, float (&v)[32]) {
         const long long col0 = (long long)tn * 256 + c0;
         const float* cr = crow_base + c0;
-        if (beta == 0.f || row >= m) {
+        if (bt == 0.f || row >= m) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = 0.f;
         } else if (vec && col0 + 32 <= n) {
@@ -275,7 +308,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (row < m) {
           float* cr = crow_base + c0;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) cv[e] = fmaf(alpha, __uint_as_float(r[e]), beta * cv[e]);
+          for (int e = 0; e < 32; ++e) cv[e] = fmaf(alpha, __uint_as_float(r[e]), bt * cv[e]);
           if (vec && col0 + 32 <= n) {
 #pragma unroll
             for (int e = 0; e < 8; ++e)
@@ -289,6 +322,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       tc_fence_before();
+      if (ksplit > 1 && part == 0) {  // publish this CTA's rows of the tile
+        __threadfence();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (warp == 2 && lane == 0) st_release_gpu(flag, epoch);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tempty_bar[acc]), 0));
     }
@@ -340,7 +378,7 @@ int num_sms3() { return device_sms(); }
 bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const float* a_hi,
                        const float* a_lo, long long lda, const float* b_hi, const float* b_lo,
                        long long ldb, float beta, float* c, long long ldc, cudaStream_t st,
-                       bool pdl) {
+                       bool pdl, int ksplit, int* kflag, int epoch) {
   if (m <= 0 || n <= 0) return true;
   if (!encoder3() || k <= 0 || m >= (1LL << 31) || n >= (1LL << 31)) return false;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -353,7 +391,11 @@ bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const
   cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   const int tiles_m = int((m + 255) / 256), tiles_n = int((n + 255) / 256);
   const int ntiles = tiles_m * tiles_n;
-  const int npairs = std::min(ntiles, num_sms3() / 2);
+  const long long kb_total = (k + TK - 1) / TK;
+  if (ksplit < 1 || !kflag) ksplit = 1;
+  ksplit = int(std::min<long long>({(long long)ksplit, 2LL, kb_total}));
+  const int nunits = ntiles * ksplit;
+  int npairs = std::min(nunits, num_sms3() / 2);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(2 * npairs));
   cfg.blockDim = dim3(THREADS);
@@ -368,9 +410,19 @@ bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 2 : 1;
+  if (ksplit > 1) {  // part-1 units wait on part-0 units: every pair must be resident
+    int max_clusters = 0;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, tc_gemm2_kernel, &cfg) == cudaSuccess &&
+        max_clusters >= 1)
+      npairs = std::min(npairs, max_clusters);
+    cudaGetLastError();
+    cfg.gridDim = dim3(unsigned(2 * npairs));
+    cfg.numAttrs = pdl ? 2 : 1;
+  }
   count_launches(1);
   return cudaLaunchKernelEx(&cfg, tc_gemm2_kernel, mah, mal, mbh, mbl, m, n, k, alpha, beta, c,
-                            ldc, tiles_n, ntiles) == cudaSuccess;
+                            ldc, tiles_n, ntiles, ksplit, kflag, epoch) == cudaSuccess;
 }
 
 }  // namespace ocwg
