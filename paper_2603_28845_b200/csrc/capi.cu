@@ -303,6 +303,8 @@ struct GptqBufs {
   float* dhi[2];  // D tf32 hi / lo (split only: [0] m x n)
   float* dlo[2];
   int* kflag;     // split-K tile flags of the left-looking sweep GEMMs (split only)
+  float* lhi;     // n x n: tf32 hi / lo split of L (split only; the Cholesky's tcgen05 products)
+  float* llo;
   float* tcws;
   size_t tcws_floats;
 };
@@ -341,6 +343,7 @@ void gptq_reserve(Arena& ar, const ocwg_ctx* ctx, uint64_t n, uint64_t m, size_t
   o[9] = ar.reserve(tc_ws_floats(n) * sizeof(float));
   o[10] = ar.reserve(split ? n * 128 * 4 + 1024 : 0);
   o[11] = ar.reserve(split ? sweep_kflag_ints((long long)n, (long long)m) * sizeof(int) : 0);
+  o[12] = ar.reserve(split ? 2 * n * n * 4 : 0);
 }
 GptqBufs gptq_bufs(const Arena& ar, const ocwg_ctx* ctx, const size_t* o, uint64_t n, uint64_t m) {
   const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
@@ -361,6 +364,8 @@ GptqBufs gptq_bufs(const Arena& ar, const ocwg_ctx* ctx, const size_t* o, uint64
   b.dlo[0] = split ? ar.at<float>(o[8]) + n * m : nullptr;
   b.dhi[1] = b.dlo[1] = nullptr;
   b.kflag = split ? ar.at<int>(o[11]) : nullptr;
+  b.lhi = split ? ar.at<float>(o[12]) : nullptr;
+  b.llo = split ? ar.at<float>(o[12]) + n * n : nullptr;
   b.tcws = ar.at<float>(o[9]);
   b.tcws_floats = tc_ws_floats(n);
   b.gtt = split ? ar.at<float>(o[10]) : nullptr;
@@ -378,7 +383,7 @@ void run_factor_t(ocwg_ctx* ctx, const float* h_dev, uint64_t n, int actorder, d
   if (ctx->profile) cudaEventRecord(ctx->ev[1], st);
   cholesky_g<T>(static_cast<T*>(b.a), (long long)n, static_cast<T*>(b.ghi), b.glo,
                 b.glo ? static_cast<float*>(b.gpl) : nullptr, b.gtt, b.flags, ctx->flag,
-                chol_macro_cols(n), st);
+                chol_macro_cols(n), st, b.lhi, b.llo);
   if (ctx->profile) {
     cudaEventRecord(ctx->ev[2], st);
     cudaEventRecord(ctx->ev[3], st);  // (no triangular inverse on the hot path)
@@ -1093,7 +1098,7 @@ int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, do
     const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
     const uint64_t nblk = (n + 63) / 64;
     Arena ar(ctx);
-    size_t o[12];
+    size_t o[13];
     gptq_reserve(ar, ctx, n, 1, o);
     const size_t oh = ar.reserve(n * n * 4), ohi = ar.reserve(n * n * 8),
                  ou64 = ar.reserve(n * n * 8), ou = ar.reserve(n * n * es),
@@ -1136,7 +1141,7 @@ int ocwg_gptq_quantize_dev(ocwg_ctx* ctx, const float* w, uint64_t ldw, const fl
     std::lock_guard<std::mutex> lk(ctx->mu);
     begin(ctx, true);
     Arena ar(ctx);
-    size_t o[12];
+    size_t o[13];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     ar.commit();
@@ -1218,7 +1223,7 @@ int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, const
     const uint64_t ng = group_count(cfg, n, m);
     const QCfg c = qcfg(cfg, m);
     Arena ar(ctx);
-    size_t o[12];
+    size_t o[13];
     if (method == 1) gptq_reserve(ar, ctx, n, m, o);
     const size_t ow = ar.reserve(n * m * 4), og = ar.reserve(n * n * 8),
                  oc = ar.reserve(corr ? n * n * 8 : 8), oh = ar.reserve(method == 1 ? n * n * 4 : 4),
@@ -1320,7 +1325,7 @@ int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, 
     begin(ctx, true);
     const uint64_t ng = group_count(cfg, n, m);
     Arena ar(ctx);
-    size_t o[12];
+    size_t o[13];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const size_t oh = ar.reserve(n * n * 4);
@@ -1388,7 +1393,7 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
     float* hd = reinterpret_cast<float*>(io + oh);
     // ---- workspace
     Arena ar(ctx);
-    size_t o[12];
+    size_t o[13];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const long long chunk = 32768;  // tokens per H2D chunk (a multiple of the 16384 split)
@@ -1466,7 +1471,7 @@ int ocwg_quantize_layers_x_dev(ocwg_ctx* ctx, int count, const float* const* w, 
     begin(ctx, true);
     cudaStream_t st = ctx->stream;
     Arena ar(ctx);
-    size_t o[12];
+    size_t o[13];
     gptq_reserve(ar, ctx, n, mmax, o);
     const size_t om = ar.reserve(4096 * 4), oh = ar.reserve(n * n * 4);
     const size_t hws = gram_tc_workspace_bytes((long long)n);
@@ -1540,7 +1545,7 @@ int ocwg_quantize_layers_x(ocwg_ctx* ctx, int count, const float* const* w, cons
     uint8_t* pd = reinterpret_cast<uint8_t*>(io + opl);
     float* hd = reinterpret_cast<float*>(io + oh);
     Arena ar(ctx);
-    size_t o[12];
+    size_t o[13];
     gptq_reserve(ar, ctx, n, mmax, o);
     const size_t om = ar.reserve(4096 * 4);
     const long long chunk = 32768;

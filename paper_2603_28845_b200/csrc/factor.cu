@@ -28,10 +28,13 @@
 // earlier items, so with every CTA resident the schedule cannot deadlock.
 // Large n runs macro panels: the kernel over a column range, then one tcgen05
 // 3xTF32 SYRK for the trailing matrix (gemm.cu / tc_gemm.cu).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+
+#include <cuda.h>
 
 #include "kernels.h"
 
@@ -128,6 +131,10 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_1_n() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // Raw copy of a 64 x 64 tile (rows x cols valid, row stride n) into dst
 // (row-major, ld 64); 16-byte cp.async when aligned, zero outside.
@@ -178,18 +185,20 @@ __device__ __forceinline__ void ld4(const T* p, T (&o)[4]) {
 
 constexpr int LD = TB + 4;  // row stride of the owner's row-major tiles
 
+// Small fields first: the fp32 workers' tcgen05 operand stages (kUmmaOff on)
+// alias the big buffers, which a worker only uses after its k-loop.
 template <typename T>
 struct CholSmem {
-  T ps[TB * LD];      // row-major tiles (ld LD): tile-product operands / staging
-  T qs[TB * LD];
-  T lt[TB][LD];       // workers: L_cc transposed / G staging; owner: X = L_cc^-T
-  T sf[TB][TB + 1];   // diagonal tile being factored
-  T wcol4[4][72];     // factor_tile64: the producer's pivot-column ring (shared-pivot elimination)
-  T sb[2][TB * LD];   // owner: staged partial tiles (row-major, ld LD, cp.async)
-  T rdiag[TB];
   int item;
   int ready;
-  int stg[4];  // owner: which tiles the factor's idle warps staged; [3]: product done
+  alignas(16) int stg[4];  // owner: which tiles the factor's idle warps staged; [3]: product done
+  alignas(16) T rdiag[TB];
+  alignas(16) T wcol4[4][72];  // factor_tile64: the producer's pivot-column ring (shared-pivot elimination)
+  alignas(16) T ps[TB * LD];   // row-major tiles (ld LD): tile-product operands / staging
+  alignas(16) T qs[TB * LD];
+  alignas(16) T lt[TB][LD];    // workers: L_cc transposed / G staging; owner: X = L_cc^-T
+  alignas(16) T sf[TB][TB + 1];  // diagonal tile being factored
+  alignas(16) T sb[2][TB * LD];  // owner: staged partial tiles (row-major, ld LD, cp.async)
 };
 
 // Publish the finalised tile (values in t, rows b = 64r + 4ty + u, cols
@@ -431,6 +440,105 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// ---- worker tile products on the 5th-gen tensor cores (fp32 path) ----------
+// acc (TMEM, 128 lanes x 64 fp32 columns; lanes 0-63 used) += L[r,k] L[c,k]^T
+// as 3xTF32 (lo*hi + hi*lo + hi*hi, tcgen05.mma kind::tf32, M = 128, N = 64,
+// K = 8 per instruction).  Every published L tile is also stored pre-split
+// (lhi = tf32 round-to-nearest of L, llo = L - lhi), and a k-step is four
+// 64 x 64 tiles (A hi / lo, B hi / lo) brought in by TMA (SWIZZLE_128B, two
+// 32-column boxes each) into a 3-stage ring: one thread of the CTA produces
+// (tile flags, then TMA), one issues the MMAs, nobody else is involved until
+// the accumulator is read back.  M = 128 costs the same as M = 64 (the
+// instruction floor is M = 128); its upper 64 rows read the next 8 KB of the
+// stage and land in TMEM lanes never read.
+constexpr int kUmmaStage = 65536;  // A hi | A lo | B hi | B lo, 16 KB each
+constexpr int kUmmaStages = 3;
+constexpr int kUmmaOff = 4096;     // past CholSmem's small fields
+constexpr int kUmmaEnd = kUmmaOff + kUmmaStages * kUmmaStage + 1024;
+constexpr uint32_t kUmmaIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(64 >> 3) << 17) |
+                                (uint32_t(128 >> 4) << 24);
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t umma_kdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t(1) << 16;                       // LBO (unused for swizzled K-major)
+  d |= uint64_t((1024u >> 4) & 0x3FFFu) << 32;  // SBO: 8-row atoms at 1 KB
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;                       // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(kUmmaIdesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init1(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_tile(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x,
+                                         int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+// store the tile's tf32 hi / lo split beside L (rows x cols valid)
+__device__ __forceinline__ void store_split(const float (&t)[4][4], float* lhi, float* llo,
+                                            long long off, long long n, int rows, int cols) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int rr = 4 * ty + u;
+    if (rr >= rows) continue;
+    const long long o = off + (long long)rr * n + 4 * tx;
+    if (4 * tx + 4 <= cols) {
+      const float4 h = make_float4(tf32_hi(t[u][0]), tf32_hi(t[u][1]), tf32_hi(t[u][2]),
+                                   tf32_hi(t[u][3]));
+      *reinterpret_cast<float4*>(lhi + o) = h;
+      *reinterpret_cast<float4*>(llo + o) =
+          make_float4(t[u][0] - h.x, t[u][1] - h.y, t[u][2] - h.z, t[u][3] - h.w);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (4 * tx + v < cols) {
+          const float h = tf32_hi(t[u][v]);
+          lhi[o + v] = h;
+          llo[o + v] = t[u][v] - h;
+        }
+    }
+  }
+}
+struct UmmaMaps {
+  CUtensorMap hi, lo;  // lhi / llo: n x n fp32, 32 x 64 boxes, SWIZZLE_128B
+};
+
 template <typename T, bool BT>
 __device__ __forceinline__ void owner_prod(const T* A, const T* B, const T* src, T* D, int ldd,
                                            T sgn, int pad) {
@@ -708,10 +816,11 @@ __device__ __forceinline__ void emit_tile(const T (&t)[4][4], CholSmem<T>& sm, i
 enum ItemKind { kFull = 0, kPartial = 1, kEmit = 2, kOwner = 3 };
 
 template <typename T>
-__global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
+__global__ void __launch_bounds__(CT, 1)
     chol_tile_kernel(T* __restrict__ a, long long n, int nt, int c0, int c1, int* flags,
                      int* pflags, int* counter, unsigned* status, T* ghi, float* glo, float* gpl,
-                     float* gtt, unsigned long long* trace) {
+                     float* gtt, unsigned long long* trace, const __grid_constant__ UmmaMaps maps,
+                     float* lhi, float* llo, int* sflags) {
   extern __shared__ __align__(16) unsigned char smraw[];
   CholSmem<T>& sm = *reinterpret_cast<CholSmem<T>*>(smraw);
   // optional timeline (debug): per entry {r, c + 1000 kind, start, k-loop done,
@@ -777,6 +886,30 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       // L[c+1,c-1] and the next column's S'[c+1,c+1] (sm.stg bits tell which)
       auto side = [&](int half) {
         const int st = tid - 96;  // 0..159
+        if (half == 1 && st < 32 && sub && !sm.stg[2]) {
+          // the next column's S'[c+1,c+1] may land during the first half: warp 3
+          // checks again and stages it under the second half
+          int ready = 0;
+          if (st == 0) ready = ld_acquire(pflags + 2 * (c + 1));
+          ready = __shfl_sync(0xffffffffu, ready, 0);
+          if (ready) {
+            constexpr int V = 16 / sizeof(T);
+            const T* src = a + (c + 1) * tile + (long long)(c + 1) * TB;
+            for (int e = st; e < TB * TB / V; e += 32) {
+              const int rr = e / (TB / V), cc = (e % (TB / V)) * V;
+              T* d = sm.sb[1] + rr * LD + cc;
+              if (vec_ok && rr < rows1 && cc + V <= rows1) {
+                cp_async16(d, src + (long long)rr * n + cc);
+              } else {
+#pragma unroll
+                for (int u = 0; u < V; ++u)
+                  d[u] = (rr < rows1 && cc + u < rows1) ? ldcg(src + (long long)rr * n + cc + u) : T(0);
+              }
+            }
+            __syncwarp();
+            if (st == 0) sm.stg[2] = 1;
+          }
+        }
         if (half == 1) {
           // S[c+1,c] -= L[c+1,c-1] L[c,c-1]^T beside the h = 1 elimination when both
           // tiles were staged (fp32; otherwise it runs after the factor)
@@ -896,12 +1029,53 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
   }
   __syncthreads();
   if (sm.ready) return;
+  // fp32: tensor-memory accumulator (64 columns) and the MMA completion barrier
+  __shared__ __align__(8) unsigned long long full_bar[kUmmaStages], empty_bar[kUmmaStages];
+  __shared__ __align__(8) unsigned long long done_bar;
+  __shared__ uint32_t tmem_holder;
+  uint8_t* ub = nullptr;
+  uint32_t tmem = 0;
+  // ring position (producer / MMA issuer) and accumulator phase, kept across items
+  uint32_t p_stage = 0, p_phase = 0, m_stage = 0, m_phase = 0, d_phase = 0;
+  const bool umma = sizeof(T) == 4 && lhi != nullptr;
+  if (umma) {
+    ub = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + kUmmaOff + 1023) &
+                                    ~uintptr_t(1023));
+    if (tid == 0) {
+      for (int q = 0; q < kUmmaStages; ++q) {
+        mbar_init1(smem_addr(&full_bar[q]));
+        mbar_init1(smem_addr(&empty_bar[q]));
+      }
+      mbar_init1(smem_addr(&done_bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.hi)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.lo)) : "memory");
+    }
+    if (tid < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+                       smem_addr(&tmem_holder))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tmem = tmem_holder;
+  }
   while (true) {
     if (tid == 0) sm.item = atomicAdd(counter, 1);
     __syncthreads();
     long long idx = sm.item;
     __syncthreads();
-    if (idx >= total) break;
+    if (idx >= total) {
+      if (umma) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (tid < 32)
+          asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem)
+                       : "memory");
+      }
+      break;
+    }
     const long long item_id = idx;
     int c = c0;
     while (idx >= nt - c + 1) {
@@ -929,6 +1103,15 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
         if (tid == 0) wait_flag(flags + (c + q) * nt + c);
         __syncthreads();
         load_t(t, a + (c + q) * tile + (long long)c * TB, n, rq, TB, false, vec_ok);
+        if constexpr (sizeof(T) == 4) {
+          if (umma) {  // the owner's sub tile, pre-split for the k-loops (off its chain)
+            store_split(t, lhi, llo, (c + q) * tile + (long long)c * TB, n, rq, TB);
+            __threadfence();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) st_release(sflags + (c + q) * nt + c, 1);
+          }
+        }
         emit_tile(t, sm, c + q, c, n, ghi, glo, gpl, gtt);
       }
       stamp(item_id, 5);
@@ -943,62 +1126,160 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
     const int rows = int(std::min<long long>(TB, n - (long long)r * TB));
     const int kend = partial ? c - 1 : c;  // partial items leave k = c-1 to the owner
 
-    // ---- S = A[r,c] - sum_k L[r,k] L[c,k]^T: row-major tiles staged by cp.async
-    // (double-buffered while the next k is already published), tensor-core products
-    TileAcc<T> acc;
-    acc_zero(acc);
-    T* const Pb[2] = {sm.ps, sm.sb[0]};
-    T* const Qb[2] = {sm.qs, sm.sb[1]};
-    if (c0 < kend) {
-      if (tid == 0) {
-        wait_flag(flags + r * nt + c0);
-        wait_flag(flags + c * nt + c0);
+    // ---- S = A[r,c] - sum_k L[r,k] L[c,k]^T over the published k (double-
+    // buffered staging while the next k is already published)
+    if (umma) {
+      const int warp = tid >> 5, lane = tid & 31;
+      if (c0 < kend) {
+        if (warp == 0) {  // ---- producer: tile flags, then four TMA tiles per k
+          int horizon = c0;  // every k < horizon is published (rows r and c)
+          for (int k = c0; k < kend; ++k) {
+            while (horizon <= k) {  // the warp probes the next 32 k of both rows
+              const int kk = k + lane;
+              const bool ok = kk >= kend || (ld_acquire(sflags + r * nt + kk) != 0 &&
+                                             ld_acquire(sflags + c * nt + kk) != 0);
+              const unsigned bal = __ballot_sync(0xffffffffu, ok);
+              const int run = ~bal ? __ffs(~bal) - 1 : 32;
+              horizon = k + run;
+              if (run == 0) __nanosleep(40);
+            }
+            if (lane == 0) {
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              mbar_wait_parity(smem_addr(&empty_bar[p_stage]), p_phase ^ 1u);
+              const uint32_t fb = smem_addr(&full_bar[p_stage]);
+              mbar_expect(fb, kUmmaStage);
+              const uint32_t s0 = smem_addr(ub) + p_stage * kUmmaStage;
+              const int x0 = k * TB, ya = r * TB, yb = c * TB;
+#pragma unroll
+              for (int ch = 0; ch < 2; ++ch) {
+                tma_tile(s0 + ch * 8192, &maps.hi, fb, x0 + 32 * ch, ya);
+                tma_tile(s0 + 16384 + ch * 8192, &maps.lo, fb, x0 + 32 * ch, ya);
+                tma_tile(s0 + 32768 + ch * 8192, &maps.hi, fb, x0 + 32 * ch, yb);
+                tma_tile(s0 + 49152 + ch * 8192, &maps.lo, fb, x0 + 32 * ch, yb);
+              }
+              if (++p_stage == kUmmaStages) {
+                p_stage = 0;
+                p_phase ^= 1u;
+              }
+            }
+            __syncwarp();
+          }
+        } else if (warp == 1) {  // ---- MMA issuer
+          if (lane == 0) {
+            for (int k = c0; k < kend; ++k) {
+              mbar_wait_parity(smem_addr(&full_bar[m_stage]), m_phase);
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+              const uint32_t s0 = smem_addr(ub) + m_stage * kUmmaStage;
+#pragma unroll
+              for (int ch = 0; ch < 2; ++ch)
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                  const uint32_t off = ch * 8192 + kk * 32;
+                  const uint64_t ah = umma_kdesc(s0 + off), al = umma_kdesc(s0 + 16384 + off);
+                  const uint64_t bh = umma_kdesc(s0 + 32768 + off), bl = umma_kdesc(s0 + 49152 + off);
+                  umma_tf32(tmem, al, bh, (k > c0 || ch > 0 || kk > 0) ? 1u : 0u);
+                  umma_tf32(tmem, ah, bl, 1u);
+                  umma_tf32(tmem, ah, bh, 1u);
+                }
+              umma_commit(smem_addr(&empty_bar[m_stage]));
+              if (++m_stage == kUmmaStages) {
+                m_stage = 0;
+                m_phase ^= 1u;
+              }
+            }
+            umma_commit(smem_addr(&done_bar));
+          }
+          __syncwarp();
+        }
+        mbar_wait_parity(smem_addr(&done_bar), d_phase);
+        d_phase ^= 1u;
       }
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (tid < 64) {  // TMEM lanes 0-63 = rows of the product
+        T* srow = &sm.sf[tid][0];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t v[32];
+          if (c0 < kend) {
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+                "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                  "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                  "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+                  "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                  "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                  "=r"(v[30]), "=r"(v[31])
+                : "r"(tmem + (uint32_t(32 * (tid >> 5)) << 16) + uint32_t(32 * h)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = 0u;
+          }
+#pragma unroll
+          for (int e = 0; e < 32; ++e) srow[32 * h + e] = T(__uint_as_float(v[e]));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncthreads();
-      stage_tile(Pb[0], a + (long long)r * tile + (long long)c0 * TB, n, rows, TB, vec_ok);
-      stage_tile(Qb[0], a + (long long)c * tile + (long long)c0 * TB, n, cols, TB, vec_ok);
-      cp_async_commit();
-    }
-    int buf = 0;
-    int horizon = c0 + 1;  // every k < horizon is known to be published
-    for (int k = c0; k < kend; ++k, buf ^= 1) {
-      const bool more = k + 1 < kend;
-      const int* fr = flags + r * nt + k + 1;
-      const int* fc = flags + c * nt + k + 1;
-      const bool probe = more && k + 1 >= horizon;
-      if (probe && tid < 64) {
-        // refresh the horizon: warps 0 / 1 probe the next 32 k of row r / row c
-        // (one acquire round trip, all in parallel)
-        const int kk = k + 1 + (tid & 31);
-        const int* f = flags + (tid < 32 ? r : c) * nt + kk;
-        const unsigned bal = __ballot_sync(0xffffffffu, kk < kend && ld_acquire(f));
-        if ((tid & 31) == 0) sm.stg[tid >> 5] = ~bal ? __ffs(~bal) - 1 : 32;
-      }
-      __syncthreads();  // (also: everyone is done with buffer buf ^ 1)
-      if (probe) horizon = k + 1 + min(sm.stg[0], sm.stg[1]);
-      const bool ready = more && k + 1 < horizon;
-      if (ready) {  // prefetch k+1 under this product
-        stage_tile(Pb[buf ^ 1], a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
-        stage_tile(Qb[buf ^ 1], a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
-        cp_async_commit();
-        cp_async_wait_1();
-      } else {
-        cp_async_wait_all();
-      }
-      __syncthreads();
-      acc_mma(acc, Pb[buf], Qb[buf]);
-      if (more && !ready) {  // at the dependency frontier: wait, then load
-        if (tid == 0) wait_flag(fr);
-        if (tid == 32) wait_flag(fc);
+    } else {
+      // row-major tiles staged by cp.async
+      // (double-buffered while the next k is already published), tensor-core products
+      TileAcc<T> acc;
+      acc_zero(acc);
+      T* const Pb[2] = {sm.ps, sm.sb[0]};
+      T* const Qb[2] = {sm.qs, sm.sb[1]};
+      if (c0 < kend) {
+        if (tid == 0) {
+          wait_flag(flags + r * nt + c0);
+          wait_flag(flags + c * nt + c0);
+        }
         __syncthreads();
-        horizon = k + 2;
-        stage_tile(Pb[buf ^ 1], a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
-        stage_tile(Qb[buf ^ 1], a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+        stage_tile(Pb[0], a + (long long)r * tile + (long long)c0 * TB, n, rows, TB, vec_ok);
+        stage_tile(Qb[0], a + (long long)c * tile + (long long)c0 * TB, n, cols, TB, vec_ok);
         cp_async_commit();
       }
+      int buf = 0;
+      int horizon = c0 + 1;  // every k < horizon is known to be published
+      for (int k = c0; k < kend; ++k, buf ^= 1) {
+        const bool more = k + 1 < kend;
+        const int* fr = flags + r * nt + k + 1;
+        const int* fc = flags + c * nt + k + 1;
+        const bool probe = more && k + 1 >= horizon;
+        if (probe && tid < 64) {
+          // refresh the horizon: warps 0 / 1 probe the next 32 k of row r / row c
+          // (one acquire round trip, all in parallel)
+          const int kk = k + 1 + (tid & 31);
+          const int* f = flags + (tid < 32 ? r : c) * nt + kk;
+          const unsigned bal = __ballot_sync(0xffffffffu, kk < kend && ld_acquire(f));
+          if ((tid & 31) == 0) sm.stg[tid >> 5] = ~bal ? __ffs(~bal) - 1 : 32;
+        }
+        __syncthreads();  // (also: everyone is done with buffer buf ^ 1)
+        if (probe) horizon = k + 1 + min(sm.stg[0], sm.stg[1]);
+        const bool ready = more && k + 1 < horizon;
+        if (ready) {  // prefetch k+1 under this product
+          stage_tile(Pb[buf ^ 1], a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
+          stage_tile(Qb[buf ^ 1], a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+          cp_async_commit();
+          cp_async_wait_1();
+        } else {
+          cp_async_wait_all();
+        }
+        __syncthreads();
+        acc_mma(acc, Pb[buf], Qb[buf]);
+        if (more && !ready) {  // at the dependency frontier: wait, then load
+          if (tid == 0) wait_flag(fr);
+          if (tid == 32) wait_flag(fc);
+          __syncthreads();
+          horizon = k + 2;
+          stage_tile(Pb[buf ^ 1], a + (long long)r * tile + (long long)(k + 1) * TB, n, rows, TB, vec_ok);
+          stage_tile(Qb[buf ^ 1], a + (long long)c * tile + (long long)(k + 1) * TB, n, cols, TB, vec_ok);
+          cp_async_commit();
+        }
+      }
+      __syncthreads();
+      acc_store(acc, &sm.sf[0][0], TB + 1);
     }
-    __syncthreads();
-    acc_store(acc, &sm.sf[0][0], TB + 1);
     T t[4][4];
     load_t(t, a + (long long)r * tile + (long long)c * TB, n, rows, cols, false, vec_ok);
     __syncthreads();
@@ -1043,9 +1324,15 @@ __global__ void __launch_bounds__(CT, sizeof(T) == 4 ? 2 : 1)
       for (int v = 0; v < 4; ++v) t[u][v] = sm.sf[4 * ty + u][4 * tx + v];
     stamp(item_id, 4);
     store_t(t, a + (long long)r * tile + (long long)c * TB, n, rows, cols, false);
+    if constexpr (sizeof(T) == 4)
+      if (umma) store_split(t, lhi, llo, (long long)r * tile + (long long)c * TB, n, rows, cols);
     __threadfence();
+    if (umma) asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
-    if (tid == 0) st_release(flags + r * nt + c, 1);
+    if (tid == 0) {
+      st_release(flags + r * nt + c, 1);
+      if (umma) st_release(sflags + r * nt + c, 1);
+    }
     stamp(item_id, 5);
     emit_tile(t, sm, r, c, n, ghi, glo, gpl, gtt);
     __syncthreads();
@@ -1144,8 +1431,9 @@ void debug_factor_bench(int iters, long long* cycles, float* out, cudaStream_t s
 
 size_t cholesky_flag_ints(long long n) {
   const long long nt = (n + TB - 1) / TB;
-  // tile flags, partial flags, per-panel item counters + owner slots (<= nt panels)
-  return size_t(nt * nt + 2 * nt + 2 * nt + 8);
+  // tile flags, partial flags, per-panel item counters + owner slots (<= nt panels),
+  // split-stored flags (the tcgen05 k-loops' operands)
+  return size_t(nt * nt + 2 * nt + 2 * nt + 8 + nt * nt);
 }
 
 template <typename T>
@@ -1163,19 +1451,56 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
   }
 }
 
+using EncodeTiledF = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledF encoder_f() {
+  static EncodeTiledF fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return EncodeTiledF(nullptr);
+    return reinterpret_cast<EncodeTiledF>(ptr);
+  }();
+  return fn;
+}
+// n x n fp32 row-major, 32-column x 64-row boxes, SWIZZLE_128B, zero fill out of range
+bool split_map(CUtensorMap* m, const float* base, long long n) {
+  EncodeTiledF enc = encoder_f();
+  if (!enc) return false;
+  const cuuint64_t gdim[2] = {cuuint64_t(n), cuuint64_t(n)};
+  const cuuint64_t gstride[1] = {cuuint64_t(n) * 4};
+  const cuuint32_t box[2] = {32, TB};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T>
 void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, float* gtt, int* flags,
-                unsigned* status, long long macro_cols, cudaStream_t st) {
+                unsigned* status, long long macro_cols, cudaStream_t st, float* lhi, float* llo) {
+  // fp32 with the pre-split L (lhi / llo): worker products on tcgen05 (TMA ring
+  // after the shared struct's small fields, one CTA per SM)
+  UmmaMaps maps{};
+  if (sizeof(T) != 4 || n % 4 != 0 || !lhi || !llo || !split_map(&maps.hi, lhi, n) ||
+      !split_map(&maps.lo, llo, n))
+    lhi = llo = nullptr;
+  const int smem = lhi ? std::max<int>(int(sizeof(CholSmem<T>)), kUmmaEnd)
+                       : int(sizeof(CholSmem<T>));
   cudaFuncSetAttribute(chol_tile_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(sizeof(CholSmem<T>)));  // (per device: set on every call)
+                       smem);  // (per device: set on every call)
   const int nt = int((n + TB - 1) / TB);
   int* pflags = flags + (long long)nt * nt;
   int* counters = pflags + 2LL * nt;
+  int* sflags = counters + 2LL * nt + 8;
   cudaMemsetAsync(flags, 0, cholesky_flag_ints(n) * sizeof(int), st);
   if (gtt) cudaMemsetAsync(gtt, 0, size_t(n) * 128 * sizeof(float), st);  // non-emitted = 0
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_tile_kernel<T>, CT,
-                                                sizeof(CholSmem<T>));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_tile_kernel<T>, CT, smem);
   const int max_ctas = std::max(1, occ) * num_sms_f();
   const int step = macro_cols <= 0 ? nt : int(std::max<long long>(1, macro_cols / TB));
   int ci = 0;
@@ -1192,9 +1517,9 @@ void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, float* gtt, i
       cudaMallocAsync(&trace, size_t(entries) * 6 * 8, st);
       cudaMemsetAsync(trace, 0, size_t(entries) * 6 * 8, st);
     }
-    chol_tile_kernel<T><<<grid, CT, sizeof(CholSmem<T>), st>>>(a, n, nt, c0, c1, flags, pflags,
-                                                                counters + ci, status, ghi, glo, gpl,
-                                                                gtt, trace);
+    chol_tile_kernel<T><<<grid, CT, smem, st>>>(a, n, nt, c0, c1, flags, pflags, counters + ci,
+                                                status, ghi, glo, gpl, gtt, trace, maps, lhi, llo,
+                                                sflags);
     if (tp) {
       std::vector<unsigned long long> h(size_t(entries) * 6);
       cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
@@ -1265,9 +1590,9 @@ template void launch_build_factor_input<float>(const float*, long long, const in
 template void launch_build_factor_input<double>(const float*, long long, const int32_t*, double,
                                                 double*, double*, cudaStream_t);
 template void cholesky_g<float>(float*, long long, float*, float*, float*, float*, int*,
-                                unsigned*, long long, cudaStream_t);
+                                unsigned*, long long, cudaStream_t, float*, float*);
 template void cholesky_g<double>(double*, long long, double*, float*, float*, float*, int*,
-                                 unsigned*, long long, cudaStream_t);
+                                 unsigned*, long long, cudaStream_t, float*, float*);
 template void lower_inverse<float>(const float*, long long, float*, float*, cudaStream_t);
 template void lower_inverse<double>(const double*, long long, double*, double*, cudaStream_t);
 template void upper_from_cholesky<float>(const float*, long long, float*, float*, cudaStream_t);

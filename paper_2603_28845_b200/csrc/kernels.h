@@ -69,7 +69,10 @@ void launch_build_factor_input(const float* h, long long n, const int32_t* order
 size_t cholesky_flag_ints(long long n);
 template <typename T>
 void cholesky_g(T* a, long long n, T* ghi, float* glo, float* gpl, float* gtt, int* flags,
-                unsigned* status, long long macro_cols, cudaStream_t st);
+                unsigned* status, long long macro_cols, cudaStream_t st, float* lhi = nullptr,
+                float* llo = nullptr);
+// (fp32, n % 4 == 0: lhi / llo, n x n each, receive the tf32 hi / lo split of
+// every published L tile, and the workers' tile products run on tcgen05)
 // X = L^-1 (n x n lower) from the Cholesky factor; ws as upper_from_cholesky.
 template <typename T>
 void lower_inverse(const T* a, long long n, T* x, T* ws, cudaStream_t st);

@@ -49,3 +49,21 @@ print(f"  full items (c >= 8): k-loop per k-step mean {per.mean():.2f} us, media
       f"solve+publish mean {np.mean(pb[fi] - kd[fi]) / 1e3:.2f} us; items {len(fi)}")
 busy = np.sum(pb[kind < 3] - st[kind < 3]) / 1e3
 print(f"  worker busy time {busy:.0f} us over span {pb.max() / 1e3:.0f} us -> {busy / (pb.max() / 1e3):.0f} CTAs busy on average")
+
+# critical chain of the diagonal partials: X(c-2) published -> full item (c, c-2)
+# -> partial (c, c) -> owner column c start
+full = {(int(a), int(b)): i for i, (a, b, k) in enumerate(zip(r, c, kind)) if k == 0}
+rows = []
+for cc in range(4, nt):
+    if (cc, cc - 2) not in full or (cc, cc) not in par:
+        continue
+    x = pb[D[cc - 2]]
+    fi, pi = full[(cc, cc - 2)], par[(cc, cc)]
+    rows.append((kd[fi] - x, fd[fi] - x, pb[fi] - x, st[pi] - x, kd[pi] - x, pb[pi] - x, st[D[cc]] - x))
+if rows:
+    a = np.array(rows) / 1e3
+    names = ["full(c,c-2) k-loop done", "full solve done", "full published", "partial start",
+             "partial k-loop done", "partial published", "owner column c start"]
+    print("  critical chain, times after X(c-2) published (median over columns):")
+    for i, nm in enumerate(names):
+        print(f"    {nm:28s} {np.median(a[:, i]):7.2f} us")
