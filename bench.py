@@ -54,8 +54,8 @@ def peaks():
 
 
 # DRAM bytes (read + write) of one hessian_tc2_kernel launch at C2, from the
-# ncu --set full capture in profiles/r01_hessian_ncu_full.txt
-HESSIAN_TRAFFIC_BYTES = 10.744724e9 + 0.558352e9
+# ncu --set full capture of gram_tc_kernel in profiles/r02_gram_ncu_full.txt
+HESSIAN_TRAFFIC_BYTES = 5.369535e9 + 0.623804e9
 
 
 def outlier_channels(n: int, frac: float, seed: int) -> np.ndarray:
@@ -489,7 +489,7 @@ def main():
                      "algorithmic": "T*N*(N+1) flops per launch",
                      "traffic": HESSIAN_TRAFFIC_BYTES if not sharded else None,
                      "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, one launch "
-                                       "at C2 (profiles/r01_hessian_ncu_full.txt)"},
+                                       "at C2 (profiles/r02_gram_ncu_full.txt)"},
         "gpu_launches": launches,
         "clocks": ck,
         "e2e": e2e,
