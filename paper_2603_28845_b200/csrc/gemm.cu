@@ -9,6 +9,8 @@
 // fp64: 64x64 CTA tile, BK 16, 256 threads, 4x4 outputs per thread.
 // Thread->element mapping is strided so shared-memory reads broadcast;
 // tiles are double buffered through registers.
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace ocwg {
@@ -135,13 +137,142 @@ __global__ void __launch_bounds__(256) gemm_kernel(long long m, long long n, lon
   }
 }
 
+// fp64 on the tensor cores (DMMA, mma.sync m8n8k4 .f64 -- tcgen05 has no fp64
+// kind): 128 x 128 CTA tile, BK 16, 16 warps as 4 x 4, each warp a 32 x 32
+// block = 4 x 4 m8n8 accumulators (32 doubles per lane, no spills at 512
+// threads).  Operands are staged through registers (any transposition, fp32
+// inputs widened exactly) into double-buffered shared tiles stored [row][k]
+// for A and [col][k] for B, so a fragment is one 8-byte load per lane; the row
+// stride of 20 doubles puts a half-warp's fragment loads on distinct banks.
+constexpr int DBM = 128, DBN = 128, DBK = 16, DPAD = 4, DTHREADS = 512;
+constexpr int kDmmaSmem = 2 * (DBM + DBN) * (DBK + DPAD) * 8;
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <typename TA, typename TB>
+__global__ void __launch_bounds__(DTHREADS, 1) gemm_f64_dmma_kernel(
+    long long m, long long n, long long k, double alpha, const TA* __restrict__ a, long long lda,
+    int ta, const TB* __restrict__ b, long long ldb, int tb, double beta, double* __restrict__ c,
+    long long ldc, int lower_only, long long sa, long long sb, long long sc, int tri) {
+  a += (long long)blockIdx.z * sa;
+  b += (long long)blockIdx.z * sb;
+  c += (long long)blockIdx.z * sc;
+  const long long row0 = (long long)blockIdx.y * DBM, col0 = (long long)blockIdx.x * DBN;
+  if (lower_only && col0 > row0 + DBM - 1) return;
+  // triangular op(A) (tri 1: lower, 2: upper): only the k range that can be nonzero
+  const long long kbeg = tri == 2 ? row0 / DBK * DBK : 0;
+  const long long kend = tri == 1 ? std::min(k, row0 + DBM) : k;
+  extern __shared__ __align__(16) double dsm[];
+  double (*As)[DBM][DBK + DPAD] = reinterpret_cast<double (*)[DBM][DBK + DPAD]>(dsm);
+  double (*Bs)[DBN][DBK + DPAD] =
+      reinterpret_cast<double (*)[DBN][DBK + DPAD]>(dsm + 2 * DBM * (DBK + DPAD));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  constexpr int LA = DBM * DBK / DTHREADS, LB = DBN * DBK / DTHREADS;
+  double ra[LA], rb[LB];
+  auto load = [&](long long k0) {
+#pragma unroll
+    for (int q = 0; q < LA; ++q) {
+      const int l = tid + q * DTHREADS;
+      const int i = ta ? l % DBM : l / DBK, kk = ta ? l / DBM : l % DBK;
+      const long long gi = row0 + i, gk = k0 + kk;
+      ra[q] = (gi < m && gk < kend) ? double(ta ? __ldg(a + gk * lda + gi) : __ldg(a + gi * lda + gk))
+                                    : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int l = tid + q * DTHREADS;
+      const int j = tb ? l / DBK : l % DBN, kk = tb ? l % DBK : l / DBN;
+      const long long gj = col0 + j, gk = k0 + kk;
+      rb[q] = (gj < n && gk < kend) ? double(tb ? __ldg(b + gj * ldb + gk) : __ldg(b + gk * ldb + gj))
+                                    : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < LA; ++q) {
+      const int l = tid + q * DTHREADS;
+      const int i = ta ? l % DBM : l / DBK, kk = ta ? l / DBM : l % DBK;
+      As[buf][i][kk] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int l = tid + q * DTHREADS;
+      const int j = tb ? l / DBK : l % DBN, kk = tb ? l % DBK : l / DBN;
+      Bs[buf][j][kk] = rb[q];
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const long long nk = kend > kbeg ? (kend - kbeg + DBK - 1) / DBK : 0;
+  if (nk > 0) {
+    load(kbeg);
+    store(0);
+  }
+  __syncthreads();
+  const int fr = lane >> 2, fk = lane & 3;
+  for (long long kt = 0; kt < nk; ++kt) {
+    const int buf = int(kt & 1);
+    if (kt + 1 < nk) load(kbeg + (kt + 1) * DBK);
+#pragma unroll
+    for (int kq = 0; kq < DBK; kq += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[buf][wm + 8 * i + fr][kq + fk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][wn + 8 * j + fr][kq + fk];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], av[i], bv[j]);
+    }
+    if (kt + 1 < nk) store(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long gi = row0 + wm + 8 * i + fr;
+    if (gi >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const long long gj = col0 + wn + 8 * j + 2 * fk + e;
+        if (gj >= n) continue;
+        double* p = c + gi * ldc + gj;
+        *p = beta == 0.0 ? alpha * acc[i][j][e] : fma(alpha, acc[i][j][e], beta * *p);
+      }
+  }
+}
+
 }  // namespace
 
 template <typename T, typename TA, typename TB>
 void gemm(long long m, long long n, long long k, double alpha, const TA* a, long long lda, bool ta,
           const TB* b, long long ldb, bool tb, double beta, T* c, long long ldc, bool lower_only,
-          cudaStream_t st, int batch, long long sa, long long sb, long long sc) {
+          cudaStream_t st, int batch, long long sa, long long sb, long long sc, int tri) {
   if (m <= 0 || n <= 0 || batch <= 0) return;
+  if constexpr (sizeof(T) == 8) {
+    // fp64 on the DMMA tensor cores once a 128 x 128 tile is reasonably filled
+    if (m >= 64 && n >= 64 && k >= 8) {
+      cudaFuncSetAttribute(gemm_f64_dmma_kernel<TA, TB>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kDmmaSmem);
+      dim3 grid(unsigned((n + DBN - 1) / DBN), unsigned((m + DBM - 1) / DBM), unsigned(batch));
+      count_launches(1);
+      gemm_f64_dmma_kernel<TA, TB><<<grid, DTHREADS, kDmmaSmem, st>>>(
+          m, n, k, alpha, a, lda, ta ? 1 : 0, b, ldb, tb ? 1 : 0, beta, c, ldc,
+          lower_only ? 1 : 0, sa, sb, sc, tri);
+      return;
+    }
+  }
+  (void)tri;  // (the SIMT path multiplies the zeros)
   constexpr int BM = Tile<T>::BM, BN = Tile<T>::BN;
   dim3 grid(unsigned((n + BN - 1) / BN), unsigned((m + BM - 1) / BM), unsigned(batch));
   count_launches(1);
@@ -189,7 +320,7 @@ void mm<double>(long long m, long long n, long long k, double alpha, const doubl
 #define OCWG_GEMM_INST(T, TA, TB)                                                              \
   template void gemm<T, TA, TB>(long long, long long, long long, double, const TA*, long long, \
                                 bool, const TB*, long long, bool, double, T*, long long, bool, \
-                                cudaStream_t, int, long long, long long, long long);
+                                cudaStream_t, int, long long, long long, long long, int);
 OCWG_GEMM_INST(double, double, double)
 OCWG_GEMM_INST(double, float, float)
 OCWG_GEMM_INST(double, float, double)

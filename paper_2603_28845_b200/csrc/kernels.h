@@ -93,7 +93,9 @@ template <typename T, typename TA, typename TB>
 void gemm(long long m, long long n, long long k, double alpha, const TA* a, long long lda,
           bool ta, const TB* b, long long ldb, bool tb, double beta, T* c, long long ldc,
           bool lower_only, cudaStream_t st, int batch = 1, long long sa = 0, long long sb = 0,
-          long long sc = 0);
+          long long sc = 0, int tri = 0);
+// (tri, fp64 tensor-core path: op(A) is lower (1) / upper (2) triangular and the
+// k range that multiplies its zeros is skipped)
 
 // ---- tensor-core fp32-accurate GEMM (tc_gemm.cu): 3xTF32 on tcgen05 ---------
 size_t tc_gemm_workspace_floats(long long m, long long n, long long k, int batch = 1);
@@ -116,9 +118,9 @@ bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const
                        const float* a_lo, long long lda, const float* b_hi, const float* b_lo,
                        long long ldb, float beta, float* c, long long ldc, cudaStream_t st,
                        bool pdl = false, int ksplit = 1, int* kflag = nullptr, int epoch = 0);
-// (ksplit = 2: two K halves per tile on different pairs, the second adding to
-// the first's store; kflag: 2 ints per 256 x 256 tile, never equal to a fresh
-// epoch before the launch)
+// (ksplit <= 4: K parts of a tile on different pairs, each adding to the previous
+// part's store in order; kflag: 2 ints per 256 x 256 tile, below 4 epoch + 1
+// before the launch -- zero them once, then pass increasing epochs >= 1)
 // pdl: launched as a programmatic dependent of the previous kernel on st (the
 // kernel's setup overlaps that kernel's tail; its loads wait in griddepcontrol)
 // Dispatch: T = float -> tcgen05 3xTF32 (when a workspace is set and the

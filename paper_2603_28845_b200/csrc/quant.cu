@@ -150,6 +150,69 @@ __global__ void calibrate_groups_kernel(const float* __restrict__ w, long long r
   }
 }
 
+// Min-max grids of per-group quantisation, 8 groups per warp: every lane's
+// loads of the 8 groups are in flight together (the one-group-per-warp kernel
+// above is latency bound), then lane q computes group q's grid.  Same
+// extremes (order-free min / max), same grid arithmetic, same non-finite rule.
+template <int IT>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) calibrate_minmax8_kernel(
+    const float* __restrict__ w, long long rows, long long cols, long long ld, QCfg c,
+    long long ngroups, float* scales, int32_t* zeros, unsigned* flag) {
+  const long long g0 = ((long long)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5)) * 8;
+  if (g0 >= ngroups) return;
+  const int lane = int(lane_id());
+  float v[8][IT];
+  int len[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const long long g = g0 + q;
+    const Seg sg = g < ngroups ? segment_of(g, rows, cols, ld, c) : Seg{0, 1, 0};
+    len[q] = int(sg.len);
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int k = lane + 32 * i;
+      v[q][i] = k < len[q] ? __ldg(w + sg.base + k) : 0.f;
+    }
+  }
+  float mlo = 0.f, mhi = 0.f;
+  bool mbad = false;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float lo = FLT_MAX, hi = -FLT_MAX;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      if (lane + 32 * i < len[q]) {
+        bad |= !isfinite(v[q][i]);
+        lo = fminf(lo, v[q][i]);
+        hi = fmaxf(hi, v[q][i]);
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == q) {
+      mlo = lo;
+      mhi = hi;
+      mbad = bad;
+    }
+  }
+  const long long g = g0 + lane;
+  if (lane < 8 && g < ngroups) {
+    if (mbad) {
+      atomicOr(flag, kFlagNonFinite);
+    } else {
+      float s;
+      int z;
+      grid_from_extremes(mlo, mhi, c, s, z);
+      scales[g] = s;
+      zeros[g] = z;
+    }
+  }
+}
+
 // per-tensor extremes, pass 1: per-block partials; pass 2: one block
 __global__ void minmax_partial_kernel(const float* __restrict__ w, long long n, float* part,
                                       unsigned* flag) {
@@ -365,6 +428,19 @@ void launch_calibrate_grids(const float* w, long long rows, long long cols, long
     count_launches(2);
   }
   count_launches(1);
+  if (c.gran == 2 && !mse && c.group <= 128) {
+    const int blocks = int((ng + 8 * kWarpsPerBlock - 1) / (8 * kWarpsPerBlock));
+    const int it = int((c.group + 31) / 32);
+    if (it <= 1)
+      calibrate_minmax8_kernel<1><<<blocks, 32 * kWarpsPerBlock, 0, st>>>(w, rows, cols, ld, c, ng, scales, zeros, flag);
+    else if (it == 2)
+      calibrate_minmax8_kernel<2><<<blocks, 32 * kWarpsPerBlock, 0, st>>>(w, rows, cols, ld, c, ng, scales, zeros, flag);
+    else if (it == 3)
+      calibrate_minmax8_kernel<3><<<blocks, 32 * kWarpsPerBlock, 0, st>>>(w, rows, cols, ld, c, ng, scales, zeros, flag);
+    else
+      calibrate_minmax8_kernel<4><<<blocks, 32 * kWarpsPerBlock, 0, st>>>(w, rows, cols, ld, c, ng, scales, zeros, flag);
+    return;
+  }
   const int blocks = int((ng + kWarpsPerBlock - 1) / kWarpsPerBlock);
   calibrate_groups_kernel<<<blocks, 32 * kWarpsPerBlock, 0, st>>>(w, rows, cols, ld, c, mse, ng, scales,
                                                                   zeros, flag, pre);

@@ -692,6 +692,12 @@ void launch_inblock(const float* w, long long ldw, const int32_t* order, const T
 }  // namespace
 
 constexpr long long kSuperRows = 512;  // rows of G D applied per trailing GEMM (K)
+// left-looking fp32 sweep: rows per super-block and K parts per GEMM tile
+// (OCWG_SWEEP_SUPER caps the super-block as for the right-looking sweep)
+// (measured: 256-row super-blocks with 4 K parts per tile are slower -- each
+// GEMM launch carries ~28 us of fixed cost and the parts' epilogues chain)
+constexpr long long kLeftSuperRows = 512;
+constexpr int kLeftSplit = 2;
 
 size_t sweep_delta_elems(long long m) { return size_t(m) * kSuperRows; }
 size_t sweep_kflag_ints(long long n, long long m) {
@@ -773,14 +779,15 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
       // GPU.  D of every row is kept (K-major, ld n: plain for the lookahead,
       // tf32 hi / lo for the GEMM).
       cudaMemsetAsync(kflag, 0, sweep_kflag_ints(n, m) * sizeof(int), st);
-      for (long long s0 = 0, si = 0; s0 < n; s0 += SBK, ++si) {
-        const long long se = std::min(n, s0 + SBK);
+      const long long SBL = std::min<long long>(SBK, kLeftSuperRows);
+      for (long long s0 = 0, si = 0; s0 < n; s0 += SBL, ++si) {
+        const long long se = std::min(n, s0 + SBL);
         if (si > 0) {
           bool done = tc_gemm2_presplit(se - s0, m, s0, 1.0f,
                                         reinterpret_cast<const float*>(ghi) + s0 * n,
                                         glo + s0 * n, n, dhi[0], dlo[0], n, 0.0f,
-                                        reinterpret_cast<float*>(acc) + s0 * m, m, st, pdl_on, 2,
-                                        kflag, int(si));
+                                        reinterpret_cast<float*>(acc) + s0 * m, m, st, pdl_on,
+                                        kLeftSplit, kflag, int(si));
           if (!done)
             done = tc_gemm_presplit(se - s0, m, s0, 1.0f,
                                     reinterpret_cast<const float*>(ghi) + s0 * n, glo + s0 * n, n,

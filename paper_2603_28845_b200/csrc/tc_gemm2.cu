@@ -144,11 +144,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int pair = int(blockIdx.x >> 1), npairs = int(gridDim.x >> 1);
   const int kb_total = int((k + TK - 1) / TK);
   // units: (tile, K part), part-major; part q of a tile covers k-blocks
-  // [kb_total q / ksplit, kb_total (q+1) / ksplit).  With ksplit = 2 the second
-  // part adds into C after the first part's store (per-(tile, CTA) flag set to
-  // `epoch`): deterministic, no zero-fill.  A part-1 unit is assigned after its
-  // part-0 unit (round-robin over resident pairs), so it never waits on a unit
-  // that has not started.
+  // [kb_total q / ksplit, kb_total (q+1) / ksplit).  Part q > 0 adds into C
+  // after part q-1 has stored (per-(tile, CTA) flag: part q releases
+  // 4 epoch + q + 1): a fixed summation order, deterministic, no zero-fill.  A
+  // part is assigned after the parts before it (round-robin over resident
+  // pairs), so it never waits on a unit that has not started.
   const int nunits = ntiles * ksplit;
   auto kb_range = [&](int t, int& kb0, int& kb1) {
     const int q = t / ntiles;
@@ -260,9 +260,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       float* crow_base = c + row * ldc + (long long)tn * 256;
       int* flag = kflag + tile * 2 + int(rank);
       const float bt = part == 0 ? beta : 1.f;  // later parts add to the first
-      if (part > 0) {  // the first part of this tile has stored its rows
+      if (part > 0) {  // the previous part of this tile has stored its rows
         if (warp == 2 && lane == 0)
-          while (ld_acquire_gpu(flag) != epoch) __nanosleep(64);
+          while (ld_acquire_gpu(flag) != 4 * epoch + part) __nanosleep(64);
         asm volatile("bar.sync 1, 256;" ::: "memory");
       }
       auto load_c = [&](int c0, float (&v)[32]) {
@@ -322,10 +322,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       tc_fence_before();
-      if (ksplit > 1 && part == 0) {  // publish this CTA's rows of the tile
+      if (part + 1 < ksplit) {  // publish this CTA's rows of the tile to the next part
         __threadfence();
         asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (warp == 2 && lane == 0) st_release_gpu(flag, epoch);
+        if (warp == 2 && lane == 0) st_release_gpu(flag, 4 * epoch + part + 1);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&tempty_bar[acc]), 0));
@@ -393,7 +393,7 @@ bool tc_gemm2_presplit(long long m, long long n, long long k, float alpha, const
   const int ntiles = tiles_m * tiles_n;
   const long long kb_total = (k + TK - 1) / TK;
   if (ksplit < 1 || !kflag) ksplit = 1;
-  ksplit = int(std::min<long long>({(long long)ksplit, 2LL, kb_total}));
+  ksplit = int(std::min<long long>({(long long)ksplit, 4LL, kb_total}));
   const int nunits = ntiles * ksplit;
   int npairs = std::min(nunits, num_sms3() / 2);
   cudaLaunchConfig_t cfg{};
