@@ -110,6 +110,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1000,8 +1005,20 @@ __global__ void __launch_bounds__(CT, 1)
       }
       stamp(e1, 3);
       staged = sm.stg[2];  // the next column's S'[c+1,c+1], staged under the factor
+      // not staged yet: look again (relaxed load issued before the solve, so its
+      // latency hides under the product) and start the copy for the next column
+      int pv = 0;
+      if (!staged && tid == 0) pv = ld_relaxed(pflags + 2 * (c + 1));
       owner_prod<T, true>(sm.sb[0], &sm.lt[0][0], nullptr, sm.qs, LD, T(1), -1);  // -> L[c+1,c]
+      if (!staged && tid == 0) {
+        if (pv) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        sm.stg[2] = pv;
+      }
       __syncthreads();
+      if (!staged && sm.stg[2]) {  // (completes under the publish; waited at the next column)
+        stage_tile(sm.sb[1], a + (c + 1) * tile + (long long)(c + 1) * TB, n, rows1, rows1, vec_ok);
+        staged = true;
+      }
       stamp(e1, 4);
       {
         T t[4][4];

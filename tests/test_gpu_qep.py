@@ -2,7 +2,9 @@
 against the reference's own qep_target / quantize_layer (oracle/_ref), on
 seeded calibration pairs (x_fp, x_pert) whose statistics come from the
 reference's accumulate_stats.  fp64 on both sides: the corrected target is
-compared with rtol 1e-6; quantize_layer codes >= 99.9 % identical."""
+compared with rtol 1e-6; quantize_layer codes >= 99.9 % identical.  The
+larger cases run several 128 x 128 DMMA tiles, the triangular k-range skip of
+the L^-1 products and (n > 512) the macro-panel fp64 Cholesky."""
 import numpy as np
 import pytest
 
@@ -27,7 +29,8 @@ def stats_pair(ref, n, t, seed):
 
 
 @pytest.mark.parametrize("n,m,alpha,eta", [(16, 24, 1.0, 0.01), (64, 40, 0.5, 0.05),
-                                           (130, 70, 0.25, 0.01)])
+                                           (130, 70, 0.25, 0.01), (600, 300, 0.5, 0.01),
+                                           (700, 260, 1.0, 0.02)])
 def test_qep_target_matches_reference(g, ref, n, m, alpha, eta):
     gram, cross = stats_pair(ref, n, 4 * n, 900 + n)
     w = ref.random_gaussian(n, m, 77 + n, 0.02)
