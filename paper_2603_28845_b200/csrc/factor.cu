@@ -255,21 +255,34 @@ __device__ __forceinline__ T rsqrt_fast(T x) {
 // Shared-pivot elimination for factor_tile64: the eliminating warp (producer)
 // publishes each pivot column in a 4-deep shared ring (wcol4[j & 3], shifted
 // as in warp_chol32) and 1/L[j][j] in rdiag[j]; carrying warps (consumers)
-// apply the same pivots to their rows without redoing the elimination.  One
-// named barrier (id 2, nthreads = the participating warps) per pivot: after
-// it, column j and rdiag[j] are visible; the ring is deep enough that the
-// producer never overwrites a column a consumer may still read.
+// apply the same pivots to their rows without redoing the elimination.  Per
+// ring slot s two named barriers (nthreads = the participating warps):
+// full(s) = 2 + s -- the producer arrives once pivot j's column and rdiag[j]
+// are written, consumers sync; empty(s) = 6 + s -- consumers arrive once done
+// with the slot, the producer syncs before refilling it.  The producer never
+// waits for consumers unless it is 4 pivots ahead, so its pivot chain alone
+// sets the pace (a full rendezvous per pivot put the consumers' work on it).
+__device__ __forceinline__ void bar_sync_id(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_id(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 template <typename T>
 __device__ __forceinline__ bool warp_chol32_prod(T (&a)[32], T* out_row, T* rdiag,
                                                  T (*wcol4)[72], int nthreads) {
   const int lane = threadIdx.x & 31;
+  const bool cons = nthreads > 32;
   bool ok = true;
   wcol4[0][lane + 3] = a[0];
+  // the pivot travels by shuffle (the next pivot is lane j+1's updated entry),
+  // so the chain is shuffle -> rsqrt -> 3 FMA-pipe ops; only the column, which
+  // the FMAs need later, goes through the shared ring
+  T p = __shfl_sync(0xffffffffu, a[0], 0);
 #pragma unroll 4
   for (int j = 0; j < 32; ++j) {
     const int sh = (3 - j) & 3;
     __syncwarp();
-    const T p = wcol4[j & 3][j + sh];
     T v[32];
     const T* nxt = wcol4[j & 3] + j + sh + 1;
 #pragma unroll
@@ -284,14 +297,21 @@ __device__ __forceinline__ bool warp_chol32_prod(T (&a)[32], T* out_row, T* rdia
     const T l = a[0] * rs;
     const T lrs = l * rs;
     const T a0 = fma(-lrs, v[0], a[1]);
+    // slot (j+1) & 3 last held pivot j-3's column: the consumers must be done with it
+    if (cons && j >= 3 && j + 1 < 32) bar_sync_id(6 + ((j + 1) & 3), nthreads);
     if (j + 1 < 32) wcol4[(j + 1) & 3][lane + ((2 - j) & 3)] = a0;
     if (lane == j) rdiag[j] = rs;  // 1 / L[j][j]
-    if (nthreads > 32) asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+    if (cons) bar_arrive_id(2 + (j & 3), nthreads);
+    if (j + 1 < 32) p = __shfl_sync(0xffffffffu, a0, j + 1);
 #pragma unroll
     for (int k = 1; k + 1 < 32; ++k) a[k] = fma(-lrs, v[k], a[k + 1]);
     a[0] = a0;
     a[31] = T(0);
     out_row[j] = lane >= j ? l : T(0);
+  }
+  if (cons) {  // balance the empty phases of pivots 28..31
+#pragma unroll
+    for (int s = 0; s < 4; ++s) bar_sync_id(6 + s, nthreads);
   }
   return ok;
 }
@@ -301,7 +321,7 @@ __device__ __forceinline__ void warp_carry32_cons(T (&b)[32], T* out_b, const T*
 #pragma unroll 4
   for (int j = 0; j < 32; ++j) {
     const int sh = (3 - j) & 3;
-    asm volatile("bar.sync 2, %0;" ::"r"(nthreads) : "memory");
+    bar_sync_id(2 + (j & 3), nthreads);
     T v[32];
     const T* nxt = wcol4[j & 3] + j + sh + 1;
 #pragma unroll
@@ -312,6 +332,7 @@ __device__ __forceinline__ void warp_carry32_cons(T (&b)[32], T* out_b, const T*
       for (int e = 0; e < 4; ++e) v[k4 + e] = v4[e];
     }
     const T rs = rdiag[j];
+    bar_arrive_id(6 + (j & 3), nthreads);  // (slot and rdiag[j] read into registers)
     const T lb = b[0] * rs;  // (b L^-T)[j]
     const T lbrs = lb * rs;
 #pragma unroll
