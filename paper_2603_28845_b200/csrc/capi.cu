@@ -308,6 +308,7 @@ struct GptqBufs {
   int* kflag;     // split-K tile flags of the left-looking sweep GEMMs (split only)
   float* lhi;     // n x n: tf32 hi / lo split of L (split only; the Cholesky's tcgen05 products)
   float* llo;
+  void* tab;      // one super-block's sweep table (split only)
   float* tcws;
   size_t tcws_floats;
 };
@@ -347,6 +348,7 @@ void gptq_reserve(Arena& ar, const ocwg_ctx* ctx, uint64_t n, uint64_t m, size_t
   o[10] = ar.reserve(split ? n * 128 * 4 + 1024 : 0);
   o[11] = ar.reserve(split ? sweep_kflag_ints((long long)n, (long long)m) * sizeof(int) : 0);
   o[12] = ar.reserve(split ? 2 * n * n * 4 : 0);
+  o[13] = ar.reserve(split ? sweep_table_bytes((long long)std::max<uint64_t>(m, 1)) : 0);
 }
 GptqBufs gptq_bufs(const Arena& ar, const ocwg_ctx* ctx, const size_t* o, uint64_t n, uint64_t m) {
   const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
@@ -369,6 +371,7 @@ GptqBufs gptq_bufs(const Arena& ar, const ocwg_ctx* ctx, const size_t* o, uint64
   b.kflag = split ? ar.at<int>(o[11]) : nullptr;
   b.lhi = split ? ar.at<float>(o[12]) : nullptr;
   b.llo = split ? ar.at<float>(o[12]) + n * n : nullptr;
+  b.tab = split ? ar.at<void>(o[13]) : nullptr;
   b.tcws = ar.at<float>(o[9]);
   b.tcws_floats = tc_ws_floats(n);
   b.gtt = split ? ar.at<float>(o[10]) : nullptr;
@@ -412,7 +415,7 @@ void run_sweep_t(ocwg_ctx* ctx, const float* w, uint64_t ldw, uint64_t n, uint64
   gptq_sweep_g<T>(w, (long long)ldw, (long long)n, (long long)m, static_cast<const T*>(b.gpl),
                   b.gtt, static_cast<const T*>(b.ghi), b.glo, b.order, c, scales, zeros,
                   (long long)opts->block_cols, codes, w_hat, (long long)ldw, static_cast<T*>(b.acc),
-                  dp, dh, dl, b.kflag, ctx->stream);
+                  dp, dh, dl, b.kflag, ctx->stream, b.tab, ctx->aux, ctx->sev + 3);
 }
 
 // gptq_quantize on device buffers (w row stride ldw; codes/w_hat stride ldw)
@@ -1120,7 +1123,7 @@ int ocwg_gptq_factor(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, do
     const size_t es = ctx->precision == OCWG_FP64 ? 8 : 4;
     const uint64_t nblk = (n + 63) / 64;
     Arena ar(ctx);
-    size_t o[13];
+    size_t o[14];
     gptq_reserve(ar, ctx, n, 1, o);
     const size_t oh = ar.reserve(n * n * 4), ohi = ar.reserve(n * n * 8),
                  ou64 = ar.reserve(n * n * 8), ou = ar.reserve(n * n * es),
@@ -1163,7 +1166,7 @@ int ocwg_gptq_quantize_dev(ocwg_ctx* ctx, const float* w, uint64_t ldw, const fl
     std::lock_guard<std::mutex> lk(ctx->mu);
     begin(ctx, true);
     Arena ar(ctx);
-    size_t o[13];
+    size_t o[14];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     ar.commit();
@@ -1245,7 +1248,7 @@ int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, const
     const uint64_t ng = group_count(cfg, n, m);
     const QCfg c = qcfg(cfg, m);
     Arena ar(ctx);
-    size_t o[13];
+    size_t o[14];
     if (method == 1) gptq_reserve(ar, ctx, n, m, o);
     const size_t ow = ar.reserve(n * m * 4), og = ar.reserve(n * n * 8),
                  oc = ar.reserve(corr ? n * n * 8 : 8), oh = ar.reserve(method == 1 ? n * n * 4 : 4),
@@ -1347,7 +1350,7 @@ int ocwg_quantize_layer_x_dev(ocwg_ctx* ctx, const float* w, const uint16_t* x, 
     begin(ctx, true);
     const uint64_t ng = group_count(cfg, n, m);
     Arena ar(ctx);
-    size_t o[13];
+    size_t o[14];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const size_t oh = ar.reserve(n * n * 4);
@@ -1415,7 +1418,7 @@ int ocwg_quantize_layer_x(ocwg_ctx* ctx, const float* w, const uint16_t* x, uint
     float* hd = reinterpret_cast<float*>(io + oh);
     // ---- workspace
     Arena ar(ctx);
-    size_t o[13];
+    size_t o[14];
     gptq_reserve(ar, ctx, n, m, o);
     const size_t om = ar.reserve(4096 * 4);
     const long long chunk = 32768;  // tokens per H2D chunk (a multiple of the 16384 split)
@@ -1493,7 +1496,7 @@ int ocwg_quantize_layers_x_dev(ocwg_ctx* ctx, int count, const float* const* w, 
     begin(ctx, true);
     cudaStream_t st = ctx->stream;
     Arena ar(ctx);
-    size_t o[13];
+    size_t o[14];
     gptq_reserve(ar, ctx, n, mmax, o);
     const size_t om = ar.reserve(4096 * 4), oh = ar.reserve(n * n * 4);
     const size_t hws = gram_tc_workspace_bytes((long long)n);
@@ -1567,7 +1570,7 @@ int ocwg_quantize_layers_x(ocwg_ctx* ctx, int count, const float* const* w, cons
     uint8_t* pd = reinterpret_cast<uint8_t*>(io + opl);
     float* hd = reinterpret_cast<float*>(io + oh);
     Arena ar(ctx);
-    size_t o[13];
+    size_t o[14];
     gptq_reserve(ar, ctx, n, mmax, o);
     const size_t om = ar.reserve(4096 * 4);
     const long long chunk = 32768;

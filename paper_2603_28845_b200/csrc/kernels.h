@@ -145,7 +145,11 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
                   const float* gtt, const T* ghi, const float* glo, const int32_t* order, const QCfg& c,
                   const float* scales, const int32_t* zeros, long long block, int16_t* codes,
                   float* w_hat, long long ldo, T* acc, T* const dpl[2], float* const dhi[2],
-                  float* const dlo[2], int* kflag, cudaStream_t st);
+                  float* const dlo[2], int* kflag, cudaStream_t st, void* tab = nullptr,
+                  cudaStream_t aux = nullptr, cudaEvent_t* ev = nullptr);
+// (tab: sweep_table_bytes(m), one super-block's {w, s, 1/s, z} table, built on
+// `aux` beside each trailing GEMM with the two events ev[0..1])
+size_t sweep_table_bytes(long long m);
 // fp32 pre-split path (kflag != null): left-looking sweep, D of every row kept:
 // dpl[0] / dhi[0] / dlo[0] are m x n K-major (ld n); kflag: sweep_kflag_ints.
 size_t sweep_kflag_ints(long long n, long long m);

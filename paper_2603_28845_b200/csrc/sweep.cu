@@ -370,10 +370,27 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
     float* __restrict__ dcur, float* __restrict__ dcur_hi, float* __restrict__ dcur_lo, QCfg c,
     const float* __restrict__ scales, const int32_t* __restrict__ zeros, long long n, long long m,
     long long ib, int bsz, int16_t* __restrict__ codes, float* __restrict__ w_hat, long long ldo,
-    long long ldd, int trace) {
+    long long ldd, int trace, const float4* __restrict__ tabb, const int* __restrict__ tab_sbad) {
   extern __shared__ __align__(16) unsigned char smraw[];
   Smem& sm = *reinterpret_cast<Smem*>(smraw);
   stamp(trace, 0);
+  // a prepared table block (sweep_table_kernel, built beside the previous
+  // trailing GEMM): the {w, s, 1/s, z} rows are one contiguous 32 KB bulk copy
+  // instead of a gather.  Its mbarrier lives in the read-ahead row kB, which
+  // never holds data (two CTAs per SM leave no spare shared memory).
+  const uint32_t tbar = smem_u32(&sm.tab[kB][0]);
+  if (tabb && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tbar),
+                 "r"(uint32_t(kB * kCols4 * 16))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(&sm.tab[0][0])),
+        "l"(tabb + (long long)blockIdx.x * kB * kCols4), "r"(uint32_t(kB * kCols4 * 16)), "r"(tbar)
+        : "memory");
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int cc = lane & 3, rg = lane >> 2;
   const int og = tid < bsz ? order[ib + tid] : 0;
@@ -398,9 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
 
   // ---- per-(row, column) table {w, s, 1/s, z}: task = (row, 4 columns)
   const bool wvec = (ldw & 3) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0;
-  bool sbad = false;  // a scale outside scale_safe(): the chain divides exactly
+  bool sbad = tabb ? __ldg(tab_sbad + blockIdx.x) != 0 : false;  // a scale outside scale_safe():
+                                                                 // the chain divides exactly
 #pragma unroll
-  for (int i = 0; i < kB * kCols4 / 4 / kThreads; ++i) {
+  for (int i = 0; i < (tabb ? 0 : kB * kCols4 / 4 / kThreads); ++i) {
     const int e = tid + i * kThreads;
     const int li = e >> 2, q = (e & 3) * 4;
     const long long jj = j0 + q;
@@ -519,6 +537,18 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
   }
   stamp(trace, 2);
   cp_async_wait<0>();
+  if (tabb) {
+    uint32_t done;
+    do {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(tbar)
+          : "memory");
+    } while (!done);
+  }
   const bool exact_div = __syncthreads_or(sbad || (trace & 2));
   stamp(trace, 3);
 
@@ -645,12 +675,45 @@ __global__ void __launch_bounds__(kThreads, 1) inblock4_kernel(
 }
 }  // namespace l4
 
+// The sweep table of one super-block: {w, s, 1/s, z} of W[order[li], j] and its
+// grid for rows li in [r0, r1), laid out [block][16-column slab][128 rows][16]
+// float4 so an in-block CTA's 128 x 16 block is one contiguous 32 KB copy; rows
+// past r1 and columns past m are padding {0, 1, 1, 0}.  sbad[block][slab] != 0:
+// a scale outside scale_safe() -- that CTA's chain divides exactly.
+__global__ void sweep_table_kernel(const float* __restrict__ w, long long ldw, long long r0,
+                                   long long r1, long long m, int slabs,
+                                   const int32_t* __restrict__ order, QCfg c,
+                                   const float* __restrict__ scales,
+                                   const int32_t* __restrict__ zeros, float4* __restrict__ tab,
+                                   int* __restrict__ sbad) {
+  const long long nblk = (r1 - r0 + kB - 1) / kB;
+  const long long per_blk = (long long)slabs * kB * l4::kCols4;
+  const long long total = nblk * per_blk;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / per_blk, rem = e % per_blk;
+    const long long slab = rem / (kB * l4::kCols4), r2 = rem % (kB * l4::kCols4);
+    const long long lr = r2 / l4::kCols4, cl = r2 % l4::kCols4;
+    const long long li = r0 + b * kB + lr, jj = slab * l4::kCols4 + cl;
+    float4 v = make_float4(0.f, 1.f, 1.f, 0.f);
+    if (li < r1 && jj < m) {
+      const long long orig = __ldg(order + li);
+      const long long g = group_of(c, orig, jj);
+      const float sv = __ldg(scales + g);
+      v = make_float4(__ldg(w + orig * ldw + jj), sv, rcp_refined(sv), float(__ldg(zeros + g)));
+      if (!scale_safe(sv)) atomicOr(sbad + b * slabs + slab, 1);
+    }
+    tab[e] = v;
+  }
+}
+
 void launch_inblock4(const float* w, long long ldw, const int32_t* order, const float* acc,
                      int use_acc, const float* gpl, const float* gtt, const float* dprev, int bprev,
                      float* dcur, float* dch, float* dcl, const QCfg& c, const float* scales,
                      const int32_t* zeros, long long n, long long m, long long ib, int bsz,
                      int16_t* codes, float* w_hat, long long ldo, long long ldd, int trace,
-                     bool pdl, cudaStream_t st) {
+                     bool pdl, cudaStream_t st, const float4* tabb = nullptr,
+                     const int* tab_sbad = nullptr) {
   // function attributes are per device: set on every launch (cheap)
   cudaFuncSetAttribute(l4::inblock4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(sizeof(l4::Smem)));
@@ -671,7 +734,7 @@ void launch_inblock4(const float* w, long long ldw, const int32_t* order, const 
   cfg.numAttrs = pdl ? 1 : 0;
   cudaLaunchKernelEx(&cfg, l4::inblock4_kernel, w, ldw, order, acc, use_acc, gpl, gtt, dprev, bprev,
                      dcur, dch, dcl, c, scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, ldd,
-                     trace);
+                     trace, tabb, tab_sbad);
 }
 
 template <typename T, int RPT>
@@ -700,6 +763,13 @@ constexpr long long kLeftSuperRows = 512;
 constexpr int kLeftSplit = 2;
 
 size_t sweep_delta_elems(long long m) { return size_t(m) * kSuperRows; }
+size_t sweep_table_bytes(long long m) {
+  const long long slabs = (m + l4::kCols4 - 1) / l4::kCols4;
+  const long long blocks = kLeftSuperRows / kB;
+  return size_t(blocks * slabs * kB * l4::kCols4) * sizeof(float4) +
+         size_t(blocks * slabs) * sizeof(int) + 256;
+}
+
 size_t sweep_kflag_ints(long long n, long long m) {
   return size_t(2 * ((kSuperRows + 255) / 256) * ((m + 255) / 256)) + 8;
 }
@@ -715,7 +785,8 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
                   const float* gtt, const T* ghi, const float* glo, const int32_t* order,
                   const QCfg& c, const float* scales, const int32_t* zeros, long long block,
                   int16_t* codes, float* w_hat, long long ldo, T* acc, T* const dpl[2],
-                  float* const dhi[2], float* const dlo[2], int* kflag, cudaStream_t st) {
+                  float* const dhi[2], float* const dlo[2], int* kflag, cudaStream_t st,
+                  void* tab, cudaStream_t aux, cudaEvent_t* ev) {
   // Block size is a pure re-association of the trailing update (SURVEY §0
   // item 11): the fp32 path always runs the tuned 128-row kernel (so the
   // reference default block_cols = 32, layerwise.hpp:14, is fast too); the
@@ -780,8 +851,37 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
       // tf32 hi / lo for the GEMM).
       cudaMemsetAsync(kflag, 0, sweep_kflag_ints(n, m) * sizeof(int), st);
       const long long SBL = std::min<long long>(SBK, kLeftSuperRows);
+      // Each super-block's {w, s, 1/s, z} table is built just in time on the
+      // auxiliary stream, beside the GEMM that precedes the super-block (it is
+      // read from L2 right after), so the in-block kernels copy instead of
+      // gathering.  One buffer: the build waits for the previous super-block's
+      // last in-block kernel.
+      const int slabs = int((m + l4::kCols4 - 1) / l4::kCols4);
+      const bool jit_tab = tab && aux && ev && SBL == kLeftSuperRows;
+      float4* tabf = static_cast<float4*>(tab);
+      int* tsbad = jit_tab ? reinterpret_cast<int*>(tabf + (kLeftSuperRows / kB) * slabs * kB *
+                                                               l4::kCols4)
+                           : nullptr;
+      auto build_table = [&](long long s0, long long se, cudaStream_t on) {
+        cudaMemsetAsync(tsbad, 0, size_t(kLeftSuperRows / kB) * slabs * sizeof(int), on);
+        const long long total = ((se - s0 + kB - 1) / kB) * slabs * kB * l4::kCols4;
+        const int blocks = int(std::min<long long>((total + 255) / 256, 148LL * 8));
+        count_launches(1);
+        sweep_table_kernel<<<blocks, 256, 0, on>>>(w, ldw, s0, se, m, slabs, order, c, scales,
+                                                   zeros, tabf, tsbad);
+      };
       for (long long s0 = 0, si = 0; s0 < n; s0 += SBL, ++si) {
         const long long se = std::min(n, s0 + SBL);
+        if (jit_tab) {
+          if (si == 0) {
+            build_table(s0, se, st);
+          } else {  // fork: the build runs beside this super-block's GEMM
+            cudaEventRecord(ev[0], st);
+            cudaStreamWaitEvent(aux, ev[0], 0);
+            build_table(s0, se, aux);
+            cudaEventRecord(ev[1], aux);
+          }
+        }
         if (si > 0) {
           bool done = tc_gemm2_presplit(se - s0, m, s0, 1.0f,
                                         reinterpret_cast<const float*>(ghi) + s0 * n,
@@ -798,14 +898,18 @@ void gptq_sweep_g(const float* w, long long ldw, long long n, long long m, const
                           acc + s0 * m, m, false, st);
           mark('g');
         }
+        if (jit_tab && si > 0) cudaStreamWaitEvent(st, ev[1], 0);  // join
         for (long long ib = s0; ib < se; ib += B) {
           const int bsz = int(std::min(se, ib + B) - ib);
+          const long long tb = (ib - s0) / B;
           launch_inblock4(w, ldw, order, reinterpret_cast<const float*>(acc), si >= 1,
                           reinterpret_cast<const float*>(gpl), gtt,
                           reinterpret_cast<const float*>(dpl[0]) + s0, int(ib - s0),
                           reinterpret_cast<float*>(dpl[0]) + ib, dhi[0] + ib, dlo[0] + ib, c,
                           scales, zeros, n, m, ib, bsz, codes, w_hat, ldo, n, ib == trace_ib,
-                          pdl_on && ib > 0, st);
+                          pdl_on && ib > 0, st,
+                          jit_tab ? tabf + tb * slabs * kB * l4::kCols4 : nullptr,
+                          jit_tab ? tsbad + tb * slabs : nullptr);
           mark('i');
         }
       }
@@ -885,11 +989,13 @@ template void gptq_sweep_g<float>(const float*, long long, long long, long long,
                                   const float*, const float*, const float*, const int32_t*, const QCfg&,
                                   const float*, const int32_t*, long long, int16_t*, float*,
                                   long long, float*, float* const[2], float* const[2],
-                                  float* const[2], int*, cudaStream_t);
+                                  float* const[2], int*, cudaStream_t, void*, cudaStream_t,
+                                  cudaEvent_t*);
 template void gptq_sweep_g<double>(const float*, long long, long long, long long, const double*,
                                    const float*, const double*, const float*, const int32_t*, const QCfg&,
                                    const float*, const int32_t*, long long, int16_t*, float*,
                                    long long, double*, double* const[2], float* const[2],
-                                   float* const[2], int*, cudaStream_t);
+                                   float* const[2], int*, cudaStream_t, void*, cudaStream_t,
+                                   cudaEvent_t*);
 
 }  // namespace ocwg
