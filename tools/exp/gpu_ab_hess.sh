@@ -1,0 +1,18 @@
+mkdir -p gpurun_out
+L=paper_2603_28845_b200/lib
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scale.py -q -x --timeout 600 -k "hessian or c2 or gram or accumulate" > gpurun_out/t_abh.log 2>&1; echo "rc=$?" >> gpurun_out/t_abh.log
+cp $L/libocwg.so $L/libocwg_new.so
+rm -f gpurun_out/ab_hess.log
+for i in 1 2 3; do
+  for v in new prev; do
+    cp $L/libocwg_$v.so $L/libocwg.so
+    (echo -n "$v "; timeout 300 python tools/hess_time.py 2>&1 | tail -1) >> gpurun_out/ab_hess.log
+    timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 0 --no-dropin > gpurun_out/ab_b.log 2>&1
+    python -c "
+import json
+for l in open('gpurun_out/ab_b.log'):
+    if l.startswith('{'): d=json.loads(l); print('$v step', round(d['ms_per_step'],4), round(d['breakdown_ms']['hessian'],4), d['clocks']['sm_mhz'])
+" >> gpurun_out/ab_hess.log
+  done
+done
+cp $L/libocwg_new.so $L/libocwg.so
