@@ -1,7 +1,7 @@
 # A/B of the working-tree library (libocwg.so) against libocwg_prev.so on one box
 mkdir -p gpurun_out
 L=paper_2603_28845_b200/lib
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scale.py tests/test_gpu_layers.py -q -x --timeout 600 > gpurun_out/t_ab.log 2>&1; echo "rc=$?" >> gpurun_out/t_ab.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_scale.py tests/test_gpu_layers.py tests/test_gpu_macro.py -q -x --timeout 600 > gpurun_out/t_ab.log 2>&1; echo "rc=$?" >> gpurun_out/t_ab.log
 cp $L/libocwg.so $L/libocwg_new.so
 rm -f gpurun_out/ab_lib.log
 for i in 1 2 3; do
