@@ -29,7 +29,7 @@ namespace {
 
 // One context per host thread (concurrent calls).
 // Arithmetic: OCWG_FP32 by default -- tensor-core statistics (bf16 parts, fp32
-// per 2048-token window, fp64 across), fp32 Cholesky and 3xTF32 sweep: codes
+// per 8192-token window, fp64 across), fp32 Cholesky and 3xTF32 sweep: codes
 // >= 99.9 % identical to the reference's fp64 path, H within 1e-5 of it.
 // OCW_GPU_PRECISION=fp64 selects the reference's arithmetic class (fp64
 // factorisation, sweep and statistics) for bit-level comparisons.
