@@ -144,7 +144,7 @@ int ocwg_unpack_uniform(ocwg_ctx* ctx, const uint8_t* payload, uint64_t len, uin
  * OCWG_FP32 precision (default): tcgen05 tensor cores on bf16 parts of the
  * inputs (Xp = P1 + P2, X - Xp = D1 + D2; gram = P1'P1 + P1'P2 + P2'P1,
  * cross = P1'D1 + P1'D2 + P2'D1; fp32 accumulation per 8192 tokens, fp64
- * across), |dH_ij| <~ 1e-5 sqrt(H_ii H_jj).  OCWG_FP64: fp64 SIMT GEMMs. */
+ * across), |dH_ij| <~ 1e-5 sqrt(H_ii H_jj).  OCWG_FP64: fp64 GEMMs (DMMA tensor cores). */
 int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert, uint64_t rows,
                           uint64_t dim, double* gram, double* cross, uint64_t* token_count);
 /* Hessian of bf16 calibration tokens on the tensor cores: H (+)= X^T X.
