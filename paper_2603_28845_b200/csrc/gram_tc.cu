@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "tc_ptx.cuh"
@@ -73,6 +74,7 @@ struct alignas(64) GramParams {
   int seg_a[2][3], seg_b[2][3];  // [kind][segment] -> map index
   void* out[2];          // gram, cross (dim x dim, row-major)
   int accumulate;
+  int serp;              // serpentine token order across waves
 };
 
 // upper 256 x 256 tiles (bi <= bj), column block by column block
@@ -186,13 +188,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (u < 0) break;
         const Unit x = decode(p, u);
         const int arow = x.bi * 256 + int(rank) * TM, bcol = x.bj * 256 + int(rank) * TNH;
-        int seg = int(x.kb0 / p.kb_seg);
-        long long kk = x.kb0 - seg * p.kb_seg;  // k-block within the segment
-        for (long long kb = x.kb0; kb < x.kb1; ++kb) {
+        // serpentine: units of odd waves (u / pairs) walk their tokens backwards,
+        // starting where the previous wave's units ended -- that stretch of X is
+        // still in L2 (DRAM read per launch 5.4 -> 4.3 GB at C2)
+        const bool rev = p.serp && ((u / int(gridDim.x >> 1)) & 1);
+        int seg = int((rev ? x.kb1 - 1 : x.kb0) / p.kb_seg);
+        long long kk = (rev ? x.kb1 - 1 : x.kb0) - seg * p.kb_seg;  // k-block within the segment
+        for (long long i = x.kb0; i < x.kb1; ++i) {
           const int t0 = int(kk * TK);
           const CUtensorMap* ma = &p.maps[p.seg_a[x.kind][seg]];
           const CUtensorMap* mb = &p.maps[p.seg_b[x.kind][seg]];
-          if (++kk == p.kb_seg) {
+          if (rev) {
+            if (--kk < 0) {
+              kk = p.kb_seg - 1;
+              --seg;
+            }
+          } else if (++kk == p.kb_seg) {
             kk = 0;
             ++seg;
           }
@@ -455,6 +466,8 @@ int gram_tc(const GramSpec& s, void* ws, size_t ws_bytes, cudaStream_t st) {
   p.out[0] = s.gram;
   p.out[1] = s.cross;
   p.accumulate = s.accumulate ? 1 : 0;
+  p.serp = 1;
+  if (const char* e = getenv("OCWG_GRAM_SERP")) p.serp = atoi(e);  // A/B switch
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int npairs_hw = sms / 2;
