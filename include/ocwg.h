@@ -185,6 +185,33 @@ int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, const
                         const ocwg_qep_options* qep, int16_t* codes, float* scales,
                         int32_t* zeros, float* w_hat);
 
+/* ---- jointq.hpp (the format-preserving refiner of GPTQ output)
+ * W is N x M (rows x cols, the QuantizedMatrix orientation), X is T x N fp32
+ * (T calibration rows; X cols == W rows).  Objective (jointq.hpp:18-20):
+ *   ||X What - X W||_F^2 + T lambda ||What - W||_F^2.
+ * jointq_refine (jointq.cpp:169-255): codes / scales / zeros are read and
+ * overwritten with the refined matrix (same format).  trace receives the
+ * objective at entry and after each accepted move in the reference's move
+ * order (first trace_cap entries; *trace_len = total entries, 0 if the move log
+ * overflowed); *accepted_moves and *passes as JointqResult.  Searches of
+ * independent column blocks (per-group grids) run concurrently, one CTA each;
+ * the acceptance threshold uses the block's own running objective. */
+int ocwg_jointq_refine(ocwg_ctx* ctx, const float* w, uint64_t n, uint64_t m, const float* x,
+                       uint64_t tokens, const ocwg_quant_config* cfg, int16_t* codes,
+                       float* scales, int32_t* zeros, double lambda, int max_passes,
+                       int move_radius, double* trace, uint64_t trace_cap, uint64_t* trace_len,
+                       uint64_t* accepted_moves, int* passes);
+/* jointq_objective (jointq.cpp:160-167), fp64 */
+int ocwg_jointq_objective(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
+                          const int32_t* zeros, const float* w, uint64_t n, uint64_t m,
+                          const float* x, uint64_t tokens, const ocwg_quant_config* cfg,
+                          double lambda, double* out);
+/* jointq_optimal_group_scale (jointq.cpp:169-175): the 1-D optimum of one group's scale */
+int ocwg_jointq_optimal_group_scale(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
+                                    const int32_t* zeros, const float* w, uint64_t n, uint64_t m,
+                                    const float* x, uint64_t tokens, const ocwg_quant_config* cfg,
+                                    double lambda, uint64_t group, double* out);
+
 /* ---- end-to-end layer quantize from calibration tokens (north_star call) --
  * W (N x M fp32) + X (T x N bf16) -> codes, grids, dequantized W and the
  * packed OCW1 payload.  Any output may be NULL.  h_out (N x N fp32) returns

@@ -25,7 +25,7 @@ FLAGS="-std=c++20 -O2 -fPIC -Wall -Wextra -Wno-unused-parameter -I$REF/include -
 SRCS="$REF/src/matrix.cpp $REF/src/quant.cpp $REF/src/stats.cpp $REF/src/layerwise.cpp"
 # autobit.cpp (candidate_grid / estimate_error) uses std::function
 # without including <functional>; it is force-included, the source is unmodified
-$CXX $FLAGS -shared -o "$OUT/libocw_ref.so" $SRCS "$REF/src/autobit.cpp" -include functional \
+$CXX $FLAGS -shared -o "$OUT/libocw_ref.so" $SRCS "$REF/src/autobit.cpp" "$REF/src/jointq.cpp" -include functional \
     "$HERE/ref_capi.cpp" -ldl
 # container.cpp (OCW1 writer / parser) needs nlohmann/json: the
 # image ships 3.11.3 inside cudnn_frontend; without it the container checker is
@@ -39,4 +39,7 @@ fi
 for t in test_core test_layerwise; do
   $CXX $FLAGS -o "$OUT/ref_$t" "$REF/tests/test_main.cpp" "$REF/tests/$t.cpp" $SRCS -ldl
 done
-echo "build_ref: built $OUT/{libocw_ref.so,ref_test_core,ref_test_layerwise}"
+# jointq.cpp (the refiner of GPTQ output) and its own unit tests
+$CXX $FLAGS -o "$OUT/ref_test_jointq" "$REF/tests/test_main.cpp" "$REF/tests/test_jointq.cpp" $SRCS \
+    "$REF/src/jointq.cpp" -ldl
+echo "build_ref: built $OUT/{libocw_ref.so,ref_test_core,ref_test_layerwise,ref_test_jointq}"

@@ -39,6 +39,12 @@ _SIGS = {
     "ocwref_qep_target": (_I, [_P, _P, _P, _U64, _U64, C.c_double, C.c_double, _P]),
     "ocwref_quantize_layer": (_I, [_P, _P, _P, _U64, _U64, _I, _I, _I, _I, _U64, _I, _I, C.c_double,
                                    _U64, _I, C.c_double, C.c_double, _P, _P, _P]),
+    "ocwref_jointq_refine": (_I, [_P, _U64, _U64, _P, _U64, _I, _I, _I, _U64, _P, _P, _P,
+                                  C.c_double, _I, _I, _P, _U64, _P, _P, _P]),
+    "ocwref_jointq_objective": (_I, [_P, _P, _P, _P, _U64, _U64, _P, _U64, _I, _I, _I, _U64,
+                                     C.c_double, _P]),
+    "ocwref_jointq_optimal_group_scale": (_I, [_P, _P, _P, _P, _U64, _U64, _P, _U64, _I, _I, _I,
+                                               _U64, C.c_double, _U64, _P]),
 }
 
 _lib = None
@@ -296,3 +302,39 @@ def roundtrip_ocw(data: bytes) -> bytes:
     if st != 0:
         raise RuntimeError(l.ocwref_container_error().decode())
     return out[:ln.value].tobytes()
+
+
+# ---------------------------------------------------------------- jointq.cpp
+def jointq_refine(codes, scales, zeros, w, x, bits, scheme, gran, group, lambda_=0.2,
+                  max_passes=8, radius=1, trace_cap=1 << 20):
+    """jointq.cpp:177-255: (codes, scales, zeros, trace, accepted_moves, passes)."""
+    w, x = _f32(w), _f32(x)
+    codes = np.ascontiguousarray(codes, np.int16).copy()
+    s, z = _f32(scales).copy(), np.ascontiguousarray(zeros, np.int32).copy()
+    trace = np.zeros(trace_cap, np.float64)
+    tl, acc, ps = C.c_size_t(), C.c_size_t(), C.c_int()
+    _ck(lib().ocwref_jointq_refine(_p(w), w.shape[0], w.shape[1], _p(x), x.shape[0], bits, scheme,
+                                   gran, group, _p(codes), _p(s), _p(z), lambda_, max_passes, radius,
+                                   _p(trace), trace_cap, C.byref(tl), C.byref(acc), C.byref(ps)))
+    return codes, s, z, trace[:min(tl.value, trace_cap)].copy(), int(acc.value), int(ps.value)
+
+
+def jointq_objective(codes, scales, zeros, w, x, bits, scheme, gran, group, lambda_) -> float:
+    w, x = _f32(w), _f32(x)
+    out = C.c_double()
+    _ck(lib().ocwref_jointq_objective(_p(np.ascontiguousarray(codes, np.int16)), _p(_f32(scales)),
+                                      _p(np.ascontiguousarray(zeros, np.int32)), _p(w), w.shape[0],
+                                      w.shape[1], _p(x), x.shape[0], bits, scheme, gran, group,
+                                      lambda_, C.byref(out)))
+    return float(out.value)
+
+
+def jointq_optimal_group_scale(codes, scales, zeros, w, x, bits, scheme, gran, group, lambda_,
+                               g) -> float:
+    w, x = _f32(w), _f32(x)
+    out = C.c_double()
+    _ck(lib().ocwref_jointq_optimal_group_scale(
+        _p(np.ascontiguousarray(codes, np.int16)), _p(_f32(scales)),
+        _p(np.ascontiguousarray(zeros, np.int32)), _p(w), w.shape[0], w.shape[1], _p(x), x.shape[0],
+        bits, scheme, gran, group, lambda_, g, C.byref(out)))
+    return float(out.value)

@@ -17,6 +17,7 @@
 
 #include "ocw/errors.hpp"
 #include "ocw/eigen_map.hpp"
+#include "ocw/jointq.hpp"
 #include "ocw/layerwise.hpp"
 #include "ocw/autobit.hpp"
 #include "ocw/quant.hpp"
@@ -297,6 +298,47 @@ int ocwref_quantize_layer(const float* w, const double* gram, const double* cros
     if (qep) o.qep = ocw::QepOptions{alpha, eta};
     auto q = ocw::quantize_layer(to_matrix(w, n, m), s, o);
     export_q(q, codes, scales, zeros);
+  });
+}
+
+// jointq.cpp:160-255: refine in place; trace up to trace_cap entries
+int ocwref_jointq_refine(const float* w, size_t rows, size_t cols, const float* x, size_t tokens,
+                         int bits, int scheme, int gran, size_t group, int16_t* codes,
+                         float* scales, int32_t* zeros, double lambda, int max_passes, int radius,
+                         double* trace, size_t trace_cap, size_t* trace_len, size_t* accepted,
+                         int* passes) {
+  return guard([&] {
+    const ocw::QuantConfig cfg = make_cfg(bits, scheme, gran, group);
+    const ocw::QuantizedMatrix q0 = import_q(codes, scales, zeros, rows, cols, cfg);
+    const ocw::JointqResult r = ocw::jointq_refine(q0, to_matrix(w, rows, cols),
+                                                   to_matrix(x, tokens, rows),
+                                                   {lambda, max_passes, radius});
+    export_q(r.refined, codes, scales, zeros);
+    *trace_len = r.objective_trace.size();
+    for (size_t t = 0; t < r.objective_trace.size() && t < trace_cap; ++t) trace[t] = r.objective_trace[t];
+    *accepted = r.accepted_moves;
+    *passes = r.passes;
+  });
+}
+int ocwref_jointq_objective(const int16_t* codes, const float* scales, const int32_t* zeros,
+                            const float* w, size_t rows, size_t cols, const float* x, size_t tokens,
+                            int bits, int scheme, int gran, size_t group, double lambda, double* out) {
+  return guard([&] {
+    const ocw::QuantConfig cfg = make_cfg(bits, scheme, gran, group);
+    *out = ocw::jointq_objective(import_q(codes, scales, zeros, rows, cols, cfg),
+                                 to_matrix(w, rows, cols), to_matrix(x, tokens, rows), lambda);
+  });
+}
+int ocwref_jointq_optimal_group_scale(const int16_t* codes, const float* scales,
+                                      const int32_t* zeros, const float* w, size_t rows,
+                                      size_t cols, const float* x, size_t tokens, int bits,
+                                      int scheme, int gran, size_t group_size, double lambda,
+                                      size_t group, double* out) {
+  return guard([&] {
+    const ocw::QuantConfig cfg = make_cfg(bits, scheme, gran, group_size);
+    *out = ocw::jointq_optimal_group_scale(import_q(codes, scales, zeros, rows, cols, cfg),
+                                           to_matrix(w, rows, cols), to_matrix(x, tokens, rows),
+                                           lambda, group);
   });
 }
 

@@ -227,6 +227,12 @@ _SIGS = {
     "ocwg_debug_split_dev": (C.c_int, [_P, _P, _P, _U64, _U64, _U64, _P, _P, _P, _P, _P]),
     "ocwg_debug_gram_dev": (C.c_int, [_P, _P, C.c_int, _U64, _U64, _U64, C.c_int, _P, _P, C.c_int, _P,
                                       _P, _P, _P, C.c_int, C.c_int, C.c_int64]),
+    "ocwg_jointq_refine": (C.c_int, [_P, _P, _U64, _U64, _P, _U64, C.POINTER(_QCfg), _P, _P, _P,
+                                     C.c_double, C.c_int, C.c_int, _P, _U64, _P, _P, _P]),
+    "ocwg_jointq_objective": (C.c_int, [_P, _P, _P, _P, _P, _U64, _U64, _P, _U64, C.POINTER(_QCfg),
+                                        C.c_double, _P]),
+    "ocwg_jointq_optimal_group_scale": (C.c_int, [_P, _P, _P, _P, _P, _U64, _U64, _P, _U64,
+                                                  C.POINTER(_QCfg), C.c_double, _U64, _P]),
     "ocwg_launch_count": (_U64, [_P]),
     "ocwg_debug_profile": (C.c_int, [_P, C.c_int, _P]),
     "ocwg_debug_gemm": (C.c_int, [_P, C.c_int, _U64, _U64, _U64, C.c_double, _P, _U64, C.c_int, _P,
@@ -371,6 +377,75 @@ def activation_objective(w, w_hat, h, device: int = 0) -> float:
     _check(lib().ocwg_activation_objective(context(device).handle, _ptr(w), _ptr(w_hat), _ptr(h),
                                            w.shape[0], w.shape[1], C.byref(out)))
     return float(out.value)
+
+
+# ------------------------------------------------------------------ jointq.hpp
+@dataclass
+class JointqOptions:
+    """jointq.hpp:9-13"""
+    lambda_: float = 0.2
+    max_passes: int = 8
+    move_radius: int = 1
+
+
+@dataclass
+class JointqResult:
+    """jointq.hpp:27-32"""
+    refined: "QuantizedMatrix"
+    objective_trace: np.ndarray
+    accepted_moves: int
+    passes: int
+
+
+def _jq_inputs(q: "QuantizedMatrix", w, x):
+    w, x = _f32(w), _f32(x)
+    if w.shape != (q.rows, q.cols):
+        raise InvalidInput("jointq: quantized shape does not match W")
+    if x.ndim != 2 or x.shape[1] != w.shape[0]:
+        raise InvalidInput("jointq: X cols must equal W rows")
+    codes = np.ascontiguousarray(q.codes, np.int16).reshape(q.rows, q.cols)
+    return (w, x, codes.copy(), np.ascontiguousarray(q.scales, np.float32).copy(),
+            np.ascontiguousarray(q.zeros, np.int32).copy())
+
+
+def jointq_objective(q: "QuantizedMatrix", w, x, lambda_: float, device: int = 0) -> float:
+    """jointq_objective (jointq.cpp:160-167): ||X What - X W||^2 + n lambda ||What - W||^2."""
+    w, x, codes, s, z = _jq_inputs(q, w, x)
+    c = q.config._c()
+    out = C.c_double()
+    _check(lib().ocwg_jointq_objective(context(device).handle, _ptr(codes), _ptr(s), _ptr(z), _ptr(w),
+                                       q.rows, q.cols, _ptr(x), x.shape[0], C.byref(c), lambda_,
+                                       C.byref(out)))
+    return float(out.value)
+
+
+def jointq_optimal_group_scale(q: "QuantizedMatrix", w, x, lambda_: float, group: int,
+                               device: int = 0) -> float:
+    """jointq_optimal_group_scale (jointq.cpp:169-175)."""
+    w, x, codes, s, z = _jq_inputs(q, w, x)
+    c = q.config._c()
+    out = C.c_double()
+    _check(lib().ocwg_jointq_optimal_group_scale(context(device).handle, _ptr(codes), _ptr(s), _ptr(z),
+                                                 _ptr(w), q.rows, q.cols, _ptr(x), x.shape[0],
+                                                 C.byref(c), lambda_, group, C.byref(out)))
+    return float(out.value)
+
+
+def jointq_refine(q0: "QuantizedMatrix", w, x, opts: JointqOptions = JointqOptions(),
+                  device: int = 0, trace_cap: int = 1 << 20) -> JointqResult:
+    """jointq_refine (jointq.cpp:177-255) on the GPU (csrc/jointq.cu)."""
+    w, x, codes, s, z = _jq_inputs(q0, w, x)
+    c = q0.config._c()
+    trace = np.zeros(max(1, trace_cap), np.float64)
+    tlen, acc, passes = C.c_uint64(), C.c_uint64(), C.c_int()
+    _check(lib().ocwg_jointq_refine(context(device).handle, _ptr(w), q0.rows, q0.cols, _ptr(x),
+                                    x.shape[0], C.byref(c), _ptr(codes), _ptr(s), _ptr(z),
+                                    opts.lambda_, opts.max_passes, opts.move_radius, _ptr(trace),
+                                    trace.size, C.byref(tlen), C.byref(acc), C.byref(passes)))
+    if tlen.value == 0 or tlen.value > trace.size:
+        raise CudaError(f"jointq_refine: objective trace unavailable ({tlen.value} entries)")
+    refined = QuantizedMatrix(q0.rows, q0.cols, q0.config, codes, s, z)
+    return JointqResult(refined, trace[:tlen.value].copy(), int(acc.value), int(passes.value))
 
 
 # ------------------------------------------------------------------ OCW1 uniform payload

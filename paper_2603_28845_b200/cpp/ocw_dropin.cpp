@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "ocw/errors.hpp"
+#include "ocw/jointq.hpp"
 #include "ocw/layerwise.hpp"
 #include "ocw/quant.hpp"
 #include "ocw/stats.hpp"
@@ -346,6 +347,87 @@ QuantizedMatrix quantize_layer(const Matrix& w, const CalibStats& stats,
                             s.data(), z.data(), nullptr));
   q.grids = grids_of(s, z, cfg);
   return q;
+}
+
+
+// ------------------------------------------------------------------ jointq.hpp
+namespace {
+void jq_validate(const QuantizedMatrix& q, const Matrix& w, const Matrix& x) {  // jointq.cpp:42-58
+  q.config.validate();
+  if (q.rows != w.rows || q.cols != w.cols)
+    throw invalid_input("jointq: quantized shape does not match W");
+  if (x.cols != w.rows) throw invalid_input("jointq: X cols must equal W rows");
+  if (q.codes.size() != q.rows * q.cols || q.grids.size() != q.group_count())
+    throw invalid_input("jointq: malformed quantized matrix (expect the uniform GPTQ format)");
+  for (size_t i = 0; i < q.rows; ++i)
+    for (size_t j = 0; j < q.cols; ++j) {
+      const QuantGrid& g = q.grids[q.group_index(i, j)];
+      const int code = q.codes[i * q.cols + j];
+      if (code < g.qmin || code > g.qmax) throw invalid_input("jointq: code outside the codebook range");
+    }
+}
+}  // namespace
+
+double jointq_objective(const QuantizedMatrix& q, const Matrix& w, const Matrix& x, double lambda) {
+  if (lambda < 0.0) throw invalid_input("jointq_objective: lambda must be >= 0");
+  if (q.rows != w.rows || q.cols != w.cols || x.cols != w.rows)
+    throw invalid_input("jointq_objective: shape mismatch");
+  const ocwg_quant_config c = cc(q.config);
+  std::vector<float> s;
+  std::vector<int32_t> z;
+  split_grids(q, s, z);
+  double out = 0.0;
+  check(ocwg_jointq_objective(ctx(), q.codes.data(), s.data(), z.data(), w.data.data(), w.rows,
+                              w.cols, x.data.data(), x.rows, &c, lambda, &out));
+  return out;
+}
+
+double jointq_optimal_group_scale(const QuantizedMatrix& q, const Matrix& w, const Matrix& x,
+                                  double lambda, size_t group) {
+  jq_validate(q, w, x);
+  const ocwg_quant_config c = cc(q.config);
+  std::vector<float> s;
+  std::vector<int32_t> z;
+  split_grids(q, s, z);
+  double out = 0.0;
+  check(ocwg_jointq_optimal_group_scale(ctx(), q.codes.data(), s.data(), z.data(), w.data.data(),
+                                        w.rows, w.cols, x.data.data(), x.rows, &c, lambda, group,
+                                        &out));
+  return out;
+}
+
+JointqResult jointq_refine(const QuantizedMatrix& q0, const Matrix& w, const Matrix& x,
+                           const JointqOptions& opts) {
+  jq_validate(q0, w, x);
+  if (opts.lambda < 0.0) throw invalid_input("jointq_refine: lambda must be >= 0");
+  if (opts.move_radius < 1) throw invalid_input("jointq_refine: move_radius must be >= 1");
+  const ocwg_quant_config c = cc(q0.config);
+  std::vector<float> s;
+  std::vector<int32_t> z;
+  split_grids(q0, s, z);
+  JointqResult res;
+  res.refined = q0;
+  // at most one accepted move per group refit, cell and zero step per pass
+  const uint64_t bound =
+      uint64_t(std::max(0, opts.max_passes)) * (q0.rows * q0.cols + 2 * q0.grids.size()) + 1;
+  std::vector<double> trace(std::min<uint64_t>(bound, uint64_t(1) << 24));
+  uint64_t len = 0, acc = 0;
+  int passes = 0;
+  check(ocwg_jointq_refine(ctx(), w.data.data(), w.rows, w.cols, x.data.data(), x.rows, &c,
+                           res.refined.codes.data(), s.data(), z.data(), opts.lambda,
+                           opts.max_passes, opts.move_radius, trace.data(), trace.size(), &len,
+                           &acc, &passes));
+  if (len == 0 || len > trace.size())
+    throw std::runtime_error("jointq_refine: objective trace overflow");
+  for (size_t g = 0; g < res.refined.grids.size(); ++g) {
+    res.refined.grids[g].scale = s[g];
+    res.refined.grids[g].zero_point = z[g];
+  }
+  trace.resize(len);
+  res.objective_trace = std::move(trace);
+  res.accepted_moves = size_t(acc);
+  res.passes = passes;
+  return res;
 }
 
 }  // namespace ocw

@@ -827,6 +827,186 @@ int ocwg_activation_objective(ocwg_ctx* ctx, const float* w, const float* w_hat,
   });
 }
 
+// ------------------------------------------------------------------ jointq.hpp
+namespace {
+void jq_check_codes(const ocwg_quant_config* cfg, const int16_t* codes, uint64_t n, uint64_t m) {
+  const QCfg c = qcfg(cfg, m);  // jointq.cpp:50-56
+  for (uint64_t t = 0; t < n * m; ++t)
+    if (codes[t] < c.qmin || codes[t] > c.qmax)
+      fail(OCWG_INVALID_INPUT, "jointq: code outside the codebook range");
+}
+}  // namespace
+
+int ocwg_jointq_refine(ocwg_ctx* ctx, const float* w, uint64_t n, uint64_t m, const float* x,
+                       uint64_t tokens, const ocwg_quant_config* cfg, int16_t* codes,
+                       float* scales, int32_t* zeros, double lambda, int max_passes,
+                       int move_radius, double* trace, uint64_t trace_cap, uint64_t* trace_len,
+                       uint64_t* accepted_moves, int* passes) {
+  return guard([&] {
+    validate(cfg);
+    jq_check_codes(cfg, codes, n, m);
+    if (!(lambda >= 0.0)) fail(OCWG_INVALID_INPUT, "jointq_refine: lambda must be >= 0");
+    if (move_radius < 1) fail(OCWG_INVALID_INPUT, "jointq_refine: move_radius must be >= 1");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    const uint64_t ng = group_count(cfg, n, m);
+    const QCfg c = qcfg(cfg, m);
+    const long long units = (long long)jointq_units(c, (long long)m);
+    const long long max_cells = std::max<long long>(
+        1, c.gran == 0 ? (long long)(n * m) : c.gran == 1 ? (long long)m : c.group);
+    const long long log_cap = std::max<long long>(4096, (1LL << 24) / units);
+    double obj0 = 0.0;
+    std::vector<int> cnt(units, 0), fz(units, 0);
+    std::vector<std::pair<unsigned long long, double>> moves;
+    bool truncated = false;
+    if (n * m > 0 && max_passes > 0) {
+      Arena ar(ctx);
+      const size_t ox = ar.reserve(std::max<uint64_t>(1, tokens * n) * 4), ow = ar.reserve(n * m * 4),
+                   oc = ar.reserve(n * m * 2), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4),
+                   oh = ar.reserve(n * n * 8), oe = ar.reserve(n * m * 8), og = ar.reserve(n * m * 8),
+                   op = ar.reserve(256 * 8), odb = ar.reserve(size_t(units * max_cells) * 8),
+                   olk = ar.reserve(size_t(units * log_cap) * 8),
+                   old = ar.reserve(size_t(units * log_cap) * 8), olc = ar.reserve(units * 4),
+                   ofz = ar.reserve(units * 4);
+      ar.commit();
+      if (tokens) h2d(ar.at<float>(ox), x, tokens * n * 4, ctx);
+      else ck(cudaMemsetAsync(ar.at<float>(ox), 0, 4, ctx->stream), "memset");
+      h2d(ar.at<float>(ow), w, n * m * 4, ctx);
+      h2d(ar.at<int16_t>(oc), codes, n * m * 2, ctx);
+      h2d(ar.at<float>(os), scales, ng * 4, ctx);
+      h2d(ar.at<int32_t>(oz), zeros, ng * 4, ctx);
+      obj0 = jointq_setup(ar.at<float>(ox), (long long)tokens, ar.at<float>(ow), (long long)n,
+                          (long long)m, c, ar.at<int16_t>(oc), ar.at<float>(os), ar.at<int32_t>(oz),
+                          lambda, ar.at<double>(oh), ar.at<double>(oe), ar.at<double>(og),
+                          ar.at<double>(op), ctx->stream);
+      const int r = jointq_search(ar.at<float>(ow), (long long)n, (long long)m, c, ar.at<int16_t>(oc),
+                                  ar.at<float>(os), ar.at<int32_t>(oz), ar.at<double>(oh),
+                                  ar.at<double>(oe), ar.at<double>(og), ar.at<double>(odb), max_cells,
+                                  obj0, max_passes, move_radius, ar.at<unsigned long long>(olk),
+                                  ar.at<double>(old), ar.at<int>(olc), ar.at<int>(ofz), log_cap,
+                                  ctx->stream);
+      if (r != 0) fail(OCWG_CUDA_ERROR, "jointq_refine: search kernel launch failed");
+      d2h(codes, ar.at<int16_t>(oc), n * m * 2, ctx);
+      d2h(scales, ar.at<float>(os), ng * 4, ctx);
+      d2h(zeros, ar.at<int32_t>(oz), ng * 4, ctx);
+      d2h(cnt.data(), ar.at<int>(olc), units * 4, ctx);
+      d2h(fz.data(), ar.at<int>(ofz), units * 4, ctx);
+      ck(cudaStreamSynchronize(ctx->stream), "sync");
+      // the reference's move order: keys (pass, phase, index) across the units
+      std::vector<unsigned long long> kbuf;
+      std::vector<double> dbuf;
+      for (long long u = 0; u < units; ++u) {
+        const long long k = std::min<long long>(cnt[u], log_cap);
+        truncated |= cnt[u] > log_cap;
+        if (k == 0) continue;
+        kbuf.resize(k);
+        dbuf.resize(k);
+        ck(cudaMemcpy(kbuf.data(), ar.at<unsigned long long>(olk) + u * log_cap, k * 8,
+                      cudaMemcpyDeviceToHost),
+           "D2H");
+        ck(cudaMemcpy(dbuf.data(), ar.at<double>(old) + u * log_cap, k * 8, cudaMemcpyDeviceToHost),
+           "D2H");
+        for (long long t = 0; t < k; ++t) moves.emplace_back(kbuf[t], dbuf[t]);
+      }
+      finish(ctx);
+    }
+    std::sort(moves.begin(), moves.end(),
+              [](const auto& a, const auto& b) { return a.first < b.first; });
+    uint64_t total = 0;
+    int fzmax = 0;
+    for (long long u = 0; u < (long long)cnt.size(); ++u) {
+      total += uint64_t(cnt[u]);
+      fzmax = std::max(fzmax, fz[u]);
+    }
+    if (accepted_moves) *accepted_moves = total;
+    // jointq.cpp:248-250: a pass without an accepted move ends the search
+    if (passes) *passes = (n * m == 0 || max_passes <= 0) ? std::max(0, std::min(1, max_passes))
+                          : (fzmax < max_passes ? fzmax + 1 : max_passes);
+    // trace: J at entry, then after each accepted move (0 entries: move log overflowed)
+    const uint64_t len = truncated ? 0 : total + 1;
+    if (trace_len) *trace_len = len;
+    if (trace && len) {
+      double j = obj0;
+      if (trace_cap > 0) trace[0] = j;
+      for (uint64_t t = 0; t < moves.size(); ++t) {
+        j += moves[t].second;
+        if (t + 1 < trace_cap) trace[t + 1] = j;
+      }
+    }
+  });
+}
+
+int ocwg_jointq_objective(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
+                          const int32_t* zeros, const float* w, uint64_t n, uint64_t m,
+                          const float* x, uint64_t tokens, const ocwg_quant_config* cfg,
+                          double lambda, double* out) {
+  return guard([&] {
+    validate(cfg);
+    if (!(lambda >= 0.0)) fail(OCWG_INVALID_INPUT, "jointq_objective: lambda must be >= 0");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    *out = 0.0;
+    if (n * m == 0) return;
+    const uint64_t ng = group_count(cfg, n, m);
+    const QCfg c = qcfg(cfg, m);
+    const long long chunk = std::max<long long>(1, std::min<long long>((long long)tokens,
+                                                                       (1LL << 26) / (long long)m));
+    Arena ar(ctx);
+    const size_t ox = ar.reserve(std::max<uint64_t>(1, tokens * n) * 4), ow = ar.reserve(n * m * 4),
+                 oc = ar.reserve(n * m * 2), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4),
+                 oe = ar.reserve(n * m * 8), oy = ar.reserve(size_t(chunk) * m * 8),
+                 op = ar.reserve(256 * 8);
+    ar.commit();
+    if (tokens) h2d(ar.at<float>(ox), x, tokens * n * 4, ctx);
+    h2d(ar.at<float>(ow), w, n * m * 4, ctx);
+    h2d(ar.at<int16_t>(oc), codes, n * m * 2, ctx);
+    h2d(ar.at<float>(os), scales, ng * 4, ctx);
+    h2d(ar.at<int32_t>(oz), zeros, ng * 4, ctx);
+    jointq_residual(ar.at<int16_t>(oc), ar.at<float>(os), ar.at<int32_t>(oz), ar.at<float>(ow),
+                    (long long)n, (long long)m, c, ar.at<double>(oe), ctx->stream);
+    *out = jointq_objective_dev(ar.at<float>(ox), (long long)tokens, (long long)n, (long long)m,
+                                ar.at<double>(oe), lambda, ar.at<double>(oy), chunk,
+                                ar.at<double>(op), ctx->stream);
+    finish(ctx);
+  });
+}
+
+int ocwg_jointq_optimal_group_scale(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
+                                    const int32_t* zeros, const float* w, uint64_t n, uint64_t m,
+                                    const float* x, uint64_t tokens, const ocwg_quant_config* cfg,
+                                    double lambda, uint64_t group, double* out) {
+  return guard([&] {
+    validate(cfg);
+    jq_check_codes(cfg, codes, n, m);
+    const uint64_t ng = group_count(cfg, n, m);
+    if (group >= ng) fail(OCWG_INVALID_INPUT, "jointq: group index out of range");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    begin(ctx);
+    const QCfg c = qcfg(cfg, m);
+    Arena ar(ctx);
+    const size_t ox = ar.reserve(std::max<uint64_t>(1, tokens * n) * 4), ow = ar.reserve(n * m * 4),
+                 oc = ar.reserve(n * m * 2), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4),
+                 oh = ar.reserve(n * n * 8), oe = ar.reserve(n * m * 8), og = ar.reserve(n * m * 8),
+                 op = ar.reserve(256 * 8);
+    ar.commit();
+    if (tokens) h2d(ar.at<float>(ox), x, tokens * n * 4, ctx);
+    else ck(cudaMemsetAsync(ar.at<float>(ox), 0, 4, ctx->stream), "memset");
+    h2d(ar.at<float>(ow), w, n * m * 4, ctx);
+    h2d(ar.at<int16_t>(oc), codes, n * m * 2, ctx);
+    h2d(ar.at<float>(os), scales, ng * 4, ctx);
+    h2d(ar.at<int32_t>(oz), zeros, ng * 4, ctx);
+    jointq_setup(ar.at<float>(ox), (long long)tokens, ar.at<float>(ow), (long long)n, (long long)m,
+                 c, ar.at<int16_t>(oc), ar.at<float>(os), ar.at<int32_t>(oz), lambda,
+                 ar.at<double>(oh), ar.at<double>(oe), ar.at<double>(og), ar.at<double>(op),
+                 ctx->stream);
+    *out = jointq_optimal_scale(ar.at<float>(ow), (long long)n, (long long)m, c, ar.at<int16_t>(oc),
+                                ar.at<float>(os), ar.at<int32_t>(oz), ar.at<double>(oh),
+                                ar.at<double>(oe), ar.at<double>(og), (long long)group,
+                                ar.at<double>(op), ctx->stream);
+    finish(ctx);
+  });
+}
+
 // ------------------------------------------------------------------ packing
 int ocwg_pack_uniform_dev(ocwg_ctx* ctx, const int16_t* codes, const float* scales,
                           const int32_t* zeros, uint64_t rows, uint64_t cols,

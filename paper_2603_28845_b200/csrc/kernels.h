@@ -222,4 +222,34 @@ void launch_f32_to_f64(const float* in, long long n, double* out, cudaStream_t s
 void activation_objective(const float* w, const float* w_hat, const float* h, long long n,
                           long long m, double* out_dev, double* ws, cudaStream_t st);
 
+
+// ---- JointQ refiner (jointq.cu; jointq.cpp:60-255) -------------------------
+// independent search units: column blocks (per_group) or one (per_channel / per_tensor)
+size_t jointq_units(const QCfg& c, long long m);
+// E = double(s (code - z)) - double(W)
+void jointq_residual(const int16_t* codes, const float* scales, const int32_t* zeros,
+                     const float* w, long long n, long long m, const QCfg& c, double* e,
+                     cudaStream_t st);
+// H_eff = X^T X + tokens lambda I, E = What - W, G = H_eff E (fp64, device); returns J at
+// entry.  part: 256 doubles of scratch.
+double jointq_setup(const float* x, long long tokens, const float* w, long long n, long long m,
+                    const QCfg& c, const int16_t* codes, const float* scales, const int32_t* zeros,
+                    double lambda, double* h, double* e, double* g, double* part, cudaStream_t st);
+// the local search (codes / scales / zeros refined in place); per unit: log of
+// (key, objective change) of the first log_cap accepted moves, the count, and the
+// first pass without a move.  dbuf: units * max_cells doubles.
+int jointq_search(const float* w, long long n, long long m, const QCfg& c, int16_t* codes,
+                  float* scales, int32_t* zeros, const double* h, double* e, double* g,
+                  double* dbuf, long long max_cells, double obj0, int max_passes, int radius,
+                  unsigned long long* log_key, double* log_delta, int* log_count, int* first_zero,
+                  long long log_cap, cudaStream_t st);
+double jointq_optimal_scale(const float* w, long long n, long long m, const QCfg& c,
+                            const int16_t* codes, const float* scales, const int32_t* zeros,
+                            const double* h, double* e, double* g, long long group, double* out,
+                            cudaStream_t st);
+// ||X E||^2 + tokens lambda ||E||^2 (X in token chunks; y: chunk * m doubles)
+double jointq_objective_dev(const float* x, long long tokens, long long n, long long m,
+                            const double* e, double lambda, double* y, long long chunk, double* part,
+                            cudaStream_t st);
+
 }  // namespace ocwg

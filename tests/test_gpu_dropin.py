@@ -1,4 +1,5 @@
 """The reference's OWN unit tests (proj/tests/test_core.cpp, test_layerwise.cpp,
+test_jointq.cpp,
 compiled unmodified by paper_2603_28845_b200/cpp/build_dropin.sh) linked
 against the C++ drop-in (ocw:: interface over libocwg.so) instead of the
 reference's src/{quant,stats,layerwise}.cpp -- every known-answer, exact-
@@ -15,7 +16,8 @@ LIB = ROOT / "paper_2603_28845_b200" / "lib"
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["dropin_test_core", "dropin_test_layerwise"])
+@pytest.mark.parametrize("name", ["dropin_test_core", "dropin_test_layerwise",
+                                  "dropin_test_jointq"])
 def test_reference_unit_tests_pass_on_gpu_dropin(name):
     exe = LIB / name
     if not exe.exists():
@@ -33,7 +35,9 @@ def test_dropin_exports_reference_interface():
                           text=True).stdout
     for fn in ["ocw::gptq_quantize(", "ocw::quantize_layer(", "ocw::accumulate_stats(",
                "ocw::gptq_order(", "ocw::calibrate_grids(", "ocw::quantize_matrix(",
-               "ocw::dequantize(", "ocw::qep_target(", "ocw::activation_objective("]:
+               "ocw::dequantize(", "ocw::qep_target(", "ocw::activation_objective(",
+               "ocw::jointq_refine(", "ocw::jointq_objective(",
+               "ocw::jointq_optimal_group_scale("]:
         assert fn in syms, fn
     libs = subprocess.run(["ldd", str(so)], capture_output=True, text=True).stdout
     assert "libocwg.so" in libs

@@ -1,7 +1,8 @@
 """Pin the oracle (CPU only).
 
 1. The reference's own hot-path tests (proj/tests/test_core.cpp,
-   test_layerwise.cpp), compiled unmodified against the oracle build, pass.
+   test_layerwise.cpp, and test_jointq.cpp for the f4 refiner), compiled
+   unmodified against the oracle build, pass.
 2. The numpy restatement agrees with the compiled reference on seeded inputs
    (bit-exact codes/grids/order; fp64-roundoff for U / H^-1 / stats).
 3. The committed golden fixtures (tests/golden/, made by
@@ -18,7 +19,7 @@ ROOT = Path(__file__).resolve().parent.parent
 GOLDEN = ROOT / "tests" / "golden"
 
 
-@pytest.mark.parametrize("name", ["ref_test_core", "ref_test_layerwise"])
+@pytest.mark.parametrize("name", ["ref_test_core", "ref_test_layerwise", "ref_test_jointq"])
 def test_reference_unit_tests_pass_on_oracle_build(ref, name):
     exe = ROOT / "oracle" / "_ref" / name
     if not exe.exists():
