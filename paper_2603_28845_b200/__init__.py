@@ -432,11 +432,13 @@ def jointq_optimal_group_scale(q: "QuantizedMatrix", w, x, lambda_: float, group
 
 
 def jointq_refine(q0: "QuantizedMatrix", w, x, opts: JointqOptions = JointqOptions(),
-                  device: int = 0, trace_cap: int = 1 << 20) -> JointqResult:
+                  device: int = 0) -> JointqResult:
     """jointq_refine (jointq.cpp:177-255) on the GPU (csrc/jointq.cu)."""
     w, x, codes, s, z = _jq_inputs(q0, w, x)
     c = q0.config._c()
-    trace = np.zeros(max(1, trace_cap), np.float64)
+    # at most one accepted move per group refit, cell and zero step per pass
+    bound = max(0, opts.max_passes) * (q0.rows * q0.cols + 2 * len(s)) + 1
+    trace = np.zeros(min(bound, 1 << 24), np.float64)
     tlen, acc, passes = C.c_uint64(), C.c_uint64(), C.c_int()
     _check(lib().ocwg_jointq_refine(context(device).handle, _ptr(w), q0.rows, q0.cols, _ptr(x),
                                     x.shape[0], C.byref(c), _ptr(codes), _ptr(s), _ptr(z),

@@ -868,6 +868,7 @@ int ocwg_jointq_refine(ocwg_ctx* ctx, const float* w, uint64_t n, uint64_t m, co
                    olk = ar.reserve(size_t(units * log_cap) * 8),
                    old = ar.reserve(size_t(units * log_cap) * 8), olc = ar.reserve(units * 4),
                    ofz = ar.reserve(units * 4);
+      const auto ta = std::chrono::steady_clock::now();
       ar.commit();
       if (tokens) h2d(ar.at<float>(ox), x, tokens * n * 4, ctx);
       else ck(cudaMemsetAsync(ar.at<float>(ox), 0, 4, ctx->stream), "memset");
@@ -875,6 +876,14 @@ int ocwg_jointq_refine(ocwg_ctx* ctx, const float* w, uint64_t n, uint64_t m, co
       h2d(ar.at<int16_t>(oc), codes, n * m * 2, ctx);
       h2d(ar.at<float>(os), scales, ng * 4, ctx);
       h2d(ar.at<int32_t>(oz), zeros, ng * 4, ctx);
+      const bool dbg = getenv("OCWG_DEBUG_JQ") != nullptr;
+      auto tnow = [&] {
+        if (dbg) cudaStreamSynchronize(ctx->stream);
+        return std::chrono::steady_clock::now();
+      };
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      const auto t0 = tnow();
+      if (dbg) fprintf(stderr, "jointq: alloc + H2D %.1f ms\n", ms(ta, t0));
       obj0 = jointq_setup(ar.at<float>(ox), (long long)tokens, ar.at<float>(ow), (long long)n,
                           (long long)m, c, ar.at<int16_t>(oc), ar.at<float>(os), ar.at<int32_t>(oz),
                           lambda, ar.at<double>(oh), ar.at<double>(oe), ar.at<double>(og),
@@ -886,6 +895,8 @@ int ocwg_jointq_refine(ocwg_ctx* ctx, const float* w, uint64_t n, uint64_t m, co
                                   ar.at<double>(old), ar.at<int>(olc), ar.at<int>(ofz), log_cap,
                                   ctx->stream);
       if (r != 0) fail(OCWG_CUDA_ERROR, "jointq_refine: search kernel launch failed");
+      const auto t2 = tnow();
+      if (dbg) fprintf(stderr, "jointq: setup + search %.1f ms\n", ms(t0, t2));
       d2h(codes, ar.at<int16_t>(oc), n * m * 2, ctx);
       d2h(scales, ar.at<float>(os), ng * 4, ctx);
       d2h(zeros, ar.at<int32_t>(oz), ng * 4, ctx);
@@ -909,6 +920,7 @@ int ocwg_jointq_refine(ocwg_ctx* ctx, const float* w, uint64_t n, uint64_t m, co
         for (long long t = 0; t < k; ++t) moves.emplace_back(kbuf[t], dbuf[t]);
       }
       finish(ctx);
+      if (dbg) fprintf(stderr, "jointq: results + logs %.1f ms\n", ms(t2, tnow()));
     }
     std::sort(moves.begin(), moves.end(),
               [](const auto& a, const auto& b) { return a.first < b.first; });

@@ -136,6 +136,83 @@ __device__ double delta_for(const JqArgs& a, const Cells& cl, const Prop& p, flo
   return warp_sum(delta);
 }
 
+// Per-group grids, one row per group: warp 0 keeps the row's cells in
+// registers (lane: columns j0 + lane + 32 t) while it evaluates that row's
+// proposals -- the same per-cell arithmetic and lane partition as opt_scale /
+// delta_for, without a global-memory round trip per proposal.  Reloaded after
+// every accepted move (the move rewrites E and G).
+constexpr int kRowT = 8;  // cells per lane: group_size <= 256
+struct RowCache {
+  double g[kRowT], e[kRowT];
+  float w[kRowT];
+  int c[kRowT];
+  double hii;
+  long long i, j0, j1;
+};
+__device__ __forceinline__ void load_row(const JqArgs& a, RowCache& r, long long i, long long j0,
+                                         long long j1) {
+  const int lane = threadIdx.x & 31;
+  r.i = i, r.j0 = j0, r.j1 = j1;
+  r.hii = a.h[i * a.n + i];
+#pragma unroll
+  for (int t = 0; t < kRowT; ++t) {
+    const long long j = j0 + lane + 32 * t;
+    if (j < j1) {
+      r.g[t] = a.g[i * a.m + j];
+      r.e[t] = a.e[i * a.m + j];
+      r.w[t] = a.w[i * a.m + j];
+      r.c[t] = a.codes[i * a.m + j];
+    } else {
+      r.g[t] = r.e[t] = 0.0, r.w[t] = 0.f, r.c[t] = 0;
+    }
+  }
+}
+__device__ __forceinline__ double opt_scale_row(const RowCache& r, long long mj, int mc, int z) {
+  const int lane = threadIdx.x & 31;
+  double num = 0.0, den = 0.0;
+#pragma unroll
+  for (int t = 0; t < kRowT; ++t) {
+    const long long j = r.j0 + lane + 32 * t;
+    if (j >= r.j1) continue;
+    const double cc = double((j == mj ? mc : r.c[t]) - z);
+    if (cc == 0.0) continue;
+    const double what = __dadd_rn(r.e[t], double(r.w[t]));
+    const double hf = __dsub_rn(r.g[t], __dmul_rn(r.hii, what));
+    const double dn = __dadd_rn(0.0, __dmul_rn(__dmul_rn(cc, r.hii), cc));
+    num = __dadd_rn(num, __dmul_rn(cc, hf));
+    den = __dadd_rn(den, dn);
+  }
+  num = warp_sum(num);
+  den = warp_sum(den);
+  if (den <= 0.0) return 0.0;
+  return -num / den;
+}
+__device__ __forceinline__ double delta_row(const RowCache& r, long long mj, int mc, float s, int z) {
+  const int lane = threadIdx.x & 31;
+  double delta = 0.0;
+#pragma unroll
+  for (int t = 0; t < kRowT; ++t) {
+    const long long j = r.j0 + lane + 32 * t;
+    if (j >= r.j1) continue;
+    const int code = j == mj ? mc : r.c[t];
+    const double fresh = __dsub_rn(__dmul_rn(double(s), double(code - z)), double(r.w[t]));
+    const double d = __dsub_rn(fresh, r.e[t]);
+    if (d == 0.0) continue;
+    double tt = __dmul_rn(__dmul_rn(2.0, d), r.g[t]);
+    tt = __dadd_rn(tt, __dmul_rn(__dmul_rn(d, r.hii), d));
+    delta = __dadd_rn(delta, tt);
+  }
+  return warp_sum(delta);
+}
+// the current code of column j of the cached row (from lane (j - j0) % 32)
+__device__ __forceinline__ int row_code(const RowCache& r, long long j) {
+  const int q = int(j - r.j0), tj = q >> 5;
+  int v = 0;
+#pragma unroll
+  for (int t = 0; t < kRowT; ++t) v = t == tj ? r.c[t] : v;
+  return __shfl_sync(0xffffffffu, v, q & 31);
+}
+
 struct JqShared {
   int op;  // 1: apply the move below, 2: exit
   long long group;
@@ -211,15 +288,17 @@ __global__ void __launch_bounds__(256) jq_search_kernel(JqArgs a) {
   double obj = a.obj0;
   int accepted = 0;
   int fz = a.max_passes;
+  RowCache row;
+  const bool fast = a.c.gran == 2 && uj1 - uj0 <= 32 * kRowT;  // one row per group, cached
   auto try_move = [&](long long group, const Prop& p, int z, unsigned long long key) -> bool {
     const Cells cl = cells_of(a, group);
-    const double raw = opt_scale(a, cl, p, z);
+    const double raw = fast ? opt_scale_row(row, p.mj, p.mc, z) : opt_scale(a, cl, p, z);
     float s_new = fp16_round(float(raw));
     if (!(s_new > 0.0f)) {
       if (raw > 0.0) s_new = kFp16MinPositive;
       else return false;
     }
-    const double delta = delta_for(a, cl, p, s_new, z);
+    const double delta = fast ? delta_row(row, p.mj, p.mc, s_new, z) : delta_for(a, cl, p, s_new, z);
     if (delta >= -a.tol * (1.0 + fabs(obj))) return false;
     if (lane == 0) {
       sh.op = 1, sh.group = group, sh.p = p, sh.s = s_new, sh.z = z;
@@ -236,6 +315,7 @@ __global__ void __launch_bounds__(256) jq_search_kernel(JqArgs a) {
       }
     }
     ++accepted;
+    if (fast) load_row(a, row, row.i, uj0, uj1);
     return true;
   };
   const Prop none{-1, -1, 0};
@@ -245,16 +325,19 @@ __global__ void __launch_bounds__(256) jq_search_kernel(JqArgs a) {
     // (A) scale refits with the current codes (jointq.cpp:205-210)
     for (long long t = 0; t < g_count; ++t) {
       const long long group = g_first + t * g_step;
+      if (fast) load_row(a, row, t, uj0, uj1);
       if (try_move(group, none, a.zeros[group], pk | group)) ++in_pass;
     }
     // (B) code moves, row-major; deltas -1, +1, -2, +2, ... (jointq.cpp:211-230)
-    for (long long i = 0; i < a.n; ++i)
+    for (long long i = 0; i < a.n; ++i) {
+      if (fast) load_row(a, row, i, uj0, uj1);
       for (long long j = uj0; j < uj1; ++j) {
         const long long group = group_of(a.c, i, j);
+        const int cur = fast ? row_code(row, j) : int(a.codes[i * a.m + j]);
         for (int r = 1; r <= a.radius; ++r) {
           bool done = false;
           for (int sg = -1; sg <= 1; sg += 2) {
-            const int c_new = int(a.codes[i * a.m + j]) + sg * r;
+            const int c_new = cur + sg * r;
             if (c_new < a.c.qmin || c_new > a.c.qmax) continue;
             if (try_move(group, Prop{i, j, c_new}, a.zeros[group],
                          pk | (1ull << 56) | (unsigned long long)(i * a.m + j))) {
@@ -266,10 +349,12 @@ __global__ void __launch_bounds__(256) jq_search_kernel(JqArgs a) {
           if (done) break;
         }
       }
+    }
     // (C) zero-point moves (asymmetric; jointq.cpp:232-246)
     if (a.c.scheme == 1) {
       for (long long t = 0; t < g_count; ++t) {
         const long long group = g_first + t * g_step;
+        if (fast) load_row(a, row, t, uj0, uj1);
         for (int dz = -1; dz <= 1; dz += 2) {
           const int z_new = a.zeros[group] + dz;
           if (z_new < a.c.qmin || z_new > a.c.qmax) continue;
@@ -292,6 +377,256 @@ __global__ void __launch_bounds__(256) jq_search_kernel(JqArgs a) {
   }
   __syncwarp();
   bar_named(1);
+}
+
+// ---- per-group grids (one row per group, group_size <= 256): speculative
+// parallel proposals.  A row's cells (g, e, w, codes, h_ii) sit in shared
+// memory; every thread evaluates one proposal of the row against the current
+// state, in the reference's own sequential order over the cells (the sums of
+// jointq.cpp:92-141, so each proposal's numbers are those of the reference);
+// the first accepted proposal in the reference's order (cell, then delta
+// -1, +1, -2, ...) is applied, and the row's remaining proposals are
+// re-evaluated against the new state.  Proposals before the first accepted
+// one were rejected, so they saw exactly the state the sequential search
+// would have shown them: the result equals the sequential search.
+constexpr int kRowMax = 256;
+struct RowSm {
+  double g[kRowMax], e[kRowMax], d[kRowMax];
+  float w[kRowMax];
+  int c[kRowMax];
+  double hii;
+  int best;
+  float s;
+  double delta;
+  int jp, cp, z;
+};
+
+// one proposal: code cp at column jp (jp < 0: none), zero point z
+__device__ bool eval_row_prop(const RowSm& r, int ncol, int jp, int cp, int z, double thr, float& s_out,
+                              double& delta_out) {
+  double num = 0.0, den = 0.0;  // jointq.cpp:95-118
+  for (int j = 0; j < ncol; ++j) {
+    const double cc = double((j == jp ? cp : r.c[j]) - z);
+    if (cc == 0.0) continue;
+    const double what = __dadd_rn(r.e[j], double(r.w[j]));
+    const double hf = __dsub_rn(r.g[j], __dmul_rn(r.hii, what));
+    num = __dadd_rn(num, __dmul_rn(cc, hf));
+    den = __dadd_rn(den, __dmul_rn(__dmul_rn(cc, r.hii), cc));
+  }
+  const double raw = den <= 0.0 ? 0.0 : -num / den;
+  float s = fp16_round(float(raw));  // jointq.cpp:178-183
+  if (!(s > 0.0f)) {
+    if (raw > 0.0) s = kFp16MinPositive;
+    else return false;
+  }
+  double delta = 0.0;  // jointq.cpp:122-141
+  for (int j = 0; j < ncol; ++j) {
+    const double fresh =
+        __dsub_rn(__dmul_rn(double(s), double((j == jp ? cp : r.c[j]) - z)), double(r.w[j]));
+    const double d = __dsub_rn(fresh, r.e[j]);
+    if (d == 0.0) continue;
+    delta = __dadd_rn(delta, __dmul_rn(__dmul_rn(2.0, d), r.g[j]));
+    delta = __dadd_rn(delta, __dmul_rn(__dmul_rn(d, r.hii), d));
+  }
+  s_out = s;
+  delta_out = delta;
+  return delta < thr;
+}
+
+// G is updated lazily: an accepted move's residual changes d (one row i_m)
+// join a pending list; a row is materialised when loaded, and the whole
+// column block is rewritten once per kPend moves.  Every element still gets
+// its additions g += h(k, i_m) d_m(j) one at a time in move order (multiply,
+// then add), so the values are those of the per-move update (jointq.cpp:142)
+// with 1 / kPend of its memory traffic.
+constexpr int kPend = 48;
+__global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
+  __shared__ RowSm r;
+  __shared__ int pend_i[kPend];
+  __shared__ int npend;
+  extern __shared__ double pend_d[];  // [kPend][ncol]
+  const int unit = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const long long j0 = (long long)unit * a.c.group, j1 = min(a.m, j0 + a.c.group);
+  const int ncol = int(j1 - j0);
+  const int nd = 2 * a.radius;  // code deltas per cell: -1, +1, -2, +2, ...
+  double obj = a.obj0;
+  int accepted = 0, fz = a.max_passes;
+  if (tid == 0) npend = 0;
+  __syncthreads();
+  auto load = [&](long long i) {
+    const int np = npend;
+    for (int j = tid; j < ncol; j += nt) {
+      const long long o = i * a.m + j0 + j;
+      double gv = a.g[o];
+      for (int p = 0; p < np; ++p) {
+        const double dv = pend_d[p * ncol + j];
+        if (dv != 0.0) gv = __dadd_rn(gv, __dmul_rn(a.h[i * a.n + pend_i[p]], dv));
+      }
+      r.g[j] = gv;
+      r.e[j] = a.e[o];
+      r.w[j] = a.w[o];
+      r.c[j] = a.codes[o];
+    }
+    if (tid == 0) r.hii = a.h[i * a.n + i];
+    __syncthreads();
+  };
+  auto flush = [&] {  // G[:, block] += the pending moves, in order
+    const int np = npend;
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (long long k = warp; k < a.n; k += nw) {
+      double* gk = a.g + k * a.m + j0;
+      const double* hk = a.h + k * a.n;
+      for (int jb = 0; jb < ncol; jb += 128) {
+        double gv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int j = jb + lane + 32 * t;
+          gv[t] = j < ncol ? gk[j] : 0.0;
+        }
+        for (int p = 0; p < np; ++p) {
+          const double hv = hk[pend_i[p]];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int j = jb + lane + 32 * t;
+            if (j < ncol) {
+              const double dv = pend_d[p * ncol + j];
+              if (dv != 0.0) gv[t] = __dadd_rn(gv[t], __dmul_rn(hv, dv));
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int j = jb + lane + 32 * t;
+          if (j < ncol) gk[j] = gv[t];
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) npend = 0;
+    __syncthreads();
+  };
+  // apply the move in r (jointq.cpp:144-158): E now, G through the pending list
+  auto apply = [&](long long i, long long group, unsigned long long key) {
+    const int slot = npend;
+    __syncthreads();  // (every thread has its slot before thread 0 advances npend)
+    for (int j = tid; j < ncol; j += nt) {
+      const double fresh = __dsub_rn(__dmul_rn(double(r.s), double((j == r.jp ? r.cp : r.c[j]) - r.z)),
+                                     double(r.w[j]));
+      const double d = __dsub_rn(fresh, r.e[j]);
+      pend_d[slot * ncol + j] = d;
+      if (d != 0.0) a.e[i * a.m + j0 + j] = fresh;
+    }
+    if (tid == 0) {
+      pend_i[slot] = int(i);
+      npend = slot + 1;
+      if (r.jp >= 0) a.codes[i * a.m + j0 + r.jp] = int16_t(r.cp);
+      a.scales[group] = r.s;
+      a.zeros[group] = r.z;
+      if (accepted < a.log_cap) {
+        a.log_key[(long long)unit * a.log_cap + accepted] = key;
+        a.log_delta[(long long)unit * a.log_cap + accepted] = r.delta;
+      }
+    }
+    obj = __dadd_rn(obj, r.delta);
+    ++accepted;
+    __syncthreads();
+    if (npend == kPend) flush();
+    load(i);
+  };
+  auto thr_of = [&] { return __dmul_rn(-a.tol, __dadd_rn(1.0, fabs(obj))); };  // jointq.cpp:183
+  for (int pass = 0; pass < a.max_passes; ++pass) {
+    const unsigned long long pk = (unsigned long long)pass << 58;
+    int in_pass = 0;
+    // (A) scale refit of each row's group (jointq.cpp:205-210)
+    for (long long i = 0; i < a.n; ++i) {
+      const long long group = i * a.c.gpr + unit;
+      load(i);
+      if (tid == 0) {
+        float s;
+        double dl;
+        r.best = eval_row_prop(r, ncol, -1, 0, a.zeros[group], thr_of(), s, dl) ? 0 : -1;
+        r.s = s, r.delta = dl, r.jp = -1, r.cp = 0, r.z = a.zeros[group];
+      }
+      __syncthreads();
+      if (r.best == 0) {
+        apply(i, group, pk | (unsigned long long)group);
+        ++in_pass;
+      }
+      __syncthreads();
+    }
+    // (B) code moves in row-major order, speculatively in parallel (jointq.cpp:211-230)
+    for (long long i = 0; i < a.n; ++i) {
+      const long long group = i * a.c.gpr + unit;
+      load(i);
+      int start = 0;  // first cell still to try
+      while (start < ncol) {
+        if (tid == 0) r.best = 0x7fffffff;
+        __syncthreads();
+        const int z = a.zeros[group];
+        const double thr = thr_of();
+        for (int k = tid; k < (ncol - start) * nd; k += nt) {
+          const int jp = start + k / nd, di = k % nd;
+          const int cp = r.c[jp] + ((di & 1) ? 1 : -1) * (di / 2 + 1);
+          if (cp < a.c.qmin || cp > a.c.qmax) continue;
+          float s;
+          double dl;
+          if (eval_row_prop(r, ncol, jp, cp, z, thr, s, dl)) atomicMin(&r.best, k);
+        }
+        __syncthreads();
+        const int best = r.best;
+        if (best == 0x7fffffff) break;
+        __syncthreads();
+        if (tid == 0) {  // re-evaluate the winner for its (s, delta) (deterministic)
+          const int jp = start + best / nd, di = best % nd;
+          const int cp = r.c[jp] + ((di & 1) ? 1 : -1) * (di / 2 + 1);
+          float s;
+          double dl;
+          eval_row_prop(r, ncol, jp, cp, z, thr, s, dl);
+          r.s = s, r.delta = dl, r.jp = jp, r.cp = cp, r.z = z;
+        }
+        __syncthreads();
+        const int jp = r.jp;
+        apply(i, group, pk | (1ull << 56) | (unsigned long long)(i * a.m + j0 + jp));
+        ++in_pass;
+        start = jp + 1;
+      }
+      __syncthreads();
+    }
+    // (C) zero-point moves (asymmetric; jointq.cpp:232-246)
+    if (a.c.scheme == 1) {
+      for (long long i = 0; i < a.n; ++i) {
+        const long long group = i * a.c.gpr + unit;
+        load(i);
+        if (tid == 0) {
+          r.best = -1;
+          for (int dz = -1; dz <= 1 && r.best < 0; dz += 2) {
+            const int z_new = a.zeros[group] + dz;
+            if (z_new < a.c.qmin || z_new > a.c.qmax) continue;
+            float s;
+            double dl;
+            if (eval_row_prop(r, ncol, -1, 0, z_new, thr_of(), s, dl)) {
+              r.best = 0;
+              r.s = s, r.delta = dl, r.jp = -1, r.cp = 0, r.z = z_new;
+            }
+          }
+        }
+        __syncthreads();
+        if (r.best == 0) {
+          apply(i, group, pk | (2ull << 56) | (unsigned long long)group);
+          ++in_pass;
+        }
+        __syncthreads();
+      }
+    }
+    if (in_pass == 0) {
+      fz = pass;
+      break;
+    }
+  }
+  if (tid == 0) {
+    a.log_count[unit] = accepted;
+    a.first_zero[unit] = fz;
+  }
 }
 
 // e = double(s (code - z)) - double(w): the reference's to_eigen_d(dequantize(q)) - to_eigen_d(w)
@@ -377,7 +712,14 @@ int jointq_search(const float* w, long long n, long long m, const QCfg& c, int16
   a.log_key = log_key, a.log_delta = log_delta, a.log_count = log_count, a.first_zero = first_zero;
   a.log_cap = log_cap;
   const int units = int(jointq_units(c, m));
-  jq_search_kernel<<<units, 256, 0, st>>>(a);
+  if (c.gran == 2 && c.group <= kRowMax) {
+    const int ncol = int(std::min<long long>(c.group, m));
+    const size_t dyn = size_t(kPend) * ncol * sizeof(double);
+    cudaFuncSetAttribute(jq_search_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+    jq_search_rows_kernel<<<units, 256, dyn, st>>>(a);
+  } else {
+    jq_search_kernel<<<units, 256, 0, st>>>(a);
+  }
   count_launches(1);
   return int(cudaGetLastError());
 }
