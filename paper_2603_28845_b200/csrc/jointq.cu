@@ -136,83 +136,6 @@ __device__ double delta_for(const JqArgs& a, const Cells& cl, const Prop& p, flo
   return warp_sum(delta);
 }
 
-// Per-group grids, one row per group: warp 0 keeps the row's cells in
-// registers (lane: columns j0 + lane + 32 t) while it evaluates that row's
-// proposals -- the same per-cell arithmetic and lane partition as opt_scale /
-// delta_for, without a global-memory round trip per proposal.  Reloaded after
-// every accepted move (the move rewrites E and G).
-constexpr int kRowT = 8;  // cells per lane: group_size <= 256
-struct RowCache {
-  double g[kRowT], e[kRowT];
-  float w[kRowT];
-  int c[kRowT];
-  double hii;
-  long long i, j0, j1;
-};
-__device__ __forceinline__ void load_row(const JqArgs& a, RowCache& r, long long i, long long j0,
-                                         long long j1) {
-  const int lane = threadIdx.x & 31;
-  r.i = i, r.j0 = j0, r.j1 = j1;
-  r.hii = a.h[i * a.n + i];
-#pragma unroll
-  for (int t = 0; t < kRowT; ++t) {
-    const long long j = j0 + lane + 32 * t;
-    if (j < j1) {
-      r.g[t] = a.g[i * a.m + j];
-      r.e[t] = a.e[i * a.m + j];
-      r.w[t] = a.w[i * a.m + j];
-      r.c[t] = a.codes[i * a.m + j];
-    } else {
-      r.g[t] = r.e[t] = 0.0, r.w[t] = 0.f, r.c[t] = 0;
-    }
-  }
-}
-__device__ __forceinline__ double opt_scale_row(const RowCache& r, long long mj, int mc, int z) {
-  const int lane = threadIdx.x & 31;
-  double num = 0.0, den = 0.0;
-#pragma unroll
-  for (int t = 0; t < kRowT; ++t) {
-    const long long j = r.j0 + lane + 32 * t;
-    if (j >= r.j1) continue;
-    const double cc = double((j == mj ? mc : r.c[t]) - z);
-    if (cc == 0.0) continue;
-    const double what = __dadd_rn(r.e[t], double(r.w[t]));
-    const double hf = __dsub_rn(r.g[t], __dmul_rn(r.hii, what));
-    const double dn = __dadd_rn(0.0, __dmul_rn(__dmul_rn(cc, r.hii), cc));
-    num = __dadd_rn(num, __dmul_rn(cc, hf));
-    den = __dadd_rn(den, dn);
-  }
-  num = warp_sum(num);
-  den = warp_sum(den);
-  if (den <= 0.0) return 0.0;
-  return -num / den;
-}
-__device__ __forceinline__ double delta_row(const RowCache& r, long long mj, int mc, float s, int z) {
-  const int lane = threadIdx.x & 31;
-  double delta = 0.0;
-#pragma unroll
-  for (int t = 0; t < kRowT; ++t) {
-    const long long j = r.j0 + lane + 32 * t;
-    if (j >= r.j1) continue;
-    const int code = j == mj ? mc : r.c[t];
-    const double fresh = __dsub_rn(__dmul_rn(double(s), double(code - z)), double(r.w[t]));
-    const double d = __dsub_rn(fresh, r.e[t]);
-    if (d == 0.0) continue;
-    double tt = __dmul_rn(__dmul_rn(2.0, d), r.g[t]);
-    tt = __dadd_rn(tt, __dmul_rn(__dmul_rn(d, r.hii), d));
-    delta = __dadd_rn(delta, tt);
-  }
-  return warp_sum(delta);
-}
-// the current code of column j of the cached row (from lane (j - j0) % 32)
-__device__ __forceinline__ int row_code(const RowCache& r, long long j) {
-  const int q = int(j - r.j0), tj = q >> 5;
-  int v = 0;
-#pragma unroll
-  for (int t = 0; t < kRowT; ++t) v = t == tj ? r.c[t] : v;
-  return __shfl_sync(0xffffffffu, v, q & 31);
-}
-
 struct JqShared {
   int op;  // 1: apply the move below, 2: exit
   long long group;
@@ -288,17 +211,15 @@ __global__ void __launch_bounds__(256) jq_search_kernel(JqArgs a) {
   double obj = a.obj0;
   int accepted = 0;
   int fz = a.max_passes;
-  RowCache row;
-  const bool fast = a.c.gran == 2 && uj1 - uj0 <= 32 * kRowT;  // one row per group, cached
   auto try_move = [&](long long group, const Prop& p, int z, unsigned long long key) -> bool {
     const Cells cl = cells_of(a, group);
-    const double raw = fast ? opt_scale_row(row, p.mj, p.mc, z) : opt_scale(a, cl, p, z);
+    const double raw = opt_scale(a, cl, p, z);
     float s_new = fp16_round(float(raw));
     if (!(s_new > 0.0f)) {
       if (raw > 0.0) s_new = kFp16MinPositive;
       else return false;
     }
-    const double delta = fast ? delta_row(row, p.mj, p.mc, s_new, z) : delta_for(a, cl, p, s_new, z);
+    const double delta = delta_for(a, cl, p, s_new, z);
     if (delta >= -a.tol * (1.0 + fabs(obj))) return false;
     if (lane == 0) {
       sh.op = 1, sh.group = group, sh.p = p, sh.s = s_new, sh.z = z;
@@ -315,7 +236,6 @@ __global__ void __launch_bounds__(256) jq_search_kernel(JqArgs a) {
       }
     }
     ++accepted;
-    if (fast) load_row(a, row, row.i, uj0, uj1);
     return true;
   };
   const Prop none{-1, -1, 0};
@@ -325,15 +245,13 @@ __global__ void __launch_bounds__(256) jq_search_kernel(JqArgs a) {
     // (A) scale refits with the current codes (jointq.cpp:205-210)
     for (long long t = 0; t < g_count; ++t) {
       const long long group = g_first + t * g_step;
-      if (fast) load_row(a, row, t, uj0, uj1);
       if (try_move(group, none, a.zeros[group], pk | group)) ++in_pass;
     }
     // (B) code moves, row-major; deltas -1, +1, -2, +2, ... (jointq.cpp:211-230)
     for (long long i = 0; i < a.n; ++i) {
-      if (fast) load_row(a, row, i, uj0, uj1);
       for (long long j = uj0; j < uj1; ++j) {
         const long long group = group_of(a.c, i, j);
-        const int cur = fast ? row_code(row, j) : int(a.codes[i * a.m + j]);
+        const int cur = int(a.codes[i * a.m + j]);
         for (int r = 1; r <= a.radius; ++r) {
           bool done = false;
           for (int sg = -1; sg <= 1; sg += 2) {
@@ -354,7 +272,6 @@ __global__ void __launch_bounds__(256) jq_search_kernel(JqArgs a) {
     if (a.c.scheme == 1) {
       for (long long t = 0; t < g_count; ++t) {
         const long long group = g_first + t * g_step;
-        if (fast) load_row(a, row, t, uj0, uj1);
         for (int dz = -1; dz <= 1; dz += 2) {
           const int z_new = a.zeros[group] + dz;
           if (z_new < a.c.qmin || z_new > a.c.qmax) continue;
@@ -404,14 +321,18 @@ struct RowSm {
 // one proposal: code cp at column jp (jp < 0: none), zero point z
 __device__ bool eval_row_prop(const RowSm& r, int ncol, int jp, int cp, int z, double thr, float& s_out,
                               double& delta_out) {
+  // (branch-free: a skipped cell keeps the running sums by selection, so the
+  // loads and products of the next cells issue ahead of the add chains)
   double num = 0.0, den = 0.0;  // jointq.cpp:95-118
+#pragma unroll 8
   for (int j = 0; j < ncol; ++j) {
     const double cc = double((j == jp ? cp : r.c[j]) - z);
-    if (cc == 0.0) continue;
     const double what = __dadd_rn(r.e[j], double(r.w[j]));
     const double hf = __dsub_rn(r.g[j], __dmul_rn(r.hii, what));
-    num = __dadd_rn(num, __dmul_rn(cc, hf));
-    den = __dadd_rn(den, __dmul_rn(__dmul_rn(cc, r.hii), cc));
+    const double nn = __dadd_rn(num, __dmul_rn(cc, hf));
+    const double dn = __dadd_rn(den, __dmul_rn(__dmul_rn(cc, r.hii), cc));
+    num = cc != 0.0 ? nn : num;
+    den = cc != 0.0 ? dn : den;
   }
   const double raw = den <= 0.0 ? 0.0 : -num / den;
   float s = fp16_round(float(raw));  // jointq.cpp:178-183
@@ -420,13 +341,14 @@ __device__ bool eval_row_prop(const RowSm& r, int ncol, int jp, int cp, int z, d
     else return false;
   }
   double delta = 0.0;  // jointq.cpp:122-141
+#pragma unroll 8
   for (int j = 0; j < ncol; ++j) {
     const double fresh =
         __dsub_rn(__dmul_rn(double(s), double((j == jp ? cp : r.c[j]) - z)), double(r.w[j]));
     const double d = __dsub_rn(fresh, r.e[j]);
-    if (d == 0.0) continue;
-    delta = __dadd_rn(delta, __dmul_rn(__dmul_rn(2.0, d), r.g[j]));
-    delta = __dadd_rn(delta, __dmul_rn(__dmul_rn(d, r.hii), d));
+    const double t1 = __dadd_rn(delta, __dmul_rn(__dmul_rn(2.0, d), r.g[j]));
+    const double t2 = __dadd_rn(t1, __dmul_rn(__dmul_rn(d, r.hii), d));
+    delta = d != 0.0 ? t2 : delta;
   }
   s_out = s;
   delta_out = delta;
@@ -443,6 +365,7 @@ constexpr int kPend = 48;
 __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
   __shared__ RowSm r;
   __shared__ int pend_i[kPend];
+  __shared__ double pend_h[kPend];  // h(i, i_p) of the row being loaded
   __shared__ int npend;
   extern __shared__ double pend_d[];  // [kPend][ncol]
   const int unit = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
@@ -455,12 +378,14 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
   __syncthreads();
   auto load = [&](long long i) {
     const int np = npend;
+    if (tid < np) pend_h[tid] = a.h[i * a.n + pend_i[tid]];
+    __syncthreads();
     for (int j = tid; j < ncol; j += nt) {
       const long long o = i * a.m + j0 + j;
       double gv = a.g[o];
       for (int p = 0; p < np; ++p) {
         const double dv = pend_d[p * ncol + j];
-        if (dv != 0.0) gv = __dadd_rn(gv, __dmul_rn(a.h[i * a.n + pend_i[p]], dv));
+        if (dv != 0.0) gv = __dadd_rn(gv, __dmul_rn(pend_h[p], dv));
       }
       r.g[j] = gv;
       r.e[j] = a.e[o];
@@ -476,6 +401,9 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
     for (long long k = warp; k < a.n; k += nw) {
       double* gk = a.g + k * a.m + j0;
       const double* hk = a.h + k * a.n;
+      // h(k, i_p) for the pending moves: two per lane, broadcast by shuffle below
+      const double hl0 = lane < np ? hk[pend_i[lane]] : 0.0;
+      const double hl1 = lane + 32 < np ? hk[pend_i[lane + 32]] : 0.0;
       for (int jb = 0; jb < ncol; jb += 128) {
         double gv[4];
 #pragma unroll
@@ -484,7 +412,7 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
           gv[t] = j < ncol ? gk[j] : 0.0;
         }
         for (int p = 0; p < np; ++p) {
-          const double hv = hk[pend_i[p]];
+          const double hv = __shfl_sync(0xffffffffu, p < 32 ? hl0 : hl1, p & 31);
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const int j = jb + lane + 32 * t;
