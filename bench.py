@@ -55,7 +55,7 @@ def peaks():
 
 # DRAM bytes (read + write) of one hessian_tc2_kernel launch at C2, from the
 # ncu --set full capture of gram_tc_kernel in profiles/r02_gram_ncu_full.txt
-HESSIAN_TRAFFIC_BYTES = 5.369535e9 + 0.623804e9
+HESSIAN_TRAFFIC_BYTES = 4665406000 + 622313728  # ncu dram read + write, one C2 launch (profiles/r02_gram_ncu_full.txt)
 
 
 def outlier_channels(n: int, frac: float, seed: int) -> np.ndarray:
