@@ -59,6 +59,13 @@ extern "C" {
 #define OCWG_FP32 0
 #define OCWG_FP64 1
 
+/* layout of the fp64 statistics (gram / cross) host matrices taken and returned
+ * by ocwg_accumulate_stats, ocwg_quantize_layer and ocwg_qep_target: row-major
+ * (default) or column-major (an Eigen::MatrixXd's storage, CalibStats
+ * stats.hpp:15-24 -- the C++ drop-in passes them without host-side copies) */
+#define OCWG_ROW_MAJOR 0
+#define OCWG_COL_MAJOR 1
+
 /* QuantConfig (quant.hpp:21-28) */
 typedef struct ocwg_quant_config {
   int32_t bits;        /* [1, 8] */
@@ -87,6 +94,7 @@ int ocwg_destroy(ocwg_ctx* ctx);
 /* OCWG_FP32 (default, fast: tensor-core statistics, fp32 factorisation +
  * 3xTF32 sweep) or OCWG_FP64 (the reference's arithmetic class throughout). */
 int ocwg_set_precision(ocwg_ctx* ctx, int precision);
+int ocwg_set_stats_layout(ocwg_ctx* ctx, int layout);
 /* Run subsequent work on an external cudaStream_t (NULL = the CUDA legacy
  * default stream).  A new context uses its own non-blocking stream. */
 int ocwg_set_stream(ocwg_ctx* ctx, void* cuda_stream);

@@ -187,6 +187,7 @@ _SIGS = {
     "ocwg_destroy": (C.c_int, [_P]),
     "ocwg_set_stream": (C.c_int, [_P, _P]),
     "ocwg_set_precision": (C.c_int, [_P, C.c_int]),
+    "ocwg_set_stats_layout": (C.c_int, [_P, C.c_int]),
     "ocwg_synchronize": (C.c_int, [_P]),
     "ocwg_set_async": (C.c_int, [_P, C.c_int]),
     "ocwg_debug_factor_bench": (C.c_int, [_P, C.c_int, _P, _P]),

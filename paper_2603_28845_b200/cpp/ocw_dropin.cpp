@@ -43,6 +43,9 @@ ocwg_ctx* ctx() {
         throw std::runtime_error(std::string("ocwg_create: ") + ocwg_last_error());
       const char* p = std::getenv("OCW_GPU_PRECISION");
       if (p && std::strcmp(p, "fp64") == 0) ocwg_set_precision(c, OCWG_FP64);
+      // CalibStats keeps gram / cross as Eigen (column-major) matrices: hand the
+      // storage over as is, the device transposes (no host-side copies)
+      ocwg_set_stats_layout(c, OCWG_COL_MAJOR);
     }
     ~Holder() { ocwg_destroy(c); }
   } h;
@@ -227,54 +230,18 @@ Matrix CalibStats::cross_matrix() const {
   return m;
 }
 
-namespace {
-// Eigen::MatrixXd (column-major) <-> row-major buffers of the C ABI: a blocked
-// transpose over row bands on a few host threads (the N x N statistics are
-// 128 MiB each at N = 4096)
-template <typename F>
-void bands(Eigen::Index rows, F&& f) {
-  const unsigned nt = rows >= 512 ? 8u : 1u;
-  std::vector<std::thread> th;
-  for (unsigned t = 0; t < nt; ++t)
-    th.emplace_back([&, t] { f(rows * t / nt, rows * (t + 1) / nt); });
-  for (auto& x : th) x.join();
-}
-std::vector<double> row_major(const Eigen::MatrixXd& a) {
-  std::vector<double> v(size_t(a.rows()) * size_t(a.cols()));
-  const double* src = a.data();
-  const size_t R = size_t(a.rows()), Cc = size_t(a.cols());
-  bands(a.rows(), [&](Eigen::Index i0, Eigen::Index i1) {
-    for (size_t jb = 0; jb < Cc; jb += 64)
-      for (size_t i = size_t(i0); i < size_t(i1); ++i)
-        for (size_t j = jb; j < std::min(Cc, jb + 64); ++j) v[i * Cc + j] = src[j * R + i];
-  });
-  return v;
-}
-void from_row_major(const std::vector<double>& v, Eigen::MatrixXd& a) {
-  double* dst = a.data();
-  const size_t R = size_t(a.rows()), Cc = size_t(a.cols());
-  bands(a.rows(), [&](Eigen::Index i0, Eigen::Index i1) {
-    for (size_t jb = 0; jb < Cc; jb += 64)
-      for (size_t i = size_t(i0); i < size_t(i1); ++i)
-        for (size_t j = jb; j < std::min(Cc, jb + 64); ++j) dst[j * R + i] = v[i * Cc + j];
-  });
-}
-}  // namespace
 
 void accumulate_stats(CalibStats& stats, const Matrix& x_fp, const Matrix& x_pert) {
   require_same_shape(x_fp, x_pert, "accumulate_stats");
   if (x_fp.cols != stats.dim())
     throw invalid_input("accumulate_stats: stats dimension " + std::to_string(stats.dim()) +
                         " does not match inputs with " + std::to_string(x_fp.cols) + " columns");
-  std::vector<double> g = row_major(stats.gram), c = row_major(stats.cross);
   uint64_t tokens = stats.token_count;
   // identical inputs: cross += Xp^T (X - Xp) is identically zero (stats.cpp:17)
   const bool same = x_fp.data == x_pert.data;
   const float* xf = same ? x_pert.data.data() : x_fp.data.data();
-  check(ocwg_accumulate_stats(ctx(), xf, x_pert.data.data(), x_fp.rows, x_fp.cols, g.data(),
-                              same ? nullptr : c.data(), &tokens));
-  from_row_major(g, stats.gram);
-  if (!same) from_row_major(c, stats.cross);
+  check(ocwg_accumulate_stats(ctx(), xf, x_pert.data.data(), x_fp.rows, x_fp.cols,
+                              stats.gram.data(), same ? nullptr : stats.cross.data(), &tokens));
   stats.token_count = size_t(tokens);
 }
 
@@ -306,10 +273,9 @@ QuantizedMatrix gptq_quantize(const Matrix& w, const Matrix& h, const QuantConfi
 Matrix qep_target(const Matrix& w, const CalibStats& stats, const QepOptions& opts) {
   if (stats.dim() != w.rows)
     throw invalid_input("qep_target: stats dimension does not match W rows");
-  std::vector<double> g = row_major(stats.gram), c = row_major(stats.cross);
   Matrix out(w.rows, w.cols);
-  check(ocwg_qep_target(ctx(), w.data.data(), g.data(), c.data(), w.rows, w.cols, opts.alpha,
-                        opts.eta, out.data.data()));
+  check(ocwg_qep_target(ctx(), w.data.data(), stats.gram.data(), stats.cross.data(), w.rows, w.cols,
+                        opts.alpha, opts.eta, out.data.data()));
   return out;
 }
 
@@ -335,13 +301,12 @@ QuantizedMatrix quantize_layer(const Matrix& w, const CalibStats& stats,
                             uint64_t(opts.gptq.block_cols)};
   ocwg_qep_options qo{};
   if (opts.qep) qo = ocwg_qep_options{opts.qep->alpha, opts.qep->eta};
-  const std::vector<double> g = row_major(stats.gram);
-  const std::vector<double> cr = opts.qep ? row_major(stats.cross) : std::vector<double>{};
   const size_t ng = quant_group_count(cfg, w.rows, w.cols);
   std::vector<float> s(ng);
   std::vector<int32_t> z(ng);
   QuantizedMatrix q{w.rows, w.cols, cfg, std::vector<int16_t>(w.rows * w.cols), {}};
-  check(ocwg_quantize_layer(ctx(), w.data.data(), g.data(), opts.qep ? cr.data() : nullptr, w.rows,
+  check(ocwg_quantize_layer(ctx(), w.data.data(), stats.gram.data(),
+                            opts.qep ? stats.cross.data() : nullptr, w.rows,
                             w.cols, opts.method == BaseQuantMethod::gptq ? 1 : 0, &c, &o,
                             mode_of(opts.scale_mode), opts.qep ? &qo : nullptr, q.codes.data(),
                             s.data(), z.data(), nullptr));

@@ -49,6 +49,7 @@ struct ocwg_ctx {
   unsigned* flag = nullptr;  // device status word
   unsigned* flag_host = nullptr;
   int precision = OCWG_FP32;  // factorisation + sweep arithmetic
+  bool stats_colmajor = false;  // fp64 gram / cross host matrices column-major (ocwg_set_stats_layout)
   bool profile = false;       // record phase events in run_gptq
   bool tensor_core_gemm = true;  // fp32 GEMMs on tcgen05 (3xTF32) vs SIMT
   bool async_dev = false;        // *_dev calls return without draining the stream
@@ -558,6 +559,16 @@ int ocwg_destroy(ocwg_ctx* ctx) {
     cudaStreamDestroy(ctx->aux);
     cudaStreamDestroy(ctx->own);
     delete ctx;
+  });
+}
+
+int ocwg_set_stats_layout(ocwg_ctx* ctx, int layout) {
+  return guard([&] {
+    if (!ctx) fail(OCWG_INVALID_INPUT, "null context");
+    if (layout != OCWG_ROW_MAJOR && layout != OCWG_COL_MAJOR)
+      fail(OCWG_INVALID_INPUT, "layout must be OCWG_ROW_MAJOR or OCWG_COL_MAJOR");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->stats_colmajor = layout == OCWG_COL_MAJOR;
   });
 }
 
@@ -1105,9 +1116,17 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
       if (!same) h2d(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
       h2d(ar.at<double>(og), gram, dim * dim * 8, ctx);
       if (want_cross) h2d(ar.at<double>(oc), cross, dim * dim * 8, ctx);
+      if (ctx->stats_colmajor) {
+        transpose_sq_f64(ar.at<double>(og), (long long)dim, st);
+        if (want_cross) transpose_sq_f64(ar.at<double>(oc), (long long)dim, st);
+      }
       const float* xf = same ? ar.at<float>(op) : ar.at<float>(of);
       accumulate_stats_f64(xf, ar.at<float>(op), (long long)rows, (long long)dim, ar.at<double>(og),
                            want_cross ? ar.at<double>(oc) : nullptr, ar.at<double>(od), st);
+      if (ctx->stats_colmajor) {
+        transpose_sq_f64(ar.at<double>(og), (long long)dim, st);
+        if (want_cross) transpose_sq_f64(ar.at<double>(oc), (long long)dim, st);
+      }
       d2h(gram, ar.at<double>(og), dim * dim * 8, ctx);
       if (want_cross) d2h(cross, ar.at<double>(oc), dim * dim * 8, ctx);
       finish(ctx);
@@ -1132,6 +1151,10 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
       if (want_cross) h2d_big(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
       h2d_big(ar.at<double>(og), gram, dim * dim * 8, ctx);
       if (want_cross) h2d_big(ar.at<double>(oc), cross, dim * dim * 8, ctx);
+      if (ctx->stats_colmajor) {
+        transpose_sq_f64(ar.at<double>(og), (long long)dim, st);
+        if (want_cross) transpose_sq_f64(ar.at<double>(oc), (long long)dim, st);
+      }
       const auto t1 = tnow();
       if (dbg)
         fprintf(stderr, "accumulate_stats: H2D %.1f ms\n",
@@ -1179,6 +1202,10 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
         fprintf(stderr, "accumulate_stats: split %.1f ms, gram kernel %.1f ms\n",
                 std::chrono::duration<double, std::milli>(t2 - t1).count(),
                 std::chrono::duration<double, std::milli>(t3 - t2).count());
+      if (ctx->stats_colmajor) {
+        transpose_sq_f64(ar.at<double>(og), (long long)dim, st);
+        if (want_cross) transpose_sq_f64(ar.at<double>(oc), (long long)dim, st);
+      }
       d2h_big(gram, ar.at<double>(og), dim * dim * 8, ctx);
       if (want_cross) d2h_big(cross, ar.at<double>(oc), dim * dim * 8, ctx);
     }
@@ -1452,10 +1479,14 @@ int ocwg_quantize_layer(ocwg_ctx* ctx, const float* w, const double* gram, const
     ar.commit();
     float* wd = ar.at<float>(ow);
     h2d_big(wd, w, n * m * 4, ctx);
-    if (corr || method == 1) h2d_big(ar.at<double>(og), gram, n * n * 8, ctx);
+    if (corr || method == 1) {
+      h2d_big(ar.at<double>(og), gram, n * n * 8, ctx);
+      if (ctx->stats_colmajor) transpose_sq_f64(ar.at<double>(og), (long long)n, st);
+    }
     const float* target = wd;
     if (corr) {  // W* = W + alpha (gram + lambda I)^-1 (cross W)   (layerwise.cpp:103-111)
       h2d_big(ar.at<double>(oc), cross, n * n * 8, ctx);
+      if (ctx->stats_colmajor) transpose_sq_f64(ar.at<double>(oc), (long long)n, st);
       set_tc_workspace(nullptr, 0);
       qep_target_f64(wd, ar.at<double>(og), ar.at<double>(oc), (long long)n, (long long)m,
                      qep->alpha, qep->eta, ar.at<float>(ot), ar.at<double>(oqw), ar.at<int>(oqf),
@@ -1514,6 +1545,10 @@ int ocwg_qep_target(ocwg_ctx* ctx, const float* w, const double* gram, const dou
     h2d(ar.at<float>(ow), w, n * m * 4, ctx);
     h2d(ar.at<double>(og), gram, n * n * 8, ctx);
     h2d(ar.at<double>(oc), cross, n * n * 8, ctx);
+    if (ctx->stats_colmajor) {
+      transpose_sq_f64(ar.at<double>(og), (long long)n, ctx->stream);
+      transpose_sq_f64(ar.at<double>(oc), (long long)n, ctx->stream);
+    }
     set_tc_workspace(nullptr, 0);
     qep_target_f64(ar.at<float>(ow), ar.at<double>(og), ar.at<double>(oc), (long long)n,
                    (long long)m, alpha, eta, ar.at<float>(oo), ar.at<double>(ows), ar.at<int>(of),

@@ -252,4 +252,7 @@ double jointq_objective_dev(const float* x, long long tokens, long long n, long 
                             const double* e, double lambda, double* y, long long chunk, double* part,
                             cudaStream_t st);
 
+// in-place transpose of an n x n fp64 matrix (column-major caller statistics)
+void transpose_sq_f64(double* a, long long n, cudaStream_t st);
+
 }  // namespace ocwg

@@ -204,4 +204,33 @@ void activation_objective(const float* w, const float* w_hat, const float* h, lo
   dot_kernel<<<1, 1024, 0, st>>>(d, hd, n * m, out_dev);
 }
 
+
+// In-place transpose of an n x n fp64 matrix (column-major statistics from a
+// caller, ocwg_set_stats_layout): one 32 x 32 tile pair per block, upper pairs.
+__global__ void transpose_sq_f64_kernel(double* a, long long n) {
+  __shared__ double t1[32][33], t2[32][33];
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bj < bi) return;
+  const int tx = threadIdx.x;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const long long i1 = (long long)bi * 32 + r, j1 = (long long)bj * 32 + tx;
+    const long long i2 = (long long)bj * 32 + r, j2 = (long long)bi * 32 + tx;
+    t1[r][tx] = (i1 < n && j1 < n) ? a[i1 * n + j1] : 0.0;
+    t2[r][tx] = (i2 < n && j2 < n) ? a[i2 * n + j2] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const long long i1 = (long long)bi * 32 + r, j1 = (long long)bj * 32 + tx;
+    const long long i2 = (long long)bj * 32 + r, j2 = (long long)bi * 32 + tx;
+    if (i1 < n && j1 < n) a[i1 * n + j1] = t2[tx][r];
+    if (i2 < n && j2 < n) a[i2 * n + j2] = t1[tx][r];
+  }
+}
+void transpose_sq_f64(double* a, long long n, cudaStream_t st) {
+  if (n <= 1) return;
+  const unsigned nb = unsigned((n + 31) / 32);
+  transpose_sq_f64_kernel<<<dim3(nb, nb), dim3(32, 8), 0, st>>>(a, n);
+  count_launches(1);
+}
+
 }  // namespace ocwg

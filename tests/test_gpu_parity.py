@@ -442,3 +442,38 @@ def test_split_bf16_parts(g, orc):
     d = xf.astype(np.float64) - xp.astype(np.float64)
     np.testing.assert_array_equal(d1[:, :n], orc.bf16_bits(d.astype(np.float32)))
     assert int(fl.item()) == 3
+
+
+@pytest.mark.gpu
+def test_column_major_statistics_layout(ref):
+    """ocwg_set_stats_layout(OCWG_COL_MAJOR) (the drop-in's CalibStats storage):
+    gram / cross in and out column-major give the transposes of the row-major
+    results (quantize_layer / qep_target through the column-major drop-in are
+    covered by the reference's own tests in test_gpu_dropin.py)."""
+    import ctypes as C
+
+    import paper_2603_28845_b200 as g
+    lib = g.lib()
+    n, t = 72, 300
+    xp = ref.random_gaussian(t, n, 4401)
+    xf = xp + 0.05 * ref.random_gaussian(t, n, 4402)
+    g0 = ref.random_gaussian(n, n, 4403).astype(np.float64)
+    g0 = g0 + g0.T  # the accumulated gram is symmetric; cross need not be
+    c0 = ref.random_gaussian(n, n, 4404).astype(np.float64)
+    out = {}
+    for layout in (0, 1):
+        h = C.c_void_p()
+        assert lib.ocwg_create(0, C.byref(h)) == 0
+        try:
+            assert lib.ocwg_set_stats_layout(h, layout) == 0
+            gm = np.ascontiguousarray(g0 if layout == 0 else g0.T).copy()
+            cm = np.ascontiguousarray(c0 if layout == 0 else c0.T).copy()
+            tc = C.c_uint64(0)
+            assert lib.ocwg_accumulate_stats(h, xf.ctypes.data, xp.ctypes.data, t, n, gm.ctypes.data,
+                                             cm.ctypes.data, C.byref(tc)) == 0
+            out[layout] = (gm, cm)
+        finally:
+            lib.ocwg_destroy(h)
+    np.testing.assert_array_equal(out[1][0], out[0][0].T)
+    np.testing.assert_array_equal(out[1][1], out[0][1].T)
+    assert lib.ocwg_set_stats_layout(g.context().handle, 7) == 1  # invalid layout
