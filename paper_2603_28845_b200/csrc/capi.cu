@@ -261,6 +261,37 @@ void h2d_big(void* d, const void* h, size_t bytes, ocwg_ctx* ctx) {
   ck(cudaStreamWaitEvent(ctx->stream, ctx->stage_ev[0], 0), "event");
   ck(cudaStreamWaitEvent(ctx->stream, ctx->stage_ev[1], 0), "event");
 }
+// Staged H2D of a (pageable) host buffer on ctx->cpy, ordered after `dep` (an
+// event on another stream marking the destination free; null: none) and NOT
+// joined to ctx->stream -- the caller waits on an event recorded on ctx->cpy.
+// Returns once the last staging memcpy is issued (its DMA may be in flight).
+void h2d_staged_async(void* d, const void* h, size_t bytes, ocwg_ctx* ctx, cudaEvent_t dep,
+                      cudaEvent_t done) {
+  ensure_stage(ctx);
+  if (dep) ck(cudaStreamWaitEvent(ctx->cpy, dep, 0), "event");
+  if (bytes < kStageBytes || is_pinned(h)) {
+    if (is_pinned(h)) {
+      ck(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->cpy), "H2D");
+    } else {  // small pageable: through staging buffer 0
+      ck(cudaEventSynchronize(ctx->stage_ev[0]), "event sync");
+      std::memcpy(ctx->stage[0], h, bytes);
+      ck(cudaMemcpyAsync(d, ctx->stage[0], bytes, cudaMemcpyHostToDevice, ctx->cpy), "H2D(staged)");
+      ck(cudaEventRecord(ctx->stage_ev[0], ctx->cpy), "event");
+    }
+  } else {
+    for (size_t off = 0, k = 0; off < bytes; off += kStageBytes, ++k) {
+      const int b = int(k & 1);
+      const size_t len = std::min(kStageBytes, bytes - off);
+      ck(cudaEventSynchronize(ctx->stage_ev[b]), "event sync");  // its previous DMA is done
+      par_memcpy(ctx->stage[b], static_cast<const char*>(h) + off, len);
+      ck(cudaMemcpyAsync(static_cast<char*>(d) + off, ctx->stage[b], len, cudaMemcpyHostToDevice,
+                         ctx->cpy),
+         "H2D(staged)");
+      ck(cudaEventRecord(ctx->stage_ev[b], ctx->cpy), "event");
+    }
+  }
+  if (done) ck(cudaEventRecord(done, ctx->cpy), "event");
+}
 // D2H of a large device buffer after the work on ctx->stream; synchronous
 void d2h_big(void* h, const void* d, size_t bytes, ocwg_ctx* ctx) {
   if (!h || !bytes) return;
@@ -1131,81 +1162,113 @@ int ocwg_accumulate_stats(ocwg_ctx* ctx, const float* x_fp, const float* x_pert,
       if (want_cross) d2h(cross, ar.at<double>(oc), dim * dim * 8, ctx);
       finish(ctx);
     } else {
-      // tensor cores: X_hat = P1 + P2, X - X_hat = D1 + D2 (bf16 parts), fp64 outputs
+      // tensor cores: X_hat = P1 + P2, X - X_hat = D1 + D2 (bf16 parts), fp64 outputs.
+      // Token chunks are pipelined: the staged copy of chunk k+1 (host memcpy into
+      // pinned staging + DMA on ctx->cpy) runs while chunk k is split and
+      // accumulated on ctx->stream; the fp32 chunk buffers are double-buffered.
       const uint64_t ld = (dim + 7) / 8 * 8;
+      const uint64_t chunk = std::min<uint64_t>(rows, 32768);  // a multiple of the 8192-token window
+      const uint64_t nch = (rows + chunk - 1) / chunk;
       Arena ar(ctx);
-      const size_t op = ar.reserve(rows * dim * 4), of = ar.reserve(want_cross ? rows * dim * 4 : 4),
-                   o1 = ar.reserve(rows * ld * 2), o2 = ar.reserve(rows * ld * 2),
-                   o3 = ar.reserve(want_cross ? rows * ld * 2 : 16),
-                   o4 = ar.reserve(want_cross ? rows * ld * 2 : 16), og = ar.reserve(dim * dim * 8),
+      size_t op[2], of[2];
+      for (int b = 0; b < 2; ++b) {
+        op[b] = ar.reserve(chunk * dim * 4);
+        of[b] = ar.reserve(want_cross ? chunk * dim * 4 : 4);
+      }
+      const size_t o1 = ar.reserve(chunk * ld * 2), o2 = ar.reserve(chunk * ld * 2),
+                   o3 = ar.reserve(want_cross ? chunk * ld * 2 : 16),
+                   o4 = ar.reserve(want_cross ? chunk * ld * 2 : 16), og = ar.reserve(dim * dim * 8),
                    oc = ar.reserve(want_cross ? dim * dim * 8 : 8), ofl = ar.reserve(16),
                    ows = ar.reserve(gram_tc_workspace_bytes((long long)dim));
       ar.commit();
       const bool dbg = getenv("OCWG_DEBUG_STATS") != nullptr;
-      auto tnow = [&] {
-        if (dbg) cudaStreamSynchronize(st);
-        return std::chrono::steady_clock::now();
-      };
-      const auto t0 = tnow();
-      h2d_big(ar.at<float>(op), x_pert, rows * dim * 4, ctx);
-      if (want_cross) h2d_big(ar.at<float>(of), x_fp, rows * dim * 4, ctx);
+      const auto t0 = std::chrono::steady_clock::now();
       h2d_big(ar.at<double>(og), gram, dim * dim * 8, ctx);
       if (want_cross) h2d_big(ar.at<double>(oc), cross, dim * dim * 8, ctx);
       if (ctx->stats_colmajor) {
         transpose_sq_f64(ar.at<double>(og), (long long)dim, st);
         if (want_cross) transpose_sq_f64(ar.at<double>(oc), (long long)dim, st);
       }
-      const auto t1 = tnow();
-      if (dbg)
-        fprintf(stderr, "accumulate_stats: H2D %.1f ms\n",
-                std::chrono::duration<double, std::milli>(t1 - t0).count());
-      unsigned* fl = ar.at<unsigned>(ofl);
-      ck(cudaMemsetAsync(fl, 0, 4, st), "memset");
+      cudaEvent_t ev_free[2], ev_copied[2];
+      for (int b = 0; b < 2; ++b) {
+        ck(cudaEventCreateWithFlags(&ev_free[b], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming), "cudaEventCreate");
+      }
+      struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+          for (int b = 0; b < 4; ++b) cudaEventDestroy(e[b]);
+        }
+      };
+      cudaEvent_t evs[4] = {ev_free[0], ev_free[1], ev_copied[0], ev_copied[1]};
+      EvGuard guard_ev{evs};
+      bool freed[2] = {false, false};
+      auto copy_chunk = [&](uint64_t k) {  // tokens of chunk k -> slot k & 1
+        const int b = int(k & 1);
+        const uint64_t t0k = k * chunk, len = std::min(chunk, rows - t0k);
+        h2d_staged_async(ar.at<float>(op[b]), x_pert + t0k * dim, len * dim * 4, ctx,
+                         freed[b] ? ev_free[b] : nullptr, nullptr);
+        if (want_cross)
+          h2d_staged_async(ar.at<float>(of[b]), x_fp + t0k * dim, len * dim * 4, ctx, nullptr,
+                           nullptr);
+        ck(cudaEventRecord(ev_copied[b], ctx->cpy), "event");
+      };
       uint16_t *p1 = ar.at<uint16_t>(o1), *p2 = ar.at<uint16_t>(o2), *d1 = ar.at<uint16_t>(o3),
                *d2 = ar.at<uint16_t>(o4);
-      launch_split_bf16(ar.at<float>(op), want_cross ? ar.at<float>(of) : nullptr, (long long)rows,
-                        (long long)dim, (long long)ld, p1, p2, d1, d2, fl, st);
-      unsigned f = 0;
-      d2h(&f, fl, 4, ctx);
-      ck(cudaStreamSynchronize(st), "sync");
-      if (getenv("OCWG_DEBUG_STATS")) fprintf(stderr, "accumulate_stats: split flags %u\n", f);
-      GramSpec s;
-      s.tokens = (long long)rows;
-      s.dim = (long long)dim;
-      s.ld = (long long)ld;
-      s.ops[0] = p1;
-      s.ops[1] = p2;
-      s.ops[2] = d1;
-      s.ops[3] = d2;
-      s.nops = 4;
-      // gram = P1'P1 (+ P1'P2 + P2'P1 when X_hat is not bf16-exact)
-      s.gseg = (f & 1u) ? 3 : 1;
-      const int ga[3] = {0, 0, 1}, gb[3] = {0, 1, 0};
-      // cross = P1'D1 + P1'D2 + P2'D1
-      s.cseg = (want_cross && (f & 2u)) ? 3 : 0;
-      const int ca[3] = {0, 0, 1}, cb[3] = {2, 3, 2};
-      for (int k = 0; k < 3; ++k) s.gA[k] = ga[k], s.gB[k] = gb[k], s.cA[k] = ca[k], s.cB[k] = cb[k];
-      s.gram = ar.at<double>(og);
-      s.cross = ar.at<double>(oc);
-      s.f64 = true;
-      s.accumulate = true;
-      // fp32 TMEM accumulations of 8192 tokens, fp64 across windows (half the
-      // hot path's window; measured at C2: 2048 -> 8192 tokens takes the kernel
-      // from 273 to 75 ms with the error still set by the bf16 split, ~7e-6)
-      s.window_tokens = 8192;
-      const auto t2 = tnow();
-      const int r = gram_tc(s, ar.at<void>(ows), gram_tc_workspace_bytes((long long)dim), st);
-      if (r != 0) fail(OCWG_CUDA_ERROR, "accumulate_stats: tensor-core kernel launch failed");
-      finish(ctx);
-      const auto t3 = tnow();
-      if (dbg)
-        fprintf(stderr, "accumulate_stats: split %.1f ms, gram kernel %.1f ms\n",
-                std::chrono::duration<double, std::milli>(t2 - t1).count(),
-                std::chrono::duration<double, std::milli>(t3 - t2).count());
+      unsigned* fl = ar.at<unsigned>(ofl);
+      copy_chunk(0);
+      for (uint64_t k = 0; k < nch; ++k) {
+        const int b = int(k & 1);
+        const uint64_t len = std::min(chunk, rows - k * chunk);
+        ck(cudaStreamWaitEvent(st, ev_copied[b], 0), "event");
+        ck(cudaMemsetAsync(fl, 0, 4, st), "memset");
+        launch_split_bf16(ar.at<float>(op[b]), want_cross ? ar.at<float>(of[b]) : nullptr,
+                          (long long)len, (long long)dim, (long long)ld, p1, p2, d1, d2, fl, st);
+        ck(cudaEventRecord(ev_free[b], st), "event");  // the split has read slot b
+        freed[b] = true;
+        if (k + 1 < nch) copy_chunk(k + 1);  // (host staging overlaps the split / gram on st)
+        unsigned f = 0;
+        d2h(&f, fl, 4, ctx);
+        ck(cudaStreamSynchronize(st), "sync");
+        if (dbg) fprintf(stderr, "accumulate_stats: chunk %llu split flags %u\n", (unsigned long long)k, f);
+        GramSpec s;
+        s.tokens = (long long)len;
+        s.dim = (long long)dim;
+        s.ld = (long long)ld;
+        s.ops[0] = p1;
+        s.ops[1] = p2;
+        s.ops[2] = d1;
+        s.ops[3] = d2;
+        s.nops = 4;
+        // gram = P1'P1 (+ P1'P2 + P2'P1 when X_hat is not bf16-exact)
+        s.gseg = (f & 1u) ? 3 : 1;
+        const int ga[3] = {0, 0, 1}, gb[3] = {0, 1, 0};
+        // cross = P1'D1 + P1'D2 + P2'D1
+        s.cseg = (want_cross && (f & 2u)) ? 3 : 0;
+        const int ca[3] = {0, 0, 1}, cb[3] = {2, 3, 2};
+        for (int q = 0; q < 3; ++q) s.gA[q] = ga[q], s.gB[q] = gb[q], s.cA[q] = ca[q], s.cB[q] = cb[q];
+        s.gram = ar.at<double>(og);
+        s.cross = ar.at<double>(oc);
+        s.f64 = true;
+        s.accumulate = true;
+        // fp32 TMEM accumulations of 8192 tokens, fp64 across windows (measured at
+        // C2: 2048 -> 8192-token windows take the kernel from 273 to 75 ms, the
+        // error still set by the bf16 split, ~7e-6)
+        s.window_tokens = 8192;
+        if (s.gseg > 0 || s.cseg > 0) {
+          const int r = gram_tc(s, ar.at<void>(ows), gram_tc_workspace_bytes((long long)dim), st);
+          if (r != 0) fail(OCWG_CUDA_ERROR, "accumulate_stats: tensor-core kernel launch failed");
+        }
+      }
       if (ctx->stats_colmajor) {
         transpose_sq_f64(ar.at<double>(og), (long long)dim, st);
         if (want_cross) transpose_sq_f64(ar.at<double>(oc), (long long)dim, st);
       }
+      finish(ctx);
+      if (dbg)
+        fprintf(stderr, "accumulate_stats: pipelined H2D + split + gram %.1f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                    .count());
       d2h_big(gram, ar.at<double>(og), dim * dim * 8, ctx);
       if (want_cross) d2h_big(cross, ar.at<double>(oc), dim * dim * 8, ctx);
     }
