@@ -28,6 +28,7 @@
 // in a different order than the reference's sequential loops (fp64 rounding).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -55,6 +56,7 @@ struct JqArgs {
   int* log_count;   // per unit accepted moves (the log keeps the first log_cap)
   int* first_zero;  // per unit: first pass without an accepted move (max_passes: none)
   long long log_cap;
+  unsigned long long* prof;  // debug: unit 0's cycles per phase (null: off)
 };
 
 struct Cells {  // rows [r0, r1) x columns [j0, j1) (jointq.cpp:18-40)
@@ -376,6 +378,8 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
   int accepted = 0, fz = a.max_passes;
   if (tid == 0) npend = 0;
   __syncthreads();
+  unsigned long long tph[6] = {0, 0, 0, 0, 0, 0};  // debug timers: A, B evals, B, C, rounds, flush
+  auto clk = [] { return (unsigned long long)clock64(); };
   auto load = [&](long long i) {
     const int np = npend;
     if (tid < np) pend_h[tid] = a.h[i * a.n + pend_i[tid]];
@@ -396,36 +400,52 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
     __syncthreads();
   };
   auto flush = [&] {  // G[:, block] += the pending moves, in order
+    // a warp takes kFR rows at a time: 4 kFR independent add chains per lane
+    // (each element still adds its moves one at a time, in order), and every
+    // pending d read from shared memory serves kFR rows
+    constexpr int kFR = 8;
     const int np = npend;
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (long long k = warp; k < a.n; k += nw) {
-      double* gk = a.g + k * a.m + j0;
-      const double* hk = a.h + k * a.n;
-      // h(k, i_p) for the pending moves: two per lane, broadcast by shuffle below
-      const double hl0 = lane < np ? hk[pend_i[lane]] : 0.0;
-      const double hl1 = lane + 32 < np ? hk[pend_i[lane + 32]] : 0.0;
+    for (long long k0 = (long long)warp * kFR; k0 < a.n; k0 += (long long)nw * kFR) {
       for (int jb = 0; jb < ncol; jb += 128) {
-        double gv[4];
+        double gv[kFR][4], hl0[kFR], hl1[kFR];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int j = jb + lane + 32 * t;
-          gv[t] = j < ncol ? gk[j] : 0.0;
-        }
-        for (int p = 0; p < np; ++p) {
-          const double hv = __shfl_sync(0xffffffffu, p < 32 ? hl0 : hl1, p & 31);
+        for (int q = 0; q < kFR; ++q) {
+          const long long k = k0 + q;
+          const bool kok = k < a.n;
+          const double* hk = a.h + (kok ? k : 0) * a.n;
+          hl0[q] = kok && lane < np ? hk[pend_i[lane]] : 0.0;
+          hl1[q] = kok && lane + 32 < np ? hk[pend_i[lane + 32]] : 0.0;
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const int j = jb + lane + 32 * t;
-            if (j < ncol) {
-              const double dv = pend_d[p * ncol + j];
-              if (dv != 0.0) gv[t] = __dadd_rn(gv[t], __dmul_rn(hv, dv));
-            }
+            gv[q][t] = (kok && j < ncol) ? a.g[k * a.m + j0 + j] : 0.0;
+          }
+        }
+        for (int p = 0; p < np; ++p) {
+          double dv[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int j = jb + lane + 32 * t;
+            dv[t] = j < ncol ? pend_d[p * ncol + j] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < kFR; ++q) {
+            const double hv = __shfl_sync(0xffffffffu, p < 32 ? hl0[q] : hl1[q], p & 31);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (dv[t] != 0.0) gv[q][t] = __dadd_rn(gv[q][t], __dmul_rn(hv, dv[t]));
           }
         }
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int j = jb + lane + 32 * t;
-          if (j < ncol) gk[j] = gv[t];
+        for (int q = 0; q < kFR; ++q) {
+          const long long k = k0 + q;
+          if (k >= a.n) continue;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int j = jb + lane + 32 * t;
+            if (j < ncol) a.g[k * a.m + j0 + j] = gv[q][t];
+          }
         }
       }
     }
@@ -458,13 +478,16 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
     obj = __dadd_rn(obj, r.delta);
     ++accepted;
     __syncthreads();
+    const unsigned long long tf = clk();
     if (npend == kPend) flush();
+    tph[5] += clk() - tf;
     load(i);
   };
   auto thr_of = [&] { return __dmul_rn(-a.tol, __dadd_rn(1.0, fabs(obj))); };  // jointq.cpp:183
   for (int pass = 0; pass < a.max_passes; ++pass) {
     const unsigned long long pk = (unsigned long long)pass << 58;
     int in_pass = 0;
+    unsigned long long tc0 = clk();
     // (A) scale refit of each row's group (jointq.cpp:205-210)
     for (long long i = 0; i < a.n; ++i) {
       const long long group = i * a.c.gpr + unit;
@@ -482,12 +505,15 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
       }
       __syncthreads();
     }
+    tph[0] += clk() - tc0;
+    tc0 = clk();
     // (B) code moves in row-major order, speculatively in parallel (jointq.cpp:211-230)
     for (long long i = 0; i < a.n; ++i) {
       const long long group = i * a.c.gpr + unit;
       load(i);
       int start = 0;  // first cell still to try
       while (start < ncol) {
+        const unsigned long long te = clk();
         if (tid == 0) r.best = 0x7fffffff;
         __syncthreads();
         const int z = a.zeros[group];
@@ -502,6 +528,8 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
         }
         __syncthreads();
         const int best = r.best;
+        tph[1] += clk() - te;
+        tph[4] += 1;
         if (best == 0x7fffffff) break;
         __syncthreads();
         if (tid == 0) {  // re-evaluate the winner for its (s, delta) (deterministic)
@@ -520,6 +548,8 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
       }
       __syncthreads();
     }
+    tph[2] += clk() - tc0;
+    tc0 = clk();
     // (C) zero-point moves (asymmetric; jointq.cpp:232-246)
     if (a.c.scheme == 1) {
       for (long long i = 0; i < a.n; ++i) {
@@ -546,6 +576,7 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
         __syncthreads();
       }
     }
+    tph[3] += clk() - tc0;
     if (in_pass == 0) {
       fz = pass;
       break;
@@ -554,6 +585,8 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
   if (tid == 0) {
     a.log_count[unit] = accepted;
     a.first_zero[unit] = fz;
+    if (a.prof && unit == 0)
+      for (int q = 0; q < 6; ++q) a.prof[q] = tph[q];
   }
 }
 
@@ -639,12 +672,25 @@ int jointq_search(const float* w, long long n, long long m, const QCfg& c, int16
   a.max_passes = max_passes, a.radius = radius, a.tol = 1e-10, a.obj0 = obj0;
   a.log_key = log_key, a.log_delta = log_delta, a.log_count = log_count, a.first_zero = first_zero;
   a.log_cap = log_cap;
+  static unsigned long long* prof = nullptr;
+  if (getenv("OCWG_DEBUG_JQ")) {
+    if (!prof) cudaMalloc(&prof, 6 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 6 * sizeof(unsigned long long), st);
+    a.prof = prof;
+  }
   const int units = int(jointq_units(c, m));
   if (c.gran == 2 && c.group <= kRowMax) {
     const int ncol = int(std::min<long long>(c.group, m));
     const size_t dyn = size_t(kPend) * ncol * sizeof(double);
     cudaFuncSetAttribute(jq_search_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
     jq_search_rows_kernel<<<units, 256, dyn, st>>>(a);
+    if (a.prof) {
+      unsigned long long h[6];
+      cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "jointq unit 0 Mcycles: A %.1f, B %.1f (evals %.1f in %llu rounds), C %.1f, flush %.1f\n",
+              h[0] / 1e6, h[2] / 1e6, h[1] / 1e6, h[4], h[3] / 1e6, h[5] / 1e6);
+    }
   } else {
     jq_search_kernel<<<units, 256, 0, st>>>(a);
   }
