@@ -951,7 +951,7 @@ int ocwg_jointq_refine(ocwg_ctx* ctx, const float* w, uint64_t n, uint64_t m, co
     std::vector<int> cnt(units, 0), fz(units, 0);
     std::vector<std::pair<unsigned long long, double>> moves;
     bool truncated = false;
-    if (n * m > 0 && max_passes > 0) {
+    if (n * m > 0) {
       Arena ar(ctx);
       const size_t ox = ar.reserve(std::max<uint64_t>(1, tokens * n) * 4), ow = ar.reserve(n * m * 4),
                    oc = ar.reserve(n * m * 2), os = ar.reserve(ng * 4), oz = ar.reserve(ng * 4),
@@ -980,13 +980,18 @@ int ocwg_jointq_refine(ocwg_ctx* ctx, const float* w, uint64_t n, uint64_t m, co
                           (long long)m, c, ar.at<int16_t>(oc), ar.at<float>(os), ar.at<int32_t>(oz),
                           lambda, ar.at<double>(oh), ar.at<double>(oe), ar.at<double>(og),
                           ar.at<double>(op), ctx->stream);
-      const int r = jointq_search(ar.at<float>(ow), (long long)n, (long long)m, c, ar.at<int16_t>(oc),
-                                  ar.at<float>(os), ar.at<int32_t>(oz), ar.at<double>(oh),
-                                  ar.at<double>(oe), ar.at<double>(og), ar.at<double>(odb), max_cells,
-                                  obj0, max_passes, move_radius, ar.at<unsigned long long>(olk),
-                                  ar.at<double>(old), ar.at<int>(olc), ar.at<int>(ofz), log_cap,
-                                  ctx->stream);
-      if (r != 0) fail(OCWG_CUDA_ERROR, "jointq_refine: search kernel launch failed");
+      if (max_passes > 0) {
+        const int r = jointq_search(ar.at<float>(ow), (long long)n, (long long)m, c,
+                                    ar.at<int16_t>(oc), ar.at<float>(os), ar.at<int32_t>(oz),
+                                    ar.at<double>(oh), ar.at<double>(oe), ar.at<double>(og),
+                                    ar.at<double>(odb), max_cells, obj0, max_passes, move_radius,
+                                    ar.at<unsigned long long>(olk), ar.at<double>(old),
+                                    ar.at<int>(olc), ar.at<int>(ofz), log_cap, ctx->stream);
+        if (r != 0) fail(OCWG_CUDA_ERROR, "jointq_refine: search kernel launch failed");
+      } else {
+        ck(cudaMemsetAsync(ar.at<int>(olc), 0, units * 4, ctx->stream), "memset");
+        ck(cudaMemsetAsync(ar.at<int>(ofz), 0, units * 4, ctx->stream), "memset");
+      }
       const auto t2 = tnow();
       if (dbg) fprintf(stderr, "jointq: setup + search %.1f ms\n", ms(t0, t2));
       d2h(codes, ar.at<int16_t>(oc), n * m * 2, ctx);
@@ -1024,8 +1029,9 @@ int ocwg_jointq_refine(ocwg_ctx* ctx, const float* w, uint64_t n, uint64_t m, co
     }
     if (accepted_moves) *accepted_moves = total;
     // jointq.cpp:248-250: a pass without an accepted move ends the search
-    if (passes) *passes = (n * m == 0 || max_passes <= 0) ? std::max(0, std::min(1, max_passes))
-                          : (fzmax < max_passes ? fzmax + 1 : max_passes);
+    if (passes) *passes = max_passes <= 0 ? 0
+                          : n * m == 0 ? 1
+                                       : (fzmax < max_passes ? fzmax + 1 : max_passes);
     // trace: J at entry, then after each accepted move (0 entries: move log overflowed)
     const uint64_t len = truncated ? 0 : total + 1;
     if (trace_len) *trace_len = len;

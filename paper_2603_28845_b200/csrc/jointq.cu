@@ -653,7 +653,10 @@ void jointq_residual(const int16_t* codes, const float* scales, const int32_t* z
 double jointq_setup(const float* x, long long tokens, const float* w, long long n, long long m,
                     const QCfg& c, const int16_t* codes, const float* scales, const int32_t* zeros,
                     double lambda, double* h, double* e, double* g, double* part, cudaStream_t st) {
-  gemm<double, float, float>(n, n, tokens, 1.0, x, n, true, x, n, false, 0.0, h, n, false, st);
+  if (tokens > 0)
+    gemm<double, float, float>(n, n, tokens, 1.0, x, n, true, x, n, false, 0.0, h, n, false, st);
+  else
+    cudaMemsetAsync(h, 0, size_t(n) * size_t(n) * sizeof(double), st);
   jq_add_diag_kernel<<<64, 256, 0, st>>>(h, n, double(tokens) * lambda);
   count_launches(1);
   jointq_residual(codes, scales, zeros, w, n, m, c, e, st);

@@ -129,3 +129,20 @@ def test_local_optimum_is_returned_unchanged(ref):
     assert res.accepted_moves == 0
     assert np.array_equal(res.refined.codes, c)
     assert res.objective_trace.shape == (1,)
+
+
+def test_refine_edge_cases_match_reference(ref):
+    """max_passes 0 (trace = the objective at entry), no calibration rows (H = 0)."""
+    w = ref.random_gaussian(16, 24, 61, 0.5)
+    x = ref.random_gaussian(20, 16, 62)
+    c, s, z = ref.quantize_matrix(w, 3, 1, 2, 8)
+    rc, rs, rz, rtrace, racc, rpass = ref.jointq_refine(c, s, z, w, x, 3, 1, 2, 8, 0.2, 0, 1)
+    res = g.jointq_refine(_gpu_q(c, s, z, 3, 1, 2, 8), w, x, g.JointqOptions(0.2, 0, 1))
+    assert (res.accepted_moves, res.passes) == (racc, rpass) == (0, 0)
+    np.testing.assert_allclose(res.objective_trace, rtrace, rtol=1e-10)
+    x0 = np.zeros((0, 16), np.float32)
+    rc, rs, rz, rtrace, racc, rpass = ref.jointq_refine(c, s, z, w, x0, 3, 1, 2, 8, 0.2, 4, 1)
+    res = g.jointq_refine(_gpu_q(c, s, z, 3, 1, 2, 8), w, x0, g.JointqOptions(0.2, 4, 1))
+    assert (res.accepted_moves, res.passes) == (racc, rpass)
+    assert np.array_equal(res.refined.codes, rc)
+    np.testing.assert_allclose(res.objective_trace, rtrace, rtol=1e-9, atol=1e-12)
