@@ -321,7 +321,13 @@ struct RowSm {
 };
 
 // one proposal: code cp at column jp (jp < 0: none), zero point z
-__device__ bool eval_row_prop(const RowSm& r, int ncol, int jp, int cp, int z, double thr, float& s_out,
+struct RowView {  // a row's cells in shared memory
+  const double *g, *e;
+  const float* w;
+  const int* c;
+  double hii;
+};
+__device__ bool eval_row_prop(const RowView& r, int ncol, int jp, int cp, int z, double thr, float& s_out,
                               double& delta_out) {
   // (branch-free: a skipped cell keeps the running sums by selection, so the
   // loads and products of the next cells issue ahead of the add chains)
@@ -364,18 +370,27 @@ __device__ bool eval_row_prop(const RowSm& r, int ncol, int jp, int cp, int z, d
 // then add), so the values are those of the per-move update (jointq.cpp:142)
 // with 1 / kPend of its memory traffic.
 constexpr int kPend = 48;
+constexpr int kSpec = 16;  // rows per speculative refit round (phases A and C)
 __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
   __shared__ RowSm r;
   __shared__ int pend_i[kPend];
   __shared__ double pend_h[kPend];  // h(i, i_p) of the row being loaded
   __shared__ int npend;
-  extern __shared__ double pend_d[];  // [kPend][ncol]
+  extern __shared__ double pend_d[];  // [kPend][ncol], then the speculative rows below
   const int unit = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const long long j0 = (long long)unit * a.c.group, j1 = min(a.m, j0 + a.c.group);
   const int ncol = int(j1 - j0);
   const int nd = 2 * a.radius;  // code deltas per cell: -1, +1, -2, +2, ...
   double obj = a.obj0;
   int accepted = 0, fz = a.max_passes;
+  // kSpec rows for the speculative refits (phases A and C): g, e, w, codes, h_ii,
+  // h(i, i_p) of the pending moves
+  double* sp_g = pend_d + kPend * ncol;
+  double* sp_e = sp_g + kSpec * ncol;
+  double* sp_ph = sp_e + kSpec * ncol;  // [kSpec][kPend]
+  double* sp_h = sp_ph + kSpec * kPend;
+  float* sp_w = reinterpret_cast<float*>(sp_h + kSpec);
+  int* sp_c = reinterpret_cast<int*>(sp_w + kSpec * ncol);
   if (tid == 0) npend = 0;
   __syncthreads();
   unsigned long long tph[6] = {0, 0, 0, 0, 0, 0};  // debug timers: A, B evals, B, C, rounds, flush
@@ -398,6 +413,33 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
     }
     if (tid == 0) r.hii = a.h[i * a.n + i];
     __syncthreads();
+  };
+  // rows i0 .. i0+R-1 into the speculative buffers (G materialised like load())
+  auto load_spec = [&](long long i0, int R) {
+    const int np = npend;
+    for (int e = tid; e < R * kPend; e += nt) {
+      const int q = e / kPend, p = e % kPend;
+      if (p < np) sp_ph[q * kPend + p] = a.h[(i0 + q) * a.n + pend_i[p]];
+    }
+    if (tid < R) sp_h[tid] = a.h[(i0 + tid) * a.n + i0 + tid];
+    __syncthreads();
+    for (int e = tid; e < R * ncol; e += nt) {
+      const int q = e / ncol, j = e % ncol;
+      const long long o = (i0 + q) * a.m + j0 + j;
+      double gv = a.g[o];
+      for (int p = 0; p < np; ++p) {
+        const double dv = pend_d[p * ncol + j];
+        if (dv != 0.0) gv = __dadd_rn(gv, __dmul_rn(sp_ph[q * kPend + p], dv));
+      }
+      sp_g[q * ncol + j] = gv;
+      sp_e[q * ncol + j] = a.e[o];
+      sp_w[q * ncol + j] = a.w[o];
+      sp_c[q * ncol + j] = a.codes[o];
+    }
+    __syncthreads();
+  };
+  auto spec_view = [&](int q) {
+    return RowView{sp_g + q * ncol, sp_e + q * ncol, sp_w + q * ncol, sp_c + q * ncol, sp_h[q]};
   };
   auto flush = [&] {  // G[:, block] += the pending moves, in order
     // a warp takes kFR rows at a time: 4 kFR independent add chains per lane
@@ -484,18 +526,21 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
     load(i);
   };
   auto thr_of = [&] { return __dmul_rn(-a.tol, __dadd_rn(1.0, fabs(obj))); };  // jointq.cpp:183
+  auto rowv = [&] { return RowView{r.g, r.e, r.w, r.c, r.hii}; };
   for (int pass = 0; pass < a.max_passes; ++pass) {
     const unsigned long long pk = (unsigned long long)pass << 58;
     int in_pass = 0;
     unsigned long long tc0 = clk();
-    // (A) scale refit of each row's group (jointq.cpp:205-210)
+    // (A) scale refit of each row's group (jointq.cpp:205-210), one row at a time:
+    // refits are accepted often, so evaluating rows ahead mostly repeats work
+    // (measured: kSpec-row rounds took phase A from 1.5 to 2.5 G cycles at C2)
     for (long long i = 0; i < a.n; ++i) {
       const long long group = i * a.c.gpr + unit;
       load(i);
       if (tid == 0) {
         float s;
         double dl;
-        r.best = eval_row_prop(r, ncol, -1, 0, a.zeros[group], thr_of(), s, dl) ? 0 : -1;
+        r.best = eval_row_prop(rowv(), ncol, -1, 0, a.zeros[group], thr_of(), s, dl) ? 0 : -1;
         r.s = s, r.delta = dl, r.jp = -1, r.cp = 0, r.z = a.zeros[group];
       }
       __syncthreads();
@@ -524,7 +569,7 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
           if (cp < a.c.qmin || cp > a.c.qmax) continue;
           float s;
           double dl;
-          if (eval_row_prop(r, ncol, jp, cp, z, thr, s, dl)) atomicMin(&r.best, k);
+          if (eval_row_prop(rowv(), ncol, jp, cp, z, thr, s, dl)) atomicMin(&r.best, k);
         }
         __syncthreads();
         const int best = r.best;
@@ -537,7 +582,7 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
           const int cp = r.c[jp] + ((di & 1) ? 1 : -1) * (di / 2 + 1);
           float s;
           double dl;
-          eval_row_prop(r, ncol, jp, cp, z, thr, s, dl);
+          eval_row_prop(rowv(), ncol, jp, cp, z, thr, s, dl);
           r.s = s, r.delta = dl, r.jp = jp, r.cp = cp, r.z = z;
         }
         __syncthreads();
@@ -552,28 +597,43 @@ __global__ void __launch_bounds__(256) jq_search_rows_kernel(JqArgs a) {
     tc0 = clk();
     // (C) zero-point moves (asymmetric; jointq.cpp:232-246)
     if (a.c.scheme == 1) {
-      for (long long i = 0; i < a.n; ++i) {
-        const long long group = i * a.c.gpr + unit;
+      // kSpec rows x (z - 1, z + 1) at a time, first accepted in the reference's order
+      // (zero moves are rarely accepted: C2 phase C 0.86 -> 0.13 G cycles)
+      for (long long i0 = 0; i0 < a.n;) {
+        const int R = int(min((long long)kSpec, a.n - i0));
+        load_spec(i0, R);
+        if (tid == 0) r.best = 0x7fffffff;
+        __syncthreads();
+        const double thr = thr_of();
+        if (tid < 2 * R) {
+          const int q = tid >> 1, dz = (tid & 1) ? 1 : -1;
+          const long long group = (i0 + q) * a.c.gpr + unit;
+          const int z_new = a.zeros[group] + dz;
+          float s;
+          double dl;
+          if (z_new >= a.c.qmin && z_new <= a.c.qmax &&
+              eval_row_prop(spec_view(q), ncol, -1, 0, z_new, thr, s, dl))
+            atomicMin(&r.best, tid);
+        }
+        __syncthreads();
+        const int best = r.best;
+        if (best == 0x7fffffff) {
+          i0 += R;
+          continue;
+        }
+        const long long i = i0 + (best >> 1), group = i * a.c.gpr + unit;
+        const int z_new = a.zeros[group] + ((best & 1) ? 1 : -1);
         load(i);
         if (tid == 0) {
-          r.best = -1;
-          for (int dz = -1; dz <= 1 && r.best < 0; dz += 2) {
-            const int z_new = a.zeros[group] + dz;
-            if (z_new < a.c.qmin || z_new > a.c.qmax) continue;
-            float s;
-            double dl;
-            if (eval_row_prop(r, ncol, -1, 0, z_new, thr_of(), s, dl)) {
-              r.best = 0;
-              r.s = s, r.delta = dl, r.jp = -1, r.cp = 0, r.z = z_new;
-            }
-          }
+          float s;
+          double dl;
+          eval_row_prop(rowv(), ncol, -1, 0, z_new, thr, s, dl);
+          r.s = s, r.delta = dl, r.jp = -1, r.cp = 0, r.z = z_new;
         }
         __syncthreads();
-        if (r.best == 0) {
-          apply(i, group, pk | (2ull << 56) | (unsigned long long)group);
-          ++in_pass;
-        }
-        __syncthreads();
+        apply(i, group, pk | (2ull << 56) | (unsigned long long)group);
+        ++in_pass;
+        i0 = i + 1;
       }
     }
     tph[3] += clk() - tc0;
@@ -684,7 +744,9 @@ int jointq_search(const float* w, long long n, long long m, const QCfg& c, int16
   const int units = int(jointq_units(c, m));
   if (c.gran == 2 && c.group <= kRowMax) {
     const int ncol = int(std::min<long long>(c.group, m));
-    const size_t dyn = size_t(kPend) * ncol * sizeof(double);
+    const size_t dyn = size_t(kPend) * ncol * sizeof(double) +                 // pending d
+                       size_t(kSpec) * ncol * (2 * sizeof(double) + sizeof(float) + sizeof(int)) +
+                       size_t(kSpec) * (kPend + 1) * sizeof(double);            // h(i, i_p), h_ii
     cudaFuncSetAttribute(jq_search_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
     jq_search_rows_kernel<<<units, 256, dyn, st>>>(a);
     if (a.prof) {
