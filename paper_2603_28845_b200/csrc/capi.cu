@@ -465,9 +465,13 @@ void run_factor_t(ocwg_ctx* ctx, const float* h_dev, uint64_t n, int actorder, d
                   const GptqBufs& b) {
   cudaStream_t st = ctx->stream;
   set_tc_workspace(ctx->tensor_core_gemm ? b.tcws : nullptr, b.tcws_floats);
-  launch_order(h_dev, (long long)n, actorder, b.order, st);
+  // damp first, leaving a contiguous diag(H) in the factor-input buffer (the
+  // build below overwrites it) so the act-order rank count reads it coalesced
+  float* diag = actorder ? static_cast<float*>(b.a) : nullptr;
+  launch_damp(h_dev, (long long)n, percdamp, b.damp, diag, st);
+  launch_order(diag, (long long)n, actorder, b.order, st);
   launch_build_factor_input<T>(h_dev, (long long)n, b.order, percdamp, static_cast<T*>(b.a), b.damp,
-                               st);
+                               st, /*damp_ready=*/true);
   if (ctx->profile) cudaEventRecord(ctx->ev[1], st);
   cholesky_g<T>(static_cast<T*>(b.a), (long long)n, static_cast<T*>(b.ghi), b.glo,
                 b.glo ? static_cast<float*>(b.gpl) : nullptr, b.gtt, b.flags, ctx->flag,
@@ -1440,10 +1444,15 @@ int ocwg_gptq_order(ocwg_ctx* ctx, const float* h, uint64_t n, int actorder, int
     std::lock_guard<std::mutex> lk(ctx->mu);
     begin(ctx);
     Arena ar(ctx);
-    const size_t oh = ar.reserve(n * n * 4), oo = ar.reserve(n * 4);
+    const size_t oh = ar.reserve(n * n * 4), oo = ar.reserve(n * 4), od = ar.reserve(n * 4);
     ar.commit();
     h2d(ar.at<float>(oh), h, n * n * 4, ctx);
-    if (n) launch_order(ar.at<float>(oh), (long long)n, actorder, ar.at<int32_t>(oo), ctx->stream);
+    if (n) {
+      float* diag = ar.at<float>(od);  // diag(H), contiguous
+      ck(cudaMemcpy2DAsync(diag, 4, ar.at<float>(oh), (n + 1) * 4, 4, n, cudaMemcpyDeviceToDevice,
+                           ctx->stream), "diag copy");
+      launch_order(diag, (long long)n, actorder, ar.at<int32_t>(oo), ctx->stream);
+    }
     std::vector<int32_t> o(n);
     d2h(o.data(), ar.at<int32_t>(oo), n * 4, ctx);
     finish(ctx);

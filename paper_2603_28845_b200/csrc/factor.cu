@@ -90,10 +90,14 @@ __global__ void __launch_bounds__(256) build_input_rows_kernel(const float* __re
 
 // damp = percdamp * mean(diag(fp64 H))  (layerwise.cpp:32-33)
 __global__ void damp_kernel(const float* __restrict__ h, long long n, double percdamp,
-                            double* damp) {
+                            double* damp, float* __restrict__ diag) {
   __shared__ double part[32];
   double s = 0.0;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) s += double(h[i * n + i]);
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const float v = h[i * n + i];
+    if (diag) diag[i] = v;
+    s += double(v);
+  }
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
   __syncthreads();
@@ -1474,11 +1478,17 @@ size_t cholesky_flag_ints(long long n) {
   return size_t(nt * nt + 2 * nt + 2 * nt + 8 + nt * nt);
 }
 
+void launch_damp(const float* h, long long n, double percdamp, double* damp, float* diag,
+                 cudaStream_t st) {
+  count_launches(1);
+  damp_kernel<<<1, 1024, 0, st>>>(h, n, percdamp, damp, diag);
+}
+
 template <typename T>
 void launch_build_factor_input(const float* h, long long n, const int32_t* order, double percdamp,
-                               T* a, double* damp, cudaStream_t st) {
-  count_launches(2);
-  damp_kernel<<<1, 1024, 0, st>>>(h, n, percdamp, damp);
+                               T* a, double* damp, cudaStream_t st, bool damp_ready) {
+  if (!damp_ready) launch_damp(h, n, percdamp, damp, nullptr, st);
+  count_launches(1);
   const size_t row_bytes = size_t(n) * sizeof(float);
   if (row_bytes <= 200 * 1024) {
     cudaFuncSetAttribute(build_input_rows_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1624,9 +1634,9 @@ void launch_gram_upper(const T* u, long long n, double* hinv, cudaStream_t st) {
 }
 
 template void launch_build_factor_input<float>(const float*, long long, const int32_t*, double,
-                                               float*, double*, cudaStream_t);
+                                               float*, double*, cudaStream_t, bool);
 template void launch_build_factor_input<double>(const float*, long long, const int32_t*, double,
-                                                double*, double*, cudaStream_t);
+                                                double*, double*, cudaStream_t, bool);
 template void cholesky_g<float>(float*, long long, float*, float*, float*, float*, int*,
                                 unsigned*, long long, cudaStream_t, float*, float*);
 template void cholesky_g<double>(double*, long long, double*, float*, float*, float*, int*,

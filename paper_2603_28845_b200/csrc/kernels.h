@@ -43,8 +43,9 @@ void launch_pack(const int16_t* codes, long long n_codes, long long n_groups, co
                  const float* scales, const int32_t* zeros, uint8_t* out, cudaStream_t st);
 void launch_unpack(const uint8_t* payload, long long n_codes, long long n_groups, const QCfg& c,
                    int16_t* codes, float* scales, int32_t* zeros, cudaStream_t st);
-// act-order: stable descending sort of diag(H) (layerwise.cpp:11-18)
-void launch_order(const float* h, long long n, int actorder, int32_t* order, cudaStream_t st);
+// act-order: stable descending sort of diag(H) (layerwise.cpp:11-18); `diag`
+// is a contiguous copy of diag(H) (launch_damp writes one; unused without act-order)
+void launch_order(const float* diag, long long n, int actorder, int32_t* order, cudaStream_t st);
 // AutoBit candidate grid (autobit.cpp:45-61): out[14] = RTN errors of bits
 // {2..8} x {per_group 128, per_channel}, symmetric; partial: rows x 14 doubles
 void launch_candidate_grid(const float* w, long long rows, long long cols, long long ld, int act,
@@ -54,10 +55,16 @@ void launch_candidate_grid(const float* w, long long rows, long long cols, long 
 // ---- factorisation (factor.cu), T = float (default) or double ---------------
 // A = reversed-permuted, dampened copy of H (layerwise.cpp:31-41):
 //   A[i][j] = T(double(H[o(i)][o(j)]) + (i==j) * damp),  o(i) = order[n-1-i]
-// damp = percdamp * mean(diag(double(H))) computed on device into *damp.
+// damp = percdamp * mean(diag(double(H))) computed on device into *damp
+// (layerwise.cpp:32-33); with diag != nullptr the kernel also stores diag(H)
+// there contiguously (n floats) for launch_order.
+void launch_damp(const float* h, long long n, double percdamp, double* damp, float* diag,
+                 cudaStream_t st);
+// damp_ready: *damp was already written by launch_damp on the same stream.
 template <typename T>
 void launch_build_factor_input(const float* h, long long n, const int32_t* order,
-                               double percdamp, T* a, double* damp, cudaStream_t st);
+                               double percdamp, T* a, double* damp, cudaStream_t st,
+                               bool damp_ready = false);
 // In-place lower Cholesky A = L L^T (n x n row-major, lower used) by the
 // persistent tile-dataflow kernel, over macro panels of `macro_cols` columns
 // (<= 0: one panel) with a trailing SYRK (mm<T>) between panels.  Emits

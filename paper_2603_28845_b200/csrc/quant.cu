@@ -374,31 +374,36 @@ __global__ void unpack_meta_kernel(const uint8_t* __restrict__ meta, long long n
 }
 
 // Stable descending rank of diag(H): rank_i = #{j: d_j > d_i} + #{j < i: d_j == d_i}.
-// O(n^2) comparisons: 8 threads per row i split the j range (diag tiles staged
-// in shared memory), then a shuffle reduction; bit-exact with
-// std::stable_sort(order, h[a][a] > h[b][b]) for NaN-free diagonals.
-constexpr int kOrdThreads = 256, kOrdSplit = 8, kOrdTile = 8192;
-__global__ void __launch_bounds__(kOrdThreads) order_rank_kernel(const float* __restrict__ h,
-                                                                 long long n, int32_t* order) {
+// O(n^2) comparisons: kSplit threads per row i split the j range (diag tiles
+// staged in shared memory), then a shuffle reduction; bit-exact with
+// std::stable_sort(order, h[a][a] > h[b][b]) for NaN-free diagonals.  The diag
+// is read at stride `ds` from `d` (a contiguous copy of diag(H), ds = 1: the
+// factor path's damp kernel leaves it beside the factor input).
+constexpr int kOrdThreads = 256, kOrdTile = 8192;
+template <int kSplit>
+__global__ void __launch_bounds__(kOrdThreads) order_rank_kernel(const float* __restrict__ d,
+                                                                 long long ds, long long n,
+                                                                 int32_t* order) {
   __shared__ float tile[kOrdTile];
-  const int part = threadIdx.x % kOrdSplit;
-  const long long i = (long long)blockIdx.x * (kOrdThreads / kOrdSplit) + threadIdx.x / kOrdSplit;
-  const float di = i < n ? h[i * n + i] : 0.0f;
+  const int part = threadIdx.x % kSplit;
+  const long long i = (long long)blockIdx.x * (kOrdThreads / kSplit) + threadIdx.x / kSplit;
+  const float di = i < n ? d[i * ds] : 0.0f;
   long long rank = 0;
   for (long long j0 = 0; j0 < n; j0 += kOrdTile) {
     const int cnt = int(min((long long)kOrdTile, n - j0));
     __syncthreads();
-    for (int t = threadIdx.x; t < cnt; t += kOrdThreads) tile[t] = h[(j0 + t) * (n + 1)];
+    for (int t = threadIdx.x; t < cnt; t += kOrdThreads) tile[t] = d[(j0 + t) * ds];
     __syncthreads();
     const long long lim = i - j0;  // t < lim  <=>  j0 + t < i
     int cnt_r = 0;
-    for (int t = part; t < cnt; t += kOrdSplit) {
+#pragma unroll 4
+    for (int t = part; t < cnt; t += kSplit) {
       const float dj = tile[t];
       cnt_r += (dj > di) | ((dj == di) & (t < lim));
     }
     rank += cnt_r;
   }
-  for (int o = 1; o < kOrdSplit; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+  for (int o = 1; o < kSplit; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
   if (part == 0 && i < n) order[rank] = int32_t(i);
 }
 
@@ -491,15 +496,15 @@ void launch_unpack(const uint8_t* payload, long long n_codes, long long n_groups
                                                                c.scheme == 1, scales, zeros);
 }
 
-void launch_order(const float* h, long long n, int actorder, int32_t* order, cudaStream_t st) {
+void launch_order(const float* diag, long long n, int actorder, int32_t* order, cudaStream_t st) {
   count_launches(1);
   if (!actorder) {
     iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, order);
     return;
   }
-  const long long rows_per_cta = kOrdThreads / kOrdSplit;
-  order_rank_kernel<<<int((n + rows_per_cta - 1) / rows_per_cta), kOrdThreads, 0, st>>>(h, n,
-                                                                                      order);
+  constexpr int split = 16;  // threads per row; diag tiles staged coalesced
+  constexpr long long rows = kOrdThreads / split;
+  order_rank_kernel<split><<<int((n + rows - 1) / rows), kOrdThreads, 0, st>>>(diag, 1, n, order);
 }
 
 // ---- AutoBit's default candidate grid (autobit.cpp:45-61, estimate_error
