@@ -138,13 +138,15 @@ __global__ void __launch_bounds__(256) gemm_kernel(long long m, long long n, lon
 }
 
 // fp64 on the tensor cores (DMMA, mma.sync m8n8k4 .f64 -- tcgen05 has no fp64
-// kind): 128 x 128 CTA tile, BK 16, 16 warps as 4 x 4, each warp a 32 x 32
-// block = 4 x 4 m8n8 accumulators (32 doubles per lane, no spills at 512
-// threads).  Operands are staged through registers (any transposition, fp32
+// kind): 128 x 128 CTA tile, BK 16, 32 warps as 4 x 8, each warp a 32 x 16
+// block = 4 x 2 m8n8 accumulators (16 doubles per lane).  The kernel is
+// latency bound: 32 warps beat 16 warps of 32 x 32 (5-15 % on the factor and
+// sweep shapes, equal on square 4096) and 8 warps of 64 x 32 (-12 %), see
+// profiles/r02_dmma_threads_ab.log.  Operands are staged through registers (any transposition, fp32
 // inputs widened exactly) into double-buffered shared tiles stored [row][k]
 // for A and [col][k] for B, so a fragment is one 8-byte load per lane; the row
 // stride of 20 doubles puts a half-warp's fragment loads on distinct banks.
-constexpr int DBM = 128, DBN = 128, DBK = 16, DPAD = 4, DTHREADS = 512;
+constexpr int DBM = 128, DBN = 128, DBK = 16, DPAD = 4, DTHREADS = 1024;
 constexpr int kDmmaSmem = 2 * (DBM + DBN) * (DBK + DPAD) * 8;
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
@@ -171,7 +173,8 @@ __global__ void __launch_bounds__(DTHREADS, 1) gemm_f64_dmma_kernel(
   double (*Bs)[DBN][DBK + DPAD] =
       reinterpret_cast<double (*)[DBN][DBK + DPAD]>(dsm + 2 * DBM * (DBK + DPAD));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  constexpr int WN = 16, NJ = WN / 8;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * WN;
   constexpr int LA = DBM * DBK / DTHREADS, LB = DBN * DBK / DTHREADS;
   double ra[LA], rb[LB];
   auto load = [&](long long k0) {
@@ -206,11 +209,11 @@ __global__ void __launch_bounds__(DTHREADS, 1) gemm_f64_dmma_kernel(
       Bs[buf][j][kk] = rb[q];
     }
   };
-  double acc[4][4][2];
+  double acc[4][NJ][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const long long nk = kend > kbeg ? (kend - kbeg + DBK - 1) / DBK : 0;
   if (nk > 0) {
     load(kbeg);
@@ -223,15 +226,15 @@ __global__ void __launch_bounds__(DTHREADS, 1) gemm_f64_dmma_kernel(
     if (kt + 1 < nk) load(kbeg + (kt + 1) * DBK);
 #pragma unroll
     for (int kq = 0; kq < DBK; kq += 4) {
-      double av[4], bv[4];
+      double av[4], bv[NJ];
 #pragma unroll
       for (int i = 0; i < 4; ++i) av[i] = As[buf][wm + 8 * i + fr][kq + fk];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][wn + 8 * j + fr][kq + fk];
+      for (int j = 0; j < NJ; ++j) bv[j] = Bs[buf][wn + 8 * j + fr][kq + fk];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], av[i], bv[j]);
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], av[i], bv[j]);
     }
     if (kt + 1 < nk) store(buf ^ 1);
     __syncthreads();
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) gemm_f64_dmma_kernel(
     const long long gi = row0 + wm + 8 * i + fr;
     if (gi >= m) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const long long gj = col0 + wn + 8 * j + 2 * fk + e;
